@@ -1,0 +1,336 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A C-ABI shim over the UNMODIFIED reference library, compiled by
+// oracle/Makefile from the sources where they lie under
+// /root/reference/proj/src into oracle/_ref/libsemd_ref.so. It lets the
+// Python tests and the bench's CPU-baseline leg call the reference itself.
+// It also holds the trace replayer: the extract_imf loop (emd.cpp:127-153)
+// re-driven through the reference's public find_extrema / envelope so that
+// every find_extrema call's extrema lists can be hashed; ref_emd_traced checks
+// its own output against semd::emd bit-for-bit and reports any divergence.
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "semd/emd.hpp"
+#include "semd/serialize.hpp"
+#include "semd/synth.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct TraceRec {
+    int32_t task, m, k, iter;
+    uint32_t n_max, n_min;
+    uint64_t hash;
+};
+
+uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+uint64_t hash_extrema(const semd::Extrema& e) {
+    uint64_t h = 0;
+    for (std::size_t j = 0; j < e.max_idx.size(); ++j) h += mix64((uint64_t(j) << 32) ^ uint64_t(e.max_idx[j]));
+    for (std::size_t j = 0; j < e.min_idx.size(); ++j)
+        h += mix64(0x8000000000000000ULL ^ (uint64_t(j) << 32) ^ uint64_t(e.min_idx[j]));
+    return h;
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const semd::InsufficientExtrema& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const semd::InvalidInput& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 4;
+    }
+}
+
+struct Out {
+    std::vector<double> imfs;  // K x n
+    std::vector<double> residue;
+    std::vector<int32_t> counts;
+    std::vector<TraceRec> trace;
+    std::size_t K = 0;
+};
+
+void store(Out* o, const semd::Decomposition& d) {
+    o->K = d.imfs.size();
+    const std::size_t n = d.residue.size();
+    o->imfs.resize(o->K * n);
+    for (std::size_t k = 0; k < o->K; ++k) std::memcpy(o->imfs.data() + k * n, d.imfs[k].data(), n * 8);
+    o->residue = d.residue;
+}
+
+// The replayer: emd.cpp:127-153 through the public API, with per-call traces.
+semd::SiftResult replay_extract(const semd::Signal& x, const semd::SiftConfig& cfg, std::vector<TraceRec>* tr,
+                                int task, int m, int k) {
+    semd::SiftResult res{x, 0};
+    semd::Signal& cur = res.imf;
+    for (int iter = 0; iter < cfg.max_sift_iters; ++iter) {
+        semd::Extrema ext = semd::find_extrema(cur);
+        tr->push_back({task, m, k, iter, uint32_t(ext.max_idx.size()), uint32_t(ext.min_idx.size()), hash_extrema(ext)});
+        semd::Signal upper, lower;
+        try {
+            upper = semd::envelope(ext.max_idx, ext.max_val, cur.size());
+            lower = semd::envelope(ext.min_idx, ext.min_val, cur.size());
+        } catch (const semd::InsufficientExtrema&) {
+            if (res.sift_count == 0) throw;
+            return res;
+        }
+        double num = 0.0, den = 0.0;
+        for (std::size_t i = 0; i < cur.size(); ++i) {
+            const double mean = 0.5 * (upper[i] + lower[i]);
+            num += mean * mean;
+            den += cur[i] * cur[i];
+            cur[i] -= mean;
+        }
+        ++res.sift_count;
+        if (den == 0.0 || num / den < cfg.sd_threshold) return res;
+    }
+    return res;
+}
+
+semd::Decomposition replay_emd(const semd::Signal& x, const semd::SiftConfig& cfg, std::vector<TraceRec>* tr,
+                               std::vector<int32_t>* counts, int m) {
+    if (x.size() < 4) throw semd::InvalidInput("emd: signal too short (need at least 4 samples)");
+    semd::Decomposition d;
+    semd::Signal residue = x;
+    while (cfg.max_imfs == 0 || d.imfs.size() < std::size_t(cfg.max_imfs)) {
+        semd::SiftResult r;
+        try {
+            r = replay_extract(residue, cfg, tr, 0, m, int(d.imfs.size()));
+        } catch (const semd::InsufficientExtrema&) {
+            break;
+        }
+        for (std::size_t i = 0; i < residue.size(); ++i) residue[i] -= r.imf[i];
+        if (counts) counts->push_back(r.sift_count);
+        d.imfs.push_back(std::move(r.imf));
+    }
+    d.residue = std::move(residue);
+    return d;
+}
+
+bool same(const semd::Decomposition& a, const semd::Decomposition& b) {
+    if (a.imfs.size() != b.imfs.size()) return false;
+    for (std::size_t k = 0; k < a.imfs.size(); ++k)
+        if (a.imfs[k] != b.imfs[k]) return false;
+    return a.residue == b.residue;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void* ref_out_new() { return new Out(); }
+void ref_out_free(void* o) { delete static_cast<Out*>(o); }
+std::size_t ref_out_K(void* o) { return static_cast<Out*>(o)->K; }
+const double* ref_out_imfs(void* o) { return static_cast<Out*>(o)->imfs.data(); }
+const double* ref_out_residue(void* o) { return static_cast<Out*>(o)->residue.data(); }
+std::size_t ref_out_ncounts(void* o) { return static_cast<Out*>(o)->counts.size(); }
+const int32_t* ref_out_counts(void* o) { return static_cast<Out*>(o)->counts.data(); }
+std::size_t ref_out_ntrace(void* o) { return static_cast<Out*>(o)->trace.size(); }
+const void* ref_out_trace(void* o) { return static_cast<Out*>(o)->trace.data(); }
+
+uint64_t ref_derive_seed(uint64_t base, uint64_t index) { return semd::derive_seed(base, index); }
+
+void ref_mt19937_64(uint64_t seed, std::size_t n, uint64_t* out) {
+    std::mt19937_64 g(seed);
+    for (std::size_t i = 0; i < n; ++i) out[i] = g();
+}
+
+int ref_white_noise(std::size_t n, uint64_t seed, double std, double* out) {
+    return guard([&] {
+        const semd::Signal w = semd::white_noise(n, seed, std);
+        std::memcpy(out, w.data(), n * 8);
+    });
+}
+
+double ref_signal_std(const double* x, std::size_t n) { return semd::signal_std(semd::Signal(x, x + n)); }
+
+int ref_find_extrema(const double* x, std::size_t n, std::size_t* max_idx, double* max_val, std::size_t* n_max,
+                     std::size_t* min_idx, double* min_val, std::size_t* n_min) {
+    return guard([&] {
+        const semd::Extrema e = semd::find_extrema(semd::Signal(x, x + n));
+        *n_max = e.max_idx.size();
+        *n_min = e.min_idx.size();
+        std::memcpy(max_idx, e.max_idx.data(), *n_max * sizeof(std::size_t));
+        std::memcpy(max_val, e.max_val.data(), *n_max * 8);
+        std::memcpy(min_idx, e.min_idx.data(), *n_min * sizeof(std::size_t));
+        std::memcpy(min_val, e.min_val.data(), *n_min * 8);
+    });
+}
+
+int ref_envelope(const std::size_t* idx, const double* val, std::size_t n, std::size_t length, double* out) {
+    return guard([&] {
+        const semd::Signal e = semd::envelope(std::vector<std::size_t>(idx, idx + n), semd::Signal(val, val + n), length);
+        std::memcpy(out, e.data(), length * 8);
+    });
+}
+
+int ref_extract_imf(const double* x, std::size_t n, double sd, int iters, int imfs, double* out, int32_t* count) {
+    return guard([&] {
+        const semd::SiftResult r = semd::extract_imf(semd::Signal(x, x + n), {sd, iters, imfs});
+        std::memcpy(out, r.imf.data(), n * 8);
+        *count = r.sift_count;
+    });
+}
+
+// The reference's own decompose (algo 0/1/2), bit-for-bit its output.
+int ref_decompose(const double* x, std::size_t n, int algo, double sd, int iters, int imfs, double nstd, int nr,
+                  uint64_t seed, void* out) {
+    return guard([&] {
+        const semd::Decomposition d = semd::decompose(semd::Signal(x, x + n), static_cast<semd::Algorithm>(algo),
+                                                      {sd, iters, imfs}, {nstd, nr, seed});
+        store(static_cast<Out*>(out), d);
+    });
+}
+
+// EMD via the replayer; returns 3 if the replay is not bit-identical to semd::emd.
+int ref_emd_traced(const double* x, std::size_t n, double sd, int iters, int imfs, void* out) {
+    int mismatch = 0;
+    int rc = guard([&] {
+        Out* o = static_cast<Out*>(out);
+        const semd::Signal s(x, x + n);
+        const semd::SiftConfig cfg{sd, iters, imfs};
+        const semd::Decomposition d = replay_emd(s, cfg, &o->trace, &o->counts, 0);
+        if (!same(d, semd::emd(s, cfg))) mismatch = 1;
+        store(o, d);
+    });
+    if (rc == 0 && mismatch) {
+        g_err = "replay diverged from semd::emd";
+        return 3;
+    }
+    return rc;
+}
+
+// EEMD realizations [m_begin, m_end) through the replayer (per-realization
+// traces and sift counts; counts are concatenated in realization order), with
+// the per-realization emd checked against semd::emd. Sums are unscaled.
+int ref_eemd_traced(const double* x, std::size_t n, double sd, int iters, int imfs, double nstd, int nr,
+                    uint64_t seed, int m_begin, int m_end, void* out) {
+    int mismatch = 0;
+    int rc = guard([&] {
+        Out* o = static_cast<Out*>(out);
+        const semd::Signal s(x, x + n);
+        const semd::SiftConfig cfg{sd, iters, imfs};
+        if (nr < 1) throw semd::InvalidInput("ensemble: nr must be at least 1");
+        const double beta = nstd * semd::signal_std(s);
+        std::vector<semd::Signal> sums;
+        for (int m = m_begin; m < m_end; ++m) {
+            const semd::Signal w = semd::white_noise(n, semd::derive_seed(seed, std::uint64_t(m)));
+            semd::Signal xm(n);
+            for (std::size_t i = 0; i < n; ++i) xm[i] = s[i] + beta * w[i];
+            std::vector<int32_t> counts;
+            const semd::Decomposition d = replay_emd(xm, cfg, &o->trace, &counts, m);
+            if (!same(d, semd::emd(xm, cfg))) mismatch = 1;
+            o->counts.push_back(int32_t(d.imfs.size()));  // K_m, then its sift counts
+            o->counts.insert(o->counts.end(), counts.begin(), counts.end());
+            while (sums.size() < d.imfs.size()) sums.emplace_back(n, 0.0);
+            for (std::size_t k = 0; k < d.imfs.size(); ++k)
+                for (std::size_t i = 0; i < n; ++i) sums[k][i] += d.imfs[k][i];
+        }
+        o->K = sums.size();
+        o->imfs.resize(o->K * n);
+        for (std::size_t k = 0; k < o->K; ++k) std::memcpy(o->imfs.data() + k * n, sums[k].data(), n * 8);
+        o->residue.assign(n, 0.0);
+    });
+    if (rc == 0 && mismatch) {
+        g_err = "replay diverged from semd::emd";
+        return 3;
+    }
+    return rc;
+}
+
+// All-core realization-parallel reference EEMD work (the CPU baseline of
+// BASELINE.md): realizations [m_begin, m_begin+count) of x + beta*w_m, each
+// decomposed by the reference's own semd::emd, on `threads` threads. This is
+// exactly eemd()'s per-realization work (emd.cpp:237-244) without its
+// NR x K x L store; the sifted-sample count is taken from the parity-checked
+// GPU run of the same realizations.
+int ref_emd_realizations(const double* x, std::size_t n, double sd, int iters, int imfs, double nstd,
+                         uint64_t seed, int m_begin, int count, int threads, double* checksum) {
+    return guard([&] {
+        const semd::Signal s(x, x + n);
+        const semd::SiftConfig cfg{sd, iters, imfs};
+        const double beta = nstd * semd::signal_std(s);
+        std::vector<double> part(std::size_t(threads > 0 ? threads : 1), 0.0);
+        auto work = [&](int tid) {
+            for (int q = tid; q < count; q += threads) {
+                const int m = m_begin + q;
+                const semd::Signal w = semd::white_noise(n, semd::derive_seed(seed, std::uint64_t(m)));
+                semd::Signal xm(n);
+                for (std::size_t i = 0; i < n; ++i) xm[i] = s[i] + beta * w[i];
+                const semd::Decomposition d = semd::emd(xm, cfg);
+                part[std::size_t(tid)] += d.imfs.empty() ? 0.0 : d.imfs[0][n / 2];
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+        for (auto& t : pool) t.join();
+        double c = 0.0;
+        for (double v : part) c += v;
+        *checksum = c;
+    });
+}
+
+int ref_concatenate(const double* x, std::size_t M, std::size_t N, std::size_t D, int naive, double* out) {
+    return guard([&] {
+        semd::MultiSignal ms(M, N);
+        for (std::size_t j = 0; j < N; ++j)
+            for (std::size_t i = 0; i < M; ++i) ms(i, j) = x[j * M + i];
+        const semd::Signal s = naive ? semd::concatenate_naive(ms, D) : semd::concatenate(ms, D);
+        std::memcpy(out, s.data(), s.size() * 8);
+    });
+}
+
+int ref_deconcatenate(const double* modes, std::size_t K, std::size_t L, std::size_t M, std::size_t N,
+                      std::size_t D, double* out) {
+    return guard([&] {
+        std::vector<semd::Signal> v;
+        for (std::size_t k = 0; k < K; ++k) v.emplace_back(modes + k * L, modes + (k + 1) * L);
+        const semd::ImfTensor t = semd::deconcatenate(v, M, N, D);
+        std::memcpy(out, t.data().data(), t.data().size() * 8);
+    });
+}
+
+int ref_serial_decompose(const double* x, std::size_t M, std::size_t N, std::size_t D, int algo, double sd,
+                         int iters, int imfs, double nstd, int nr, uint64_t seed, void* out) {
+    return guard([&] {
+        semd::MultiSignal ms(M, N);
+        for (std::size_t j = 0; j < N; ++j)
+            for (std::size_t i = 0; i < M; ++i) ms(i, j) = x[j * M + i];
+        const semd::ImfTensor t = semd::serial_decompose(ms, D, static_cast<semd::Algorithm>(algo),
+                                                         {sd, iters, imfs}, {nstd, nr, seed});
+        Out* o = static_cast<Out*>(out);
+        o->K = t.modes();
+        o->imfs = t.data();
+    });
+}
+
+int ref_multivariate_sinusoids(std::size_t n, double fs, double* out) {
+    return guard([&] {
+        const semd::MultiSignal s = semd::multivariate_sinusoids(semd::PickupMask::standard(), n, fs);
+        std::memcpy(out, s.data().data(), s.data().size() * 8);
+    });
+}
+
+std::size_t ref_default_transition_length(std::size_t rows) { return semd::default_transition_length(rows); }
+
+}  // extern "C"
