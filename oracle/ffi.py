@@ -253,6 +253,8 @@ class Ref:
         L.ref_emd_traced.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, C.c_void_p]
         L.ref_eemd_traced.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
                                       C.c_uint64, C.c_int, C.c_int, C.c_void_p]
+        L.ref_ceemdan_traced.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
+                                         C.c_uint64, C.c_void_p]
         L.ref_emd_realizations.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                            C.c_int, C.c_int, C.c_int, _dp]
         L.ref_serial_decompose.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, C.c_double, C.c_int,
@@ -345,6 +347,16 @@ class Ref:
             self._chk(self.lib.ref_eemd_traced(_d(x), x.size, sd, iters, imfs, nstd, nr, seed, m_begin, m_end, o))
             sums, _, counts, trace = self._out(o, x.size)
             return sums, counts, trace
+        finally:
+            self.lib.ref_out_free(o)
+
+    def ceemdan_traced(self, x, sd=0.2, iters=300, imfs=0, nstd=0.2, nr=100, seed=0):
+        x = _f64(x)
+        o = self.lib.ref_out_new()
+        try:
+            self._chk(self.lib.ref_ceemdan_traced(_d(x), x.size, sd, iters, imfs, nstd, nr, seed, o))
+            imfs_, res, _, trace = self._out(o, x.size)
+            return imfs_, res, trace
         finally:
             self.lib.ref_out_free(o)
 

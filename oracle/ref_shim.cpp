@@ -290,6 +290,91 @@ int ref_emd_realizations(const double* x, std::size_t n, double sd, int iters, i
     });
 }
 
+// CEEMDAN (emd.cpp:264-344) re-driven through the replayer so every
+// find_extrema call is traced (task 1 noise IMF, 2 first mode, 3 stage check);
+// the result is checked bit-for-bit against semd::ceemdan.
+int ref_ceemdan_traced(const double* x, std::size_t n, double sd, int iters, int imfs, double nstd, int nr,
+                       uint64_t seed, void* out) {
+    int mismatch = 0;
+    int rc = guard([&] {
+        Out* o = static_cast<Out*>(out);
+        const semd::Signal s(x, x + n);
+        const semd::SiftConfig cfg{sd, iters, imfs};
+        const semd::EnsembleConfig ens{nstd, nr, seed};
+        std::vector<TraceRec>* tr = &o->trace;
+        const std::size_t nrr = std::size_t(nr);
+        std::vector<semd::Signal> noise_res(nrr);
+        std::vector<bool> alive(nrr, true);
+        for (std::size_t m = 0; m < nrr; ++m) noise_res[m] = semd::white_noise(n, semd::derive_seed(seed, m));
+        auto first_mode = [&](const semd::Signal& v, int m, int k) {
+            try {
+                return replay_extract(v, cfg, tr, 2, m, k).imf;
+            } catch (const semd::InsufficientExtrema&) {
+                return semd::Signal(n, 0.0);
+            }
+        };
+        semd::Decomposition d;
+        semd::Signal residue = s;
+        {
+            const double beta0 = nstd * semd::signal_std(s);
+            semd::Signal mode(n, 0.0);
+            for (std::size_t m = 0; m < nrr; ++m) {
+                semd::Signal xm(n);
+                for (std::size_t i = 0; i < n; ++i) xm[i] = s[i] + beta0 * noise_res[m][i];
+                const semd::Signal e1 = first_mode(xm, int(m), 0);
+                for (std::size_t i = 0; i < n; ++i) mode[i] += e1[i];
+            }
+            const double inv = 1.0 / double(nrr);
+            for (std::size_t i = 0; i < n; ++i) {
+                mode[i] *= inv;
+                residue[i] -= mode[i];
+            }
+            d.imfs.push_back(std::move(mode));
+        }
+        while (cfg.max_imfs == 0 || d.imfs.size() < std::size_t(cfg.max_imfs)) {
+            const semd::Extrema ext = semd::find_extrema(residue);
+            const int k = int(d.imfs.size());
+            tr->push_back({3, -1, k, 0, uint32_t(ext.max_idx.size()), uint32_t(ext.min_idx.size()), hash_extrema(ext)});
+            if (ext.total() < 3) break;
+            const double beta_i = nstd * semd::signal_std(residue);
+            semd::Signal mode(n, 0.0);
+            for (std::size_t m = 0; m < nrr; ++m) {
+                semd::Signal ei(n, 0.0);
+                if (alive[m]) {
+                    try {
+                        semd::SiftResult r = replay_extract(noise_res[m], cfg, tr, 1, int(m), k);
+                        ei = std::move(r.imf);
+                        for (std::size_t i = 0; i < n; ++i) noise_res[m][i] -= ei[i];
+                    } catch (const semd::InsufficientExtrema&) {
+                        alive[m] = false;
+                    }
+                }
+                semd::Signal sm(n);
+                for (std::size_t i = 0; i < n; ++i) sm[i] = residue[i] + beta_i * ei[i];
+                const semd::Signal e1 = first_mode(sm, int(m), k);
+                for (std::size_t i = 0; i < n; ++i) mode[i] += e1[i];
+            }
+            const double inv = 1.0 / double(nrr);
+            bool all_zero = true;
+            for (std::size_t i = 0; i < n; ++i) {
+                mode[i] *= inv;
+                if (mode[i] != 0.0) all_zero = false;
+            }
+            if (all_zero) break;
+            for (std::size_t i = 0; i < n; ++i) residue[i] -= mode[i];
+            d.imfs.push_back(std::move(mode));
+        }
+        d.residue = std::move(residue);
+        if (!same(d, semd::ceemdan(s, cfg, ens))) mismatch = 1;
+        store(o, d);
+    });
+    if (rc == 0 && mismatch) {
+        g_err = "replay diverged from semd::ceemdan";
+        return 3;
+    }
+    return rc;
+}
+
 int ref_concatenate(const double* x, std::size_t M, std::size_t N, std::size_t D, int naive, double* out) {
     return guard([&] {
         semd::MultiSignal ms(M, N);
