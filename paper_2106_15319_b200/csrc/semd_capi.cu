@@ -1,0 +1,1158 @@
+// semd_capi.cu -- host engine and C ABI (include/semd_b200.h).
+//
+// The host side only stages buffers, seeds realizations and sequences kernel
+// launches; every numeric operation of the hot path runs in semd_kernels.cu
+// on the GPU. Control flow that the reference resolves per sift iteration
+// (stop tests, IMF completion, extrema counts) is decided on the device by
+// the epilogues of k_eval / k_final; the host only polls a mapped pinned word
+// a few steps behind to learn when every slot is done.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/semd_b200.h"
+#include "semd_launch.h"
+#include "semd_types.cuh"
+
+using semd::dev::Arena;
+using semd::dev::Ctrl;
+using semd::dev::Slot;
+using semd::dev::TraceRec;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw Error{code, buf};
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(SEMD_CUDA_ERROR, "%s: %s", what, cudaGetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return SEMD_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return SEMD_NO_MEMORY;
+    }
+}
+
+uint64_t derive_seed(uint64_t base, uint64_t index) {  // emd.cpp:174-179
+    uint64_t z = base + 0x9E3779B97F4A7C15ULL * (index + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// Device allocation helper that frees on scope exit.
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    explicit DBuf(size_t b) { alloc(b); }
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    void alloc(size_t b) {
+        if (p && bytes >= b) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (b == 0) b = 8;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            raise(SEMD_NO_MEMORY, "cudaMalloc(%zu bytes) failed: %s", b, cudaGetErrorString(e));
+        }
+        bytes = b;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct JobSpec {
+    int m = 0, task = 0, k = 0, kmax = 0, k0 = 0, init_kind = 0, write_imf = 1, detect_only = 0;
+    double beta = 0.0;
+    const double* a = nullptr;
+    const double* b = nullptr;
+    double* imf_out = nullptr;
+    double* res_out = nullptr;
+};
+
+}  // namespace
+
+struct semd_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    int max_slots = 0;
+    bool timing = false;
+    semd_stats stats{};
+    // engine arena
+    Arena A{};
+    int cfg_L = -1, cfg_G = -1, cfg_kcap = -1, cfg_trace = -1;
+    DBuf bufs, kidx, kval, toff, mom, status, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace;
+    int* status_host = nullptr;
+    int* status_host_dev = nullptr;
+    std::vector<Slot> h_slots;
+    std::vector<TraceRec> h_trace;
+    // scratch
+    DBuf in_x, in_y, noise, scratch, scratch2, scalar, rng_jobs;
+    cudaEvent_t ev[16]{};
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+
+    ~semd_ctx() {
+        if (status_host) cudaFreeHost(status_host);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (t0) cudaEventDestroy(t0);
+        if (t1) cudaEventDestroy(t1);
+        if (own) cudaStreamDestroy(own);
+    }
+
+    void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+
+    // ---- arena --------------------------------------------------------------
+    void configure(long long L, int G, int kcap, int trace_cap) {
+        if (L >= (1LL << 30)) raise(SEMD_INVALID_INPUT, "signal too long for the engine (%lld samples)", L);
+        if (L == cfg_L && G == cfg_G && kcap == cfg_kcap && trace_cap == cfg_trace) return;
+        const int tiles = (int)((L + semd::dev::kEvalTile - 1) / semd::dev::kEvalTile);
+        const int cap = (int)(L / 2 + 2);
+        const int rows_max = cap + 2;
+        const int max_blocks = rows_max / semd::dev::kSolveBlock + 2;
+        bufs.alloc((size_t)G * 3 * L * 8);
+        kidx.alloc((size_t)4 * G * cap * 4);
+        kval.alloc((size_t)4 * G * cap * 8);
+        toff.alloc((size_t)4 * G * (tiles + 1) * 4);
+        mom.alloc((size_t)2 * G * (cap + 4) * 8);
+        status.alloc((size_t)2 * G * tiles * 8);
+        tnum.alloc((size_t)G * tiles * 8);
+        tden.alloc((size_t)G * tiles * 8);
+        thash.alloc((size_t)G * tiles * 8);
+        slots.alloc((size_t)G * sizeof(Slot));
+        sums.alloc((size_t)kcap * L * 8);
+        imf_sifts.alloc((size_t)kcap * 4);
+        ctrl.alloc(sizeof(Ctrl));
+        lists.alloc((size_t)(G + G + 2 * G + 2 * G + 1) * 4);
+        sb.alloc((size_t)2 * G * max_blocks * 6 * 8);
+        if (trace_cap > 0) trace.alloc((size_t)trace_cap * sizeof(TraceRec));
+        A = Arena{};
+        A.L = (int)L;
+        A.G = G;
+        A.tiles = tiles;
+        A.cap = cap;
+        A.kcap = kcap;
+        A.bufs = bufs.as<double>();
+        A.kidx = kidx.as<int>();
+        A.kval = kval.as<double>();
+        A.toff = toff.as<unsigned>();
+        A.mom = mom.as<double>();
+        A.status = status.as<unsigned long long>();
+        A.tnum = tnum.as<double>();
+        A.tden = tden.as<double>();
+        A.thash = thash.as<unsigned long long>();
+        A.slots = slots.as<Slot>();
+        A.sums = sums.as<double>();
+        A.imf_sifts = imf_sifts.as<int>();
+        A.ctrl = ctrl.as<Ctrl>();
+        int* l = lists.as<int>();
+        A.eval_list = l;
+        A.final_list = l + G;
+        A.solve_item = l + 2 * G;
+        A.solve_off = l + 4 * G;
+        A.sb = sb.as<double>();
+        A.max_blocks = max_blocks;
+        A.trace = trace_cap > 0 ? trace.as<TraceRec>() : nullptr;
+        A.trace_cap = trace_cap;
+        A.status_host = status_host_dev;
+        // look-back words and toff start clean (epoch 0 never matches)
+        ck(cudaMemsetAsync(status.p, 0, status.bytes, stream), "memset status");
+        ck(cudaMemsetAsync(toff.p, 0, toff.bytes, stream), "memset toff");
+        ck(cudaMemsetAsync(sb.p, 0, sb.bytes, stream), "memset sb");
+        cfg_L = (int)L;
+        cfg_G = G;
+        cfg_kcap = kcap;
+        cfg_trace = trace_cap;
+        h_slots.assign(G, Slot{});
+        for (auto& s : h_slots) s.epoch = 1;
+    }
+
+    int auto_slots(long long L, int jobs) {
+        long long g = (64LL << 20) / std::max(1LL, L);
+        g = std::max(1LL, std::min<long long>(g, 1024));
+        if (max_slots > 0) g = std::min<long long>(g, max_slots);
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const long long per_slot = 72LL * L + 4096;
+        const long long mem_g = (long long)(0.5 * (double)free_b) / per_slot;
+        g = std::max(1LL, std::min(g, mem_g));
+        return (int)std::min<long long>(g, std::max(1, jobs));
+    }
+
+    static int default_kcap(long long L, int max_imfs) {
+        if (max_imfs > 0) return max_imfs;
+        int lg = 0;
+        while ((1LL << lg) < L) ++lg;
+        return lg + 6;
+    }
+
+    // ---- one lockstep run over the configured slots -------------------------
+    void set_jobs(const std::vector<JobSpec>& jobs) {
+        const int G = A.G;
+        for (int s = 0; s < G; ++s) {
+            Slot& S = h_slots[s];
+            const unsigned epoch = S.epoch;
+            S = Slot{};
+            S.epoch = epoch + 1;
+            if (s < (int)jobs.size()) {
+                const JobSpec& J = jobs[s];
+                S.m = J.m;
+                S.task = J.task;
+                S.k = J.k;
+                S.kmax = J.kmax;
+                S.k0 = J.k0;
+                S.init_kind = J.init_kind;
+                S.write_imf = J.write_imf;
+                S.detect_only = J.detect_only;
+                S.beta = J.beta;
+                S.init_a = J.a;
+                S.init_b = J.b;
+                S.imf_out = J.imf_out;
+                S.res_out = J.res_out;
+                S.state = semd::dev::ST_INIT;
+                S.xb = 0;
+                S.cb = -1;
+                S.par = 0;
+            } else {
+                S.state = semd::dev::ST_FREE;
+            }
+        }
+        ck(cudaMemcpyAsync(A.slots, h_slots.data(), (size_t)G * sizeof(Slot), cudaMemcpyHostToDevice, stream),
+           "upload slots");
+        Ctrl c{};
+        std::vector<int> el;
+        for (int s = 0; s < (int)jobs.size() && s < G; ++s) el.push_back(s);
+        c.n_eval = (int)el.size();
+        c.active = (int)el.size();
+        ck(cudaMemcpyAsync(A.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "upload ctrl");
+        if (!el.empty())
+            ck(cudaMemcpyAsync(A.eval_list, el.data(), el.size() * 4, cudaMemcpyHostToDevice, stream), "lists");
+        ck(cudaMemsetAsync(A.solve_off, 0, 4, stream), "lists");
+        ck(cudaStreamSynchronize(stream), "sync");  // h_slots / el are reused by the caller
+        *(volatile int*)status_host = c.active;
+    }
+
+    void run(int max_steps) {
+        const int LAG = 3, R = 16;
+        int step = 0;
+        if (timing) ck(cudaEventRecord(t0, stream), "event");
+        for (;; ++step) {
+            semd::dev::launch_step(A, sms, stream);
+            stats.kernel_launches += 3;
+            stats.eval_launches += 1;
+            ck(cudaGetLastError(), "launch step");
+            ck(cudaEventRecord(ev[step % R], stream), "event record");
+            if (step >= LAG) {
+                ck(cudaEventSynchronize(ev[(step - LAG) % R]), "step");
+                if (*(volatile int*)status_host == 0) break;
+            }
+            if (step > max_steps) raise(SEMD_CUDA_ERROR, "engine did not converge within %d steps", max_steps);
+        }
+        ck(cudaStreamSynchronize(stream), "engine run");
+        if (timing) {
+            ck(cudaEventRecord(t1, stream), "event");
+            ck(cudaEventSynchronize(t1), "event");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, t0, t1);
+            stats.eval_ms += ms;
+        }
+        stats.steps += step + 1;
+        ck(cudaMemcpy(h_slots.data(), A.slots, (size_t)A.G * sizeof(Slot), cudaMemcpyDeviceToHost), "download slots");
+        Ctrl c{};
+        ck(cudaMemcpy(&c, A.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost), "download ctrl");
+        for (const Slot& S : h_slots) {
+            stats.sifted_samples += (uint64_t)S.sifted;
+            stats.sift_iterations += (uint64_t)(S.sifted / std::max(1, A.L));
+        }
+        stats.solve_hazards += (uint64_t)c.hazards;
+        if (c.k_overflow) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", A.kcap);
+        if (A.trace) {
+            const int n = std::min(c.trace_count, A.trace_cap);
+            const size_t old = h_trace.size();
+            h_trace.resize(old + n);
+            if (n) ck(cudaMemcpy(h_trace.data() + old, A.trace, (size_t)n * sizeof(TraceRec), cudaMemcpyDeviceToHost),
+                      "trace");
+            trace_total += c.trace_count;
+        }
+        // reset counters for the next run
+        Ctrl z{};
+        ck(cudaMemcpyAsync(A.ctrl, &z, sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
+    }
+    long long trace_total = 0;
+
+    int max_steps_for(const semd_sift_cfg& cfg) const {
+        const long long it = std::max(1, cfg.max_sift_iters) + 2;
+        return (int)std::min<long long>((long long)(A.kcap + 2) * it + 64, 1LL << 30);
+    }
+
+    void reset_stats(int slots_used) {
+        stats = semd_stats{};
+        stats.slots = slots_used;
+    }
+
+    double* buf(int slot, int b) { return A.bufs + semd::dev::buf_off(A, slot, b); }
+
+    void fill_sums(int rows, double value) {
+        // +0.0 for ensembles (the reference's Signal(n, 0.0)), -0.0 where the
+        // accumulator must reproduce the IMF bit-for-bit (-0.0 + v == v).
+        const long long n = (long long)rows * A.L;
+        if (value == 0.0 && !std::signbit(value)) ck(cudaMemsetAsync(A.sums, 0, (size_t)n * 8, stream), "memset sums");
+        else semd::dev::launch_fill(A.sums, n, value, stream);
+    }
+
+    // ---- drivers ---------------------------------------------------------------
+    // emd.cpp:155-172 on a device signal; returns K. IMFs in sums rows, residue in buffer.
+    int emd_device(const double* d_x, long long n, const semd_sift_cfg& cfg, semd_trace* tr, int m = 0) {
+        if (n < 4) raise(SEMD_INVALID_INPUT, "emd: signal too short (need at least 4 samples)");
+        int kcap = default_kcap(n, cfg.max_imfs);
+        for (int attempt = 0;; ++attempt) {
+            configure(n, 1, kcap, tr ? trace_cap_for(tr) : 0);
+            A.sd_threshold = cfg.sd_threshold;
+            A.max_sift_iters = cfg.max_sift_iters;
+            fill_sums(kcap, -0.0);
+            JobSpec J;
+            J.m = m;
+            J.task = 0;
+            J.kmax = cfg.max_imfs;
+            J.a = d_x;
+            h_trace.clear();
+            trace_total = 0;
+            set_jobs({J});
+            try {
+                run(max_steps_for(cfg));
+            } catch (const Error& e) {
+                if (e.code == SEMD_CAPACITY && attempt < 3 && cfg.max_imfs == 0) {
+                    kcap *= 2;
+                    continue;
+                }
+                throw;
+            }
+            return h_slots[0].k;
+        }
+    }
+    int trace_cap_for(const semd_trace* tr) const { return tr && tr->cap ? (int)std::min<size_t>(tr->cap, 1u << 26) : 0; }
+
+    void export_trace(semd_trace* tr) {
+        if (!tr) return;
+        tr->count = (size_t)trace_total;
+        const size_t n = std::min(tr->cap, h_trace.size());
+        if (n && tr->rec) std::memcpy(tr->rec, h_trace.data(), n * sizeof(semd_trace_rec));
+    }
+
+    // white noise for realizations ms[0..g) into the noise buffer (stride Ls), std 1.
+    void gen_noise(const std::vector<uint64_t>& seeds, long long n, long long Ls, double* dst, double stdv = 1.0) {
+        const int g = (int)seeds.size();
+        std::vector<semd::dev::RngJob> jobs(g);
+        for (int i = 0; i < g; ++i) {
+            jobs[i].seed = seeds[i];
+            jobs[i].out = reinterpret_cast<uint64_t*>(dst + (size_t)i * Ls);
+            jobs[i].n = n;
+        }
+        rng_jobs.alloc(jobs.size() * sizeof(semd::dev::RngJob));
+        ck(cudaMemcpyAsync(rng_jobs.p, jobs.data(), jobs.size() * sizeof(semd::dev::RngJob), cudaMemcpyHostToDevice,
+                           stream),
+           "rng jobs");
+        semd::dev::launch_rng(rng_jobs.as<semd::dev::RngJob>(), g, stream);
+        semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(dst), (long long)g * Ls, stdv, stream);
+        ck(cudaGetLastError(), "rng");
+        ck(cudaStreamSynchronize(stream), "rng sync");  // jobs vector lifetime
+    }
+
+    double device_std(const double* d_x, long long n, double scale) {
+        scalar.alloc(16);
+        semd::dev::launch_signal_std(d_x, n, scalar.as<double>(), scale, stream);
+        double v = 0.0;
+        ck(cudaMemcpyAsync(&v, scalar.p, 8, cudaMemcpyDeviceToHost, stream), "std");
+        ck(cudaStreamSynchronize(stream), "std");
+        return v;
+    }
+
+    // EEMD realizations [m_begin, m_end): unscaled sums in A.sums rows; returns max K.
+    const double* noise_override = nullptr;  // test hook: nr x n noise (device)
+    int eemd_partial_device(const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens,
+                            int m_begin, int m_end, semd_trace* tr) {
+        if (n < 4) raise(SEMD_INVALID_INPUT, "emd: signal too short (need at least 4 samples)");
+        const int jobs = std::max(0, m_end - m_begin);
+        const int G = auto_slots(n, jobs);
+        int kcap = default_kcap(n, cfg.max_imfs);
+        const double beta = device_std(d_x, n, ens.nstd);  // emd.cpp:233
+        const long long Ls = (n + 1) / 2 * 2;
+        for (int attempt = 0;; ++attempt) {
+            configure(n, G, kcap, tr ? trace_cap_for(tr) : 0);
+            A.sd_threshold = cfg.sd_threshold;
+            A.max_sift_iters = cfg.max_sift_iters;
+            noise.alloc((size_t)G * Ls * 8);
+            fill_sums(kcap, 0.0);
+            h_trace.clear();
+            trace_total = 0;
+            int kmax_seen = 0, waves = 0;
+            try {
+                for (int w0 = m_begin; w0 < m_end; w0 += G) {
+                    const int g = std::min(G, m_end - w0);
+                    std::vector<JobSpec> js(g);
+                    if (!noise_override) {
+                        std::vector<uint64_t> seeds(g);
+                        for (int i = 0; i < g; ++i) seeds[i] = derive_seed(ens.base_seed, (uint64_t)(w0 + i));
+                        gen_noise(seeds, n, Ls, noise.as<double>());
+                    }
+                    for (int i = 0; i < g; ++i) {
+                        JobSpec& J = js[i];
+                        J.m = w0 + i;
+                        J.task = 0;
+                        J.kmax = cfg.max_imfs;
+                        J.init_kind = 1;
+                        J.beta = beta;
+                        J.a = d_x;
+                        J.b = noise_override ? noise_override + (size_t)(w0 + i) * n : noise.as<double>() + (size_t)i * Ls;
+                    }
+                    set_jobs(js);
+                    run(max_steps_for(cfg));
+                    ++waves;
+                    for (int i = 0; i < g; ++i) kmax_seen = std::max(kmax_seen, h_slots[i].k);
+                }
+            } catch (const Error& e) {
+                if (e.code == SEMD_CAPACITY && attempt < 3 && cfg.max_imfs == 0) {
+                    kcap *= 2;
+                    continue;
+                }
+                throw;
+            }
+            stats.waves += waves;
+            stats.slots = G;
+            return kmax_seen;
+        }
+    }
+
+    // emd.cpp:264-344. Returns K; IMFs in `out_imfs` (device, kcap rows), residue in out_res.
+    int ceemdan_device(const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens,
+                       double* out_imfs, int k_cap, double* out_res, semd_trace* tr, int* k_needed) {
+        if (n < 4) raise(SEMD_INVALID_INPUT, "ceemdan: signal too short (need at least 4 samples)");
+        const int nr = ens.nr;
+        const int G = auto_slots(n, nr);
+        int kcap = default_kcap(n, cfg.max_imfs);
+        configure(n, G, kcap, tr ? trace_cap_for(tr) : 0);
+        A.sd_threshold = cfg.sd_threshold;
+        A.max_sift_iters = cfg.max_sift_iters;
+        h_trace.clear();
+        trace_total = 0;
+        const long long Ls = (n + 1) / 2 * 2;
+        noise.alloc((size_t)nr * Ls * 8);    // noise residues (per realization)
+        scratch.alloc((size_t)nr * n * 8);   // E_i(w^(m))
+        scratch2.alloc((size_t)n * 8 * 2);   // residue + nonzero flag
+        double* noise_res = noise.as<double>();
+        double* E = scratch.as<double>();
+        double* residue = scratch2.as<double>();
+        int* nonzero = reinterpret_cast<int*>(residue + n);
+        if (noise_override) {
+            for (int m = 0; m < nr; ++m)
+                ck(cudaMemcpyAsync(noise_res + (size_t)m * Ls, noise_override + (size_t)m * n, n * 8,
+                                   cudaMemcpyDeviceToDevice, stream),
+                   "noise override");
+        } else {
+            for (int m0 = 0; m0 < nr; m0 += 1024) {
+                const int g = std::min(1024, nr - m0);
+                std::vector<uint64_t> seeds(g);
+                for (int i = 0; i < g; ++i) seeds[i] = derive_seed(ens.base_seed, (uint64_t)(m0 + i));
+                gen_noise(seeds, n, Ls, noise_res + (size_t)m0 * Ls);
+            }
+        }
+        std::vector<char> alive(nr, 1);
+        semd::dev::launch_copy(d_x, residue, n, stream);
+        fill_sums(kcap, 0.0);
+        const double inv = 1.0 / (double)nr;
+        int K = 0;
+        int waves = 0;
+        auto run_tasks = [&](std::vector<JobSpec>& all, std::vector<Slot>* results) {
+            results->resize(all.size());
+            for (size_t w0 = 0; w0 < all.size(); w0 += G) {
+                const size_t g = std::min<size_t>(G, all.size() - w0);
+                std::vector<JobSpec> js(all.begin() + w0, all.begin() + w0 + g);
+                set_jobs(js);
+                run(max_steps_for(cfg));
+                ++waves;
+                for (size_t i = 0; i < g; ++i) (*results)[w0 + i] = h_slots[i];
+            }
+        };
+        auto stage_mean = [&](int row, bool check_zero) -> bool {
+            double* mode = A.sums + (size_t)row * n;
+            ck(cudaMemsetAsync(nonzero, 0, 4, stream), "flag");
+            semd::dev::launch_stage_scale(mode, n, inv, nonzero, stream);
+            int nz = 0;
+            ck(cudaMemcpyAsync(&nz, nonzero, 4, cudaMemcpyDeviceToHost, stream), "flag");
+            ck(cudaStreamSynchronize(stream), "stage");
+            if (check_zero && !nz) return false;
+            semd::dev::launch_sub(residue, mode, n, stream);
+            return true;
+        };
+        {  // mode 1 (emd.cpp:292-307)
+            const double beta0 = device_std(d_x, n, ens.nstd);
+            std::vector<JobSpec> js(nr);
+            for (int m = 0; m < nr; ++m) {
+                JobSpec& J = js[m];
+                J.m = m;
+                J.task = 2;
+                J.k = 0;
+                J.kmax = 1;
+                J.init_kind = 1;
+                J.beta = beta0;
+                J.a = d_x;
+                J.b = noise_res + (size_t)m * Ls;
+            }
+            std::vector<Slot> res;
+            run_tasks(js, &res);
+            stage_mean(0, false);
+            K = 1;
+        }
+        while (cfg.max_imfs == 0 || K < cfg.max_imfs) {  // emd.cpp:310
+            if (K >= kcap) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", kcap);
+            {  // stage check: find_extrema(residue).total() < 3 (emd.cpp:311)
+                JobSpec J;
+                J.m = -1;
+                J.task = 3;
+                J.k = K;
+                J.a = residue;
+                J.detect_only = 1;
+                std::vector<JobSpec> js{J};
+                std::vector<Slot> res;
+                run_tasks(js, &res);
+                if (res[0].n[0] + res[0].n[1] < 3) break;
+            }
+            const double beta_i = device_std(residue, n, ens.nstd);  // emd.cpp:312
+            {  // E_i(w^(m)) for the living noise residues (emd.cpp:316-325)
+                std::vector<JobSpec> js;
+                std::vector<int> ms;
+                for (int m = 0; m < nr; ++m) {
+                    if (!alive[m]) continue;
+                    JobSpec J;
+                    J.m = m;
+                    J.task = 1;
+                    J.k = K;
+                    J.kmax = K + 1;
+                    J.write_imf = 0;
+                    J.a = noise_res + (size_t)m * Ls;
+                    J.imf_out = E + (size_t)m * n;
+                    J.res_out = noise_res + (size_t)m * Ls;
+                    js.push_back(J);
+                    ms.push_back(m);
+                }
+                std::vector<Slot> res;
+                run_tasks(js, &res);
+                for (size_t i = 0; i < ms.size(); ++i) {
+                    if (res[i].ended_insufficient) {
+                        alive[ms[i]] = 0;
+                        ck(cudaMemsetAsync(E + (size_t)ms[i] * n, 0, n * 8, stream), "E zero");
+                    }
+                }
+            }
+            {  // first modes of r_i + beta_i E_i (emd.cpp:326-329)
+                std::vector<JobSpec> js(nr);
+                for (int m = 0; m < nr; ++m) {
+                    JobSpec& J = js[m];
+                    J.m = m;
+                    J.task = 2;
+                    J.k = K;
+                    J.kmax = K + 1;
+                    J.init_kind = 1;
+                    J.beta = beta_i;
+                    J.a = residue;
+                    J.b = E + (size_t)m * n;
+                }
+                std::vector<Slot> res;
+                run_tasks(js, &res);
+            }
+            if (!stage_mean(K, true)) break;  // all-zero mode (emd.cpp:332-337)
+            ++K;
+        }
+        stats.waves += waves;
+        stats.slots = G;
+        *k_needed = K;
+        if (K > k_cap) return K;
+        if (out_imfs && K)
+            ck(cudaMemcpyAsync(out_imfs, A.sums, (size_t)K * n * 8, cudaMemcpyDeviceToDevice, stream), "imfs");
+        if (out_res) ck(cudaMemcpyAsync(out_res, residue, n * 8, cudaMemcpyDeviceToDevice, stream), "residue");
+        ck(cudaStreamSynchronize(stream), "ceemdan");
+        return K;
+    }
+
+    // Full decomposition with device buffers. Returns K via *k_out; SEMD_CAPACITY if K > k_cap.
+    void decompose_device(int algo, const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens,
+                          double* d_imfs, size_t k_cap, size_t* k_out, double* d_res, int32_t* sift_counts_host,
+                          semd_trace* tr) {
+        if (algo < 0 || algo > 2) raise(SEMD_INVALID_INPUT, "unknown algorithm value");
+        if (algo != SEMD_ALGO_EMD) {
+            if (ens.nr < 1) raise(SEMD_INVALID_INPUT, "ensemble: nr must be at least 1");
+            if (ens.nstd < 0.0) raise(SEMD_INVALID_INPUT, "ensemble: nstd must be non-negative");
+            if (ens.nstd == 0.0) algo = SEMD_ALGO_EMD;  // degenerate ensemble is plain emd
+        }
+        reset_stats(1);
+        if (algo != SEMD_ALGO_CEEMDAN && cfg.max_sift_iters <= 0 && cfg.max_imfs == 0)
+            raise(SEMD_INVALID_INPUT,
+                  "emd: max_sift_iters <= 0 with max_imfs == 0 never terminates (every IMF is the whole residue)");
+        if (algo == SEMD_ALGO_EMD) {
+            const int K = emd_device(d_x, n, cfg, tr);
+            *k_out = (size_t)K;
+            stats.slots = 1;
+            stats.waves = 1;
+            export_trace(tr);
+            if ((size_t)K > k_cap) raise(SEMD_CAPACITY, "output holds %zu IMFs, decomposition has %d", k_cap, K);
+            if (K && d_imfs)
+                ck(cudaMemcpyAsync(d_imfs, A.sums, (size_t)K * n * 8, cudaMemcpyDeviceToDevice, stream), "imfs");
+            if (d_res)
+                ck(cudaMemcpyAsync(d_res, buf(0, h_slots[0].xb), n * 8, cudaMemcpyDeviceToDevice, stream), "residue");
+            if (sift_counts_host && K) {
+                std::vector<int> c(K);
+                ck(cudaMemcpy(c.data(), A.imf_sifts, (size_t)K * 4, cudaMemcpyDeviceToHost), "counts");
+                for (int k = 0; k < K; ++k) sift_counts_host[k] = c[k];
+            }
+            ck(cudaStreamSynchronize(stream), "emd");
+            return;
+        }
+        if (algo == SEMD_ALGO_EEMD) {
+            if (n < 4) raise(SEMD_INVALID_INPUT, "emd: signal too short (need at least 4 samples)");
+            const int K = eemd_partial_device(d_x, n, cfg, ens, 0, ens.nr, tr);
+            *k_out = (size_t)K;
+            export_trace(tr);
+            if ((size_t)K > k_cap) raise(SEMD_CAPACITY, "output holds %zu IMFs, decomposition has %d", k_cap, K);
+            semd::dev::launch_ensemble_finish(A.sums, K, n, d_x, d_res ? d_res : buf(0, 1), 1.0 / (double)ens.nr,
+                                              stream);
+            if (K && d_imfs)
+                ck(cudaMemcpyAsync(d_imfs, A.sums, (size_t)K * n * 8, cudaMemcpyDeviceToDevice, stream), "imfs");
+            if (sift_counts_host)
+                for (int k = 0; k < K; ++k) sift_counts_host[k] = 0;
+            ck(cudaStreamSynchronize(stream), "eemd");
+            return;
+        }
+        int need = 0;
+        ceemdan_device(d_x, n, cfg, ens, d_imfs, (int)k_cap, d_res, tr, &need);
+        *k_out = (size_t)need;
+        export_trace(tr);
+        if ((size_t)need > k_cap) raise(SEMD_CAPACITY, "output holds %zu IMFs, decomposition has %d", k_cap, need);
+        if (sift_counts_host)
+            for (int k = 0; k < need; ++k) sift_counts_host[k] = 0;
+    }
+
+    double* upload(DBuf& d, const double* h, size_t n) {
+        d.alloc(n * 8);
+        if (n) ck(cudaMemcpyAsync(d.p, h, n * 8, cudaMemcpyHostToDevice, stream), "upload");
+        return d.as<double>();
+    }
+    void download(double* h, const double* d, size_t n) {
+        if (n) ck(cudaMemcpyAsync(h, d, n * 8, cudaMemcpyDeviceToHost, stream), "download");
+        ck(cudaStreamSynchronize(stream), "download");
+    }
+};
+
+namespace {
+
+semd_sift_cfg sift_or_default(const semd_sift_cfg* c) {
+    if (c) return *c;
+    return semd_sift_cfg{0.2, 300, 0};
+}
+semd_ens_cfg ens_or_default(const semd_ens_cfg* e) {
+    if (e) return *e;
+    return semd_ens_cfg{0.2, 100, 0, 0};
+}
+
+void need_ctx(semd_ctx* ctx) {
+    if (!ctx) raise(SEMD_INVALID_INPUT, "null semd_ctx");
+    ctx->use();
+}
+
+void validate_serial(size_t M, size_t N, size_t D) {  // serialize.cpp:22-26
+    if (M == 0 || N == 0) raise(SEMD_INVALID_INPUT, "concatenate: empty input");
+    if (D < 1) raise(SEMD_INVALID_INPUT, "concatenate: D must be at least 1");
+    if (D > M) raise(SEMD_INVALID_INPUT, "concatenate: transition longer than channel");
+}
+
+void concat_device(semd_ctx* c, const double* d_x, size_t M, size_t N, size_t D, double* d_out, int naive) {
+    validate_serial(M, N, D);
+    c->scratch2.alloc(std::max<size_t>(D, 1) * 8);
+    semd::dev::launch_transition_weights((long long)D, c->scratch2.as<double>(), c->stream);
+    semd::dev::launch_concatenate(d_x, (long long)M, (long long)N, (long long)D, c->scratch2.as<double>(), d_out, naive,
+                                  c->stream);
+    ck(cudaGetLastError(), "concatenate");
+}
+
+void validate_deconcat(size_t K, size_t L, size_t M, size_t N, size_t D) {  // serialize.cpp:75-81
+    if (K == 0) raise(SEMD_INVALID_INPUT, "deconcatenate: no modes given");
+    if (M == 0 || N == 0) raise(SEMD_INVALID_INPUT, "deconcatenate: empty target shape");
+    const size_t expect = M * N + D * (N - 1);
+    if (L != expect)
+        raise(SEMD_INVALID_INPUT, "deconcatenate: mode length %zu does not match M*N + D*(N-1) = %zu", L, expect);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* semd_last_error(void) { return g_err.c_str(); }
+
+int semd_ctx_create(int device, semd_ctx** out) {
+    return guard([&] {
+        if (!out) raise(SEMD_INVALID_INPUT, "null output pointer");
+        *out = nullptr;
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            raise(SEMD_CUDA_ERROR, "no CUDA device available (%s); the B200 sift engine has no CPU fallback",
+                  cudaGetErrorString(e));
+        }
+        if (device < 0 || device >= ndev) raise(SEMD_INVALID_INPUT, "device %d out of range (%d devices)", device, ndev);
+        auto* c = new semd_ctx();
+        try {
+            c->device = device;
+            c->use();
+            cudaDeviceProp prop{};
+            ck(cudaGetDeviceProperties(&prop, device), "device properties");
+            if (prop.major < 10) raise(SEMD_CUDA_ERROR, "device %s (sm_%d%d) is not sm_100", prop.name, prop.major, prop.minor);
+            c->sms = prop.multiProcessorCount;
+            ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "stream");
+            c->stream = c->own;
+            for (auto& ev : c->ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+            ck(cudaEventCreate(&c->t0), "event");
+            ck(cudaEventCreate(&c->t1), "event");
+            ck(cudaHostAlloc(&c->status_host, 64, cudaHostAllocMapped), "pinned status");
+            ck(cudaHostGetDevicePointer(&c->status_host_dev, c->status_host, 0), "mapped status");
+            ck(semd::dev::launch_setup(), "kernel attributes");
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+void semd_ctx_destroy(semd_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    delete ctx;
+}
+
+int semd_get_stats(semd_ctx* ctx, semd_stats* out) {
+    return guard([&] {
+        if (!ctx || !out) raise(SEMD_INVALID_INPUT, "null argument");
+        *out = ctx->stats;
+    });
+}
+
+int semd_set_stream(semd_ctx* ctx, void* s) {
+    return guard([&] {
+        need_ctx(ctx);
+        ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    });
+}
+
+int semd_set_timing(semd_ctx* ctx, int enable) {
+    return guard([&] {
+        need_ctx(ctx);
+        ctx->timing = enable != 0;
+    });
+}
+
+int semd_set_max_slots(semd_ctx* ctx, int slots) {
+    return guard([&] {
+        need_ctx(ctx);
+        ctx->max_slots = std::max(0, slots);
+    });
+}
+
+// Test hook: nr x n host noise used instead of the device RNG (NULL clears).
+int semd_set_noise_override(semd_ctx* ctx, const double* noise, size_t nr, size_t n) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!noise) {
+            ctx->noise_override = nullptr;
+            return;
+        }
+        ctx->in_y.alloc(nr * n * 8);
+        ck(cudaMemcpy(ctx->in_y.p, noise, nr * n * 8, cudaMemcpyHostToDevice), "noise override");
+        ctx->noise_override = ctx->in_y.as<double>();
+    });
+}
+
+uint64_t semd_derive_seed(uint64_t base, uint64_t index) { return derive_seed(base, index); }
+
+size_t semd_default_transition_length(size_t rows) {  // serialize.cpp:15-18
+    const long long d = std::llround(0.2 * (double)rows);
+    const size_t v = d < 1 ? 1 : (size_t)d;
+    return std::min(v, rows);
+}
+
+int semd_parse_algorithm(const char* name, int* algo) {
+    return guard([&] {
+        if (!name || !algo) raise(SEMD_INVALID_INPUT, "null argument");
+        std::string s;
+        for (const char* p = name; *p; ++p) s.push_back((char)std::tolower((unsigned char)*p));
+        if (s == "emd") *algo = 0;
+        else if (s == "eemd") *algo = 1;
+        else if (s == "ceemdan" || s == "eemdan") *algo = 2;
+        else raise(SEMD_INVALID_INPUT, "unknown algorithm '%s' (expected emd, eemd, or ceemdan)", name);
+    });
+}
+
+int semd_find_extrema(semd_ctx* ctx, const double* x, size_t n, size_t* max_idx, double* max_val, size_t* n_max,
+                      size_t* min_idx, double* min_val, size_t* n_min) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (n < 3) raise(SEMD_INVALID_INPUT, "find_extrema: signal too short (need at least 3 samples)");
+        const double* d_x = ctx->upload(ctx->in_x, x, n);
+        ctx->reset_stats(1);
+        ctx->configure((long long)n, 1, 1, 0);
+        ctx->A.sd_threshold = 0.2;
+        ctx->A.max_sift_iters = 1;
+        JobSpec J;
+        J.a = d_x;
+        J.detect_only = 1;
+        ctx->set_jobs({J});
+        ctx->run(8);
+        const Slot& S = ctx->h_slots[0];
+        const unsigned nm = S.n[0], nn = S.n[1];
+        std::vector<int> idx(std::max(nm, nn));
+        const semd::dev::Arena& A = ctx->A;
+        // the detect wrote parity 1 (slot started at parity 0)
+        if (nm) {
+            ck(cudaMemcpy(idx.data(), A.kidx + semd::dev::knot_off(A, 1, 0, 0), nm * 4, cudaMemcpyDeviceToHost), "idx");
+            for (unsigned i = 0; i < nm; ++i) max_idx[i] = (size_t)idx[i];
+            ck(cudaMemcpy(max_val, A.kval + semd::dev::knot_off(A, 1, 0, 0), nm * 8, cudaMemcpyDeviceToHost), "val");
+        }
+        if (nn) {
+            ck(cudaMemcpy(idx.data(), A.kidx + semd::dev::knot_off(A, 1, 1, 0), nn * 4, cudaMemcpyDeviceToHost), "idx");
+            for (unsigned i = 0; i < nn; ++i) min_idx[i] = (size_t)idx[i];
+            ck(cudaMemcpy(min_val, A.kval + semd::dev::knot_off(A, 1, 1, 0), nn * 8, cudaMemcpyDeviceToHost), "val");
+        }
+        *n_max = nm;
+        *n_min = nn;
+    });
+}
+
+int semd_envelope(semd_ctx* ctx, const size_t* idx, const double* val, size_t n, size_t length, double* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (n < 2) raise(SEMD_INSUFFICIENT_EXTREMA, "envelope: need at least 2 extrema, got %zu", n);
+        const size_t N = n + 4;
+        ctx->scratch.alloc((N * 4 + length + n * 2) * 8);
+        double* xs = ctx->scratch.as<double>();
+        double* ys = xs + N;
+        double* mom = ys + N;
+        double* work = mom + N;
+        double* d_out = work + N;
+        unsigned long long* d_idx = reinterpret_cast<unsigned long long*>(d_out + length);
+        double* d_val = reinterpret_cast<double*>(d_idx + n);
+        static_assert(sizeof(size_t) == 8, "size_t must be 64-bit");
+        ck(cudaMemcpyAsync(d_idx, idx, n * 8, cudaMemcpyHostToDevice, ctx->stream), "idx");
+        ck(cudaMemcpyAsync(d_val, val, n * 8, cudaMemcpyHostToDevice, ctx->stream), "val");
+        const bool left = idx[0] != 0, right = idx[n - 1] != length - 1;
+        const int Nk = (int)(n + (left ? 2 : 0) + (right ? 2 : 0));
+        semd::dev::launch_envelope_knots(d_idx, d_val, (long long)n, (long long)length, xs, ys, ctx->stream);
+        semd::dev::launch_envelope(xs, ys, Nk, mom, work, (long long)length, d_out, ctx->stream);
+        ck(cudaGetLastError(), "envelope");
+        ctx->download(out, d_out, length);
+    });
+}
+
+int semd_extract_imf(semd_ctx* ctx, const double* x, size_t n, const semd_sift_cfg* cfg_, double* imf,
+                     int32_t* sift_count) {
+    return guard([&] {
+        need_ctx(ctx);
+        const semd_sift_cfg cfg = sift_or_default(cfg_);
+        if (cfg.max_sift_iters <= 0) {  // the sift loop never runs: the IMF is x itself, 0 sifts
+            const double* d_x0 = ctx->upload(ctx->in_x, x, n);
+            if (sift_count) *sift_count = 0;
+            ctx->download(imf, d_x0, n);
+            return;
+        }
+        if (n < 3) raise(SEMD_INVALID_INPUT, "find_extrema: signal too short (need at least 3 samples)");
+        const double* d_x = ctx->upload(ctx->in_x, x, n);
+        ctx->reset_stats(1);
+        ctx->configure((long long)n, 1, 1, 0);
+        ctx->A.sd_threshold = cfg.sd_threshold;
+        ctx->A.max_sift_iters = cfg.max_sift_iters;
+        ctx->fill_sums(1, -0.0);
+        JobSpec J;
+        J.kmax = 1;
+        J.a = d_x;
+        ctx->set_jobs({J});
+        ctx->run(ctx->max_steps_for(cfg));
+        const Slot& S = ctx->h_slots[0];
+        if (S.ended_insufficient) {
+            const unsigned bad = S.n[0] < 2 ? S.n[0] : S.n[1];
+            raise(SEMD_INSUFFICIENT_EXTREMA, "envelope: need at least 2 extrema, got %u", bad);
+        }
+        int c = 0;
+        ck(cudaMemcpy(&c, ctx->A.imf_sifts, 4, cudaMemcpyDeviceToHost), "count");
+        if (sift_count) *sift_count = c;
+        ctx->download(imf, ctx->A.sums, n);
+    });
+}
+
+int semd_decompose(semd_ctx* ctx, int algo, const double* x, size_t n, const semd_sift_cfg* cfg,
+                   const semd_ens_cfg* ens, double* imfs, size_t k_cap, size_t* k_out, double* residue,
+                   int32_t* sift_counts, semd_trace* trace) {
+    return guard([&] {
+        need_ctx(ctx);
+        size_t K = 0;
+        const double* d_x = ctx->upload(ctx->in_x, x, n);
+        DBuf outb((k_cap + 1) * std::max<size_t>(n, 1) * 8);
+        double* d_imfs = outb.as<double>();
+        double* d_res = d_imfs + k_cap * n;
+        int rc = SEMD_OK;
+        std::string msg;
+        try {
+            ctx->decompose_device(algo, d_x, (long long)n, sift_or_default(cfg), ens_or_default(ens), d_imfs, k_cap, &K,
+                                  d_res, sift_counts, trace);
+        } catch (const Error& e) {
+            if (e.code != SEMD_CAPACITY) throw;
+            rc = e.code;
+            msg = e.msg;
+        }
+        if (k_out) *k_out = K;
+        if (rc) raise(rc, "%s", msg.c_str());
+        if (imfs && K) ctx->download(imfs, d_imfs, K * n);
+        if (residue) ctx->download(residue, d_res, n);
+    });
+}
+
+int semd_decompose_device(semd_ctx* ctx, int algo, const double* d_x, size_t n, const semd_sift_cfg* cfg,
+                          const semd_ens_cfg* ens, double* d_imfs, size_t k_cap, size_t* k_out, double* d_residue) {
+    return guard([&] {
+        need_ctx(ctx);
+        size_t K = 0;
+        try {
+            ctx->decompose_device(algo, d_x, (long long)n, sift_or_default(cfg), ens_or_default(ens), d_imfs, k_cap, &K,
+                                  d_residue, nullptr, nullptr);
+        } catch (...) {
+            if (k_out) *k_out = K;
+            throw;
+        }
+        if (k_out) *k_out = K;
+    });
+}
+
+int semd_eemd_partial_device(semd_ctx* ctx, const double* d_x, size_t n, const semd_sift_cfg* cfg_,
+                             const semd_ens_cfg* ens_, int32_t m_begin, int32_t m_end, double* d_sums, size_t k_cap,
+                             size_t* k_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        const semd_sift_cfg cfg = sift_or_default(cfg_);
+        const semd_ens_cfg ens = ens_or_default(ens_);
+        if (ens.nr < 1) raise(SEMD_INVALID_INPUT, "ensemble: nr must be at least 1");
+        if (ens.nstd < 0.0) raise(SEMD_INVALID_INPUT, "ensemble: nstd must be non-negative");
+        if (m_begin < 0 || m_end < m_begin) raise(SEMD_INVALID_INPUT, "invalid realization range");
+        ctx->reset_stats(1);
+        const int K = m_end > m_begin ? ctx->eemd_partial_device(d_x, (long long)n, cfg, ens, m_begin, m_end, nullptr) : 0;
+        if (k_out) *k_out = (size_t)K;
+        if ((size_t)K > k_cap) raise(SEMD_CAPACITY, "output holds %zu IMFs, shard has %d", k_cap, K);
+        if (k_cap) ck(cudaMemsetAsync(d_sums, 0, k_cap * n * 8, ctx->stream), "zero sums");
+        if (K) ck(cudaMemcpyAsync(d_sums, ctx->A.sums, (size_t)K * n * 8, cudaMemcpyDeviceToDevice, ctx->stream), "sums");
+        ck(cudaStreamSynchronize(ctx->stream), "partial");
+    });
+}
+
+int semd_ensemble_finish_device(semd_ctx* ctx, const double* d_x, size_t n, double* d_sums, size_t K, int32_t nr,
+                                double* d_residue) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (nr < 1) raise(SEMD_INVALID_INPUT, "ensemble: nr must be at least 1");
+        semd::dev::launch_ensemble_finish(d_sums, (int)K, (long long)n, d_x, d_residue, 1.0 / (double)nr, ctx->stream);
+        ck(cudaGetLastError(), "finish");
+        ck(cudaStreamSynchronize(ctx->stream), "finish");
+    });
+}
+
+int semd_white_noise(semd_ctx* ctx, size_t n, uint64_t seed, double std, double* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (std < 0.0) raise(SEMD_INVALID_INPUT, "white_noise: std must be non-negative");
+        if (n == 0) return;
+        if (std == 0.0) {
+            std::fill(out, out + n, 0.0);  // the reference's Signal(n, 0.0)
+            return;
+        }
+        const long long Ls = ((long long)n + 1) / 2 * 2;
+        ctx->scratch.alloc((size_t)Ls * 8);
+        ctx->gen_noise({seed}, (long long)n, Ls, ctx->scratch.as<double>(), std);
+        ctx->download(out, ctx->scratch.as<double>(), n);
+    });
+}
+
+int semd_signal_std(semd_ctx* ctx, const double* x, size_t n, double* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (n == 0) {
+            *out = 0.0;
+            return;
+        }
+        const double* d_x = ctx->upload(ctx->in_x, x, n);
+        *out = ctx->device_std(d_x, (long long)n, 1.0);
+    });
+}
+
+int semd_noise_mode(semd_ctx* ctx, const double* w, size_t n, size_t i, const semd_sift_cfg* cfg, double* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (i == 0) raise(SEMD_INVALID_INPUT, "noise_mode: mode index is 1-based");
+        const double* d_w = ctx->upload(ctx->in_x, w, n);
+        ctx->reset_stats(1);
+        const int K = ctx->emd_device(d_w, (long long)n, sift_or_default(cfg), nullptr);
+        if (i - 1 < (size_t)K) ctx->download(out, ctx->A.sums + (i - 1) * n, n);
+        else std::fill(out, out + n, 0.0);
+    });
+}
+
+int semd_transition_weights(semd_ctx* ctx, size_t d, double* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (d < 1) raise(SEMD_INVALID_INPUT, "transition_weights: D must be at least 1");
+        ctx->scratch2.alloc(d * 8);
+        semd::dev::launch_transition_weights((long long)d, ctx->scratch2.as<double>(), ctx->stream);
+        ctx->download(out, ctx->scratch2.as<double>(), d);
+    });
+}
+
+static int concat_host(semd_ctx* ctx, const double* x, size_t M, size_t N, size_t D, double* out, int naive) {
+    return guard([&] {
+        need_ctx(ctx);
+        validate_serial(M, N, D);
+        const size_t L = M * N + D * (N - 1);
+        const double* d_x = ctx->upload(ctx->in_x, x, M * N);
+        ctx->scratch.alloc(L * 8);
+        concat_device(ctx, d_x, M, N, D, ctx->scratch.as<double>(), naive);
+        ctx->download(out, ctx->scratch.as<double>(), L);
+    });
+}
+
+int semd_concatenate(semd_ctx* ctx, const double* x, size_t M, size_t N, size_t D, double* out) {
+    return concat_host(ctx, x, M, N, D, out, 0);
+}
+int semd_concatenate_naive(semd_ctx* ctx, const double* x, size_t M, size_t N, size_t D, double* out) {
+    return concat_host(ctx, x, M, N, D, out, 1);
+}
+
+int semd_deconcatenate(semd_ctx* ctx, const double* modes, size_t K, size_t L, size_t M, size_t N, size_t D,
+                       double* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        validate_deconcat(K, L, M, N, D);
+        const double* d_m = ctx->upload(ctx->in_x, modes, K * L);
+        ctx->scratch.alloc(K * M * N * 8);
+        semd::dev::launch_deconcatenate(d_m, (long long)K, (long long)L, (long long)M, (long long)N, (long long)D,
+                                        ctx->scratch.as<double>(), ctx->stream);
+        ck(cudaGetLastError(), "deconcatenate");
+        ctx->download(out, ctx->scratch.as<double>(), K * M * N);
+    });
+}
+
+static void serial_device(semd_ctx* ctx, int algo, const double* d_x, size_t M, size_t N, size_t D,
+                          const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* d_tensor, size_t k_cap,
+                          size_t* modes_out, semd_trace* trace) {
+    validate_serial(M, N, D);
+    const size_t L = M * N + D * (N - 1);
+    DBuf sig(L * 8);
+    concat_device(ctx, d_x, M, N, D, sig.as<double>(), 0);
+    ck(cudaStreamSynchronize(ctx->stream), "concatenate");
+    // modes = imfs + residue, row k contiguous
+    size_t kc = std::max<size_t>(k_cap, 1);
+    DBuf modes;
+    size_t K = 0;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        modes.alloc((kc + 1) * L * 8);
+        try {
+            ctx->decompose_device(algo, sig.as<double>(), (long long)L, sift_or_default(cfg), ens_or_default(ens),
+                                  modes.as<double>(), kc, &K, modes.as<double>() + kc * L, nullptr, trace);
+            break;
+        } catch (const Error& e) {
+            if (e.code != SEMD_CAPACITY) throw;
+            kc = std::max(kc * 2, K);
+        }
+    }
+    if (K != kc)  // move the residue right after the K IMFs
+        ck(cudaMemcpyAsync(modes.as<double>() + K * L, modes.as<double>() + kc * L, L * 8, cudaMemcpyDeviceToDevice,
+                           ctx->stream),
+           "residue");
+    *modes_out = K + 1;
+    if (K + 1 > k_cap) raise(SEMD_CAPACITY, "output holds %zu modes, decomposition has %zu", k_cap, K + 1);
+    validate_deconcat(K + 1, L, M, N, D);
+    semd::dev::launch_deconcatenate(modes.as<double>(), (long long)(K + 1), (long long)L, (long long)M, (long long)N,
+                                    (long long)D, d_tensor, ctx->stream);
+    ck(cudaGetLastError(), "deconcatenate");
+    ck(cudaStreamSynchronize(ctx->stream), "serial");
+}
+
+int semd_serial_decompose(semd_ctx* ctx, int algo, const double* x, size_t M, size_t N, size_t D,
+                          const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* tensor, size_t k_cap,
+                          size_t* modes_out, semd_trace* trace) {
+    return guard([&] {
+        need_ctx(ctx);
+        validate_serial(M, N, D);
+        const double* d_x = ctx->upload(ctx->in_x, x, M * N);
+        DBuf t(std::max<size_t>(k_cap, 1) * M * N * 8);
+        size_t mo = 0;
+        try {
+            serial_device(ctx, algo, d_x, M, N, D, cfg, ens, t.as<double>(), k_cap, &mo, trace);
+        } catch (...) {
+            if (modes_out) *modes_out = mo;
+            throw;
+        }
+        if (modes_out) *modes_out = mo;
+        ctx->download(tensor, t.as<double>(), mo * M * N);
+    });
+}
+
+int semd_serial_decompose_device(semd_ctx* ctx, int algo, const double* d_x, size_t M, size_t N, size_t D,
+                                 const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* d_tensor, size_t k_cap,
+                                 size_t* modes_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        size_t mo = 0;
+        try {
+            serial_device(ctx, algo, d_x, M, N, D, cfg, ens, d_tensor, k_cap, &mo, nullptr);
+        } catch (...) {
+            if (modes_out) *modes_out = mo;
+            throw;
+        }
+        if (modes_out) *modes_out = mo;
+    });
+}
+
+}  // extern "C"

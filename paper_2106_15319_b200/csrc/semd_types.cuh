@@ -1,0 +1,147 @@
+// semd_types.cuh -- device-side data layout of the serial-EMD sift engine.
+//
+// One "slot" runs one sifting job (the IMF loop of emd(), emd.cpp:155-172, on
+// one signal: a plain EMD input, one EEMD realization x + beta*w_m, or one
+// CEEMDAN task). G slots advance together, one phase per kernel launch
+// ("lockstep steps"); all per-slot state lives in HBM so no host round trip is
+// needed between sift iterations.
+//
+// HBM layout per engine (L = serialized length, G = slots, T = eval tile):
+//   bufs    f64 [G][3][L]        rotating X (IMF input), C (candidate), R (next residue)
+//   kidx    i32 [2 par][2 side][G][cap]   compacted extrema indices (cap = L/2+2)
+//   kval    f64 [2][2][G][cap]            extrema values
+//   toff    u32 [2][2][G][tiles+1]        exclusive per-tile knot offsets
+//   mom     f64 [2 side][G][cap+4]        spline moments of the mirrored knot system
+//   status  u64 [2 side][G][tiles]        decoupled look-back words (epoch|flag|count)
+//   tnum/tden/thash [G][tiles]            per-tile SD and trace-hash partials
+//   sums    f64 [kcap][L]                 ensemble / IMF accumulators
+#pragma once
+#include <cstdint>
+
+namespace semd {
+namespace dev {
+
+constexpr int kEvalTile = 2048;                 // samples per eval tile
+constexpr int kEvalThreads = 256;
+constexpr int kSpt = kEvalTile / kEvalThreads;  // samples per thread (consecutive)
+constexpr int kKnotCapTile = kEvalTile / 2 + 4; // knots of one side touching a tile
+
+constexpr int kSolveThreads = 128;                       // speculative chains per block
+constexpr int kSolveChunk = 32;                          // rows per chain
+constexpr int kSolveBlock = kSolveThreads * kSolveChunk; // rows per CTA
+constexpr int kSolveHalo = 64;                           // cross-block warm-up rows
+constexpr int kSolveSeqMax = 96;                         // rows solved by one exact thread
+
+constexpr int kFinalTile = 1024;
+
+enum State : int {
+    ST_FREE = 0,
+    ST_INIT = 1,    // materialise X from the job's input, then detect (iteration 0)
+    ST_DETECT = 2,  // detect extrema of X (iteration 0 of the next IMF)
+    ST_SIFT = 3,    // one sift per step
+    ST_WAITK = 4,   // IMF converged; waiting for every slot to reach the same IMF (lockstep)
+    ST_FINAL = 5,   // residue update + accumulation this step
+    ST_DONE = 6,
+};
+
+enum EvalMode : int { EM_NONE = 0, EM_INIT = 1, EM_DETECT = 2, EM_SIFT = 3 };
+
+struct Slot {
+    // ---- job description (host-written before ST_INIT) ----
+    int m;          // realization index (trace id)
+    int task;       // trace task id (0 emd, 1 ceemdan noise IMF, 2 ceemdan first mode)
+    int kmax;       // IMF limit of this job (0: unlimited)
+    int k0;         // IMF k accumulates into sums row k0 + k
+    int init_kind;  // 0: X = a ; 1: X = a + beta*b ; 2: X = a (zero IMFs allowed) ...
+    int write_imf;  // 1: IMFs are accumulated (sums[k0+k] += imf)
+    double beta;
+    const double* init_a;
+    const double* init_b;
+    double* imf_out;      // single-IMF jobs: the IMF is also written here by k_final
+    double* res_out;      // single-IMF jobs: the residue x - imf is also written here
+    int detect_only;      // job = one find_extrema call (CEEMDAN stage check), then DONE
+    // ---- dynamic state (device-written) ----
+    int state;
+    int k;       // IMFs completed
+    int iter;    // sifts done on the current IMF
+    int par;     // knot-set parity holding the current extrema
+    int xb;      // buffer id of X
+    int cb;      // buffer id of the current candidate (-1: X)
+    int db;      // destination buffer of this step's eval
+    unsigned epoch;
+    unsigned n[2];       // extrema counts (max, min) of the current knot set
+    int ended_insufficient;
+    int last_imf_b;      // buffer id that held the last finalised IMF
+    int hazards;         // speculative-solve boundary mismatches observed
+    long long sifted;    // sifted samples (L per completed sift)
+    double num, den;
+};
+
+struct TraceRec {
+    int32_t task, m, k, iter;
+    uint32_t n_max, n_min;
+    uint64_t hash;
+};
+
+// Control block: work lists and kernel bookkeeping (device memory).
+struct Ctrl {
+    unsigned ticket[4];
+    unsigned done[4];
+    int n_eval;    // slots with an eval-phase job this step
+    int n_final;   // slots finalising this step
+    int n_solve;   // (slot, side) solve items
+    int solve_blocks;  // total blocks over solve items
+    int active;    // slots not FREE/DONE
+    int trace_count;
+    int hazards;
+    int k_overflow;
+    int step;
+    int pad[7];
+};
+
+struct Arena {
+    int L, G, tiles, cap, kcap;
+    double sd_threshold;
+    int max_sift_iters;
+    int trace_cap;
+    double* bufs;
+    int* kidx;
+    double* kval;
+    unsigned* toff;
+    double* mom;
+    unsigned long long* status;
+    double* tnum;
+    double* tden;
+    unsigned long long* thash;
+    Slot* slots;
+    double* sums;
+    int* imf_sifts;   // [kcap] sift count per IMF of slot 0 (plain EMD / extract_imf)
+    Ctrl* ctrl;
+    int* eval_list;   // [G]
+    int* final_list;  // [G]
+    int* solve_item;  // [2G] (slot << 1 | side)
+    int* solve_off;   // [2G+1] block prefix
+    double* sb;       // [2][G][max_blocks][4] solve block boundary values
+    int max_blocks;
+    TraceRec* trace;
+    int* status_host; // mapped pinned: [0] active slots after this step, [1] step counter
+};
+
+__host__ __device__ inline size_t buf_off(const Arena& a, int slot, int b) {
+    return ((size_t)slot * 3 + (size_t)b) * (size_t)a.L;
+}
+__host__ __device__ inline size_t knot_off(const Arena& a, int par, int side, int slot) {
+    return (((size_t)par * 2 + side) * a.G + slot) * (size_t)a.cap;
+}
+__host__ __device__ inline size_t toff_off(const Arena& a, int par, int side, int slot) {
+    return (((size_t)par * 2 + side) * a.G + slot) * (size_t)(a.tiles + 1);
+}
+__host__ __device__ inline size_t mom_off(const Arena& a, int side, int slot) {
+    return ((size_t)side * a.G + slot) * (size_t)(a.cap + 4);
+}
+__host__ __device__ inline size_t status_off(const Arena& a, int side, int slot) {
+    return ((size_t)side * a.G + slot) * (size_t)a.tiles;
+}
+
+}  // namespace dev
+}  // namespace semd
