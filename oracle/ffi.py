@@ -330,6 +330,9 @@ class Ref:
             self.lib.ref_out_free(o)
         return imfs_, res
 
+    def emd(self, x, **kw):
+        return self.decompose(x, 0, **kw)
+
     def emd_traced(self, x, sd=0.2, iters=300, imfs=0):
         x = _f64(x)
         o = self.lib.ref_out_new()

@@ -101,6 +101,13 @@ class Context:
     def set_stream(self, stream_ptr: int | None):
         self.check(self.lib.semd_set_stream(self.ptr, C.c_void_p(stream_ptr or 0)))
 
+    def mt19937_64(self, seed: int, n: int) -> np.ndarray:
+        """TEST HOOK: raw device std::mt19937_64 draws."""
+        out = np.zeros(max(n, 1), dtype=np.uint64)
+        self.check(self.lib.semd_mt19937_64_device_test(self.ptr, C.c_uint64(seed), n,
+                                                        out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out[:n]
+
     def set_noise_override(self, noise: np.ndarray | None):
         """TEST HOOK: use the given (nr, n) noise instead of the device RNG."""
         if noise is None:

@@ -1,0 +1,432 @@
+// semd_aux.cu -- sm_100a kernels around the sift engine: the noise streams
+// (std::mt19937_64 + Box-Muller, emd.cpp:181-200), the exact signal_std
+// (emd.cpp:209-217), ensemble finish (:252-260), CEEMDAN stage means
+// (:301-306, :331-338), the serializer / deserializer (serialize.cpp:7-95) and
+// the standalone envelope() entry (emd.cpp:41-125).
+// Compiled with -fmad=false (reference rounding, see semd_device.cuh).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "semd_device.cuh"
+#include "semd_launch.h"
+#include "semd_types.cuh"
+
+namespace semd {
+namespace dev {
+
+// -------------------------------------------------------------- RNG
+//
+// std::mt19937_64 ([rand.predef]) for one realization per CTA: the 312-word
+// twist is done in three data-parallel phases, then tempering; draws are
+// written as raw u64. k_box_muller maps draw pairs exactly like
+// white_noise (emd.cpp:189-198).
+
+__device__ __forceinline__ uint64_t mt_twist(uint64_t a, uint64_t b) {
+    const uint64_t x = (a & 0xFFFFFFFF80000000ULL) | (b & 0x7FFFFFFFULL);
+    uint64_t xa = x >> 1;
+    if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+    return xa;
+}
+
+__global__ void __launch_bounds__(320) k_mt19937_64(const RngJob* jobs) {
+    __shared__ uint64_t mt[312];
+    const RngJob J = jobs[blockIdx.x];
+    const int t = threadIdx.x;
+    if (t == 0) {
+        mt[0] = J.seed;
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+    }
+    __syncthreads();
+    const long long ndraw = 2 * ((J.n + 1) / 2);
+    for (long long base = 0; base < ndraw; base += 312) {
+        uint64_t a = 0, b = 0, c = 0;
+        if (t < 312) {
+            a = mt[t];
+            b = mt[(t + 1) % 312];
+            c = mt[(t + 156) % 312];
+        }
+        __syncthreads();
+        if (t < 156) mt[t] = c ^ mt_twist(a, b);
+        __syncthreads();
+        if (t >= 156 && t < 311) mt[t] = mt[t - 156] ^ mt_twist(a, b);
+        if (t == 311) mt[311] = mt[155] ^ mt_twist(a, mt[0]);
+        __syncthreads();
+        if (t < 312 && base + t < ndraw) {
+            uint64_t y = mt[t];
+            y ^= (y >> 29) & 0x5555555555555555ULL;
+            y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+            y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+            y ^= y >> 43;
+            J.out[base + t] = y;
+        }
+    }
+}
+
+// In place: draws (u64 pairs) -> Gaussian samples (f64), emd.cpp:189-198.
+__global__ void k_box_muller(uint64_t* draws, long long n, double stdv) {
+    const long long pairs = (n + 1) / 2;
+    const double two_pi = 6.283185307179586476925286766559;
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < pairs;
+         p += (long long)gridDim.x * blockDim.x) {
+        const uint64_t d1 = draws[2 * p], d2 = draws[2 * p + 1];
+        const double u1 = (double)((d1 >> 11) + 1) * 0x1.0p-53;
+        const double r = stdv * sqrt(-2.0 * log(u1));
+        const double u2 = (double)((d2 >> 11) + 1) * 0x1.0p-53;
+        const double theta = two_pi * u2;
+        double* out = reinterpret_cast<double*>(draws);
+        out[2 * p] = r * cos(theta);
+        if (2 * p + 1 < n) out[2 * p + 1] = r * sin(theta);
+    }
+}
+
+// ------------------------------------------------------------ small kernels
+
+// emd.cpp:209-217 verbatim: two passes of SEQUENTIAL sums (the reference's
+// rounding), fed through shared memory. Warp 1 streams chunks (pass 2: the
+// squared deviations) while lane 0 of warp 0 performs the dependent additions,
+// so the cost is one fp64 add latency per sample and pass.
+constexpr int kStdChunk = 2048;
+// signals up to this length get the reference's exact sequential sums
+constexpr long long kStdExactMax = 1LL << 22;
+__global__ void __launch_bounds__(64) k_signal_std(const double* x, long long n, double* out, double scale) {
+    __shared__ double buf[2][kStdChunk];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (n == 0) {
+        if (threadIdx.x == 0) *out = 0.0;
+        return;
+    }
+    const long long nch = (n + kStdChunk - 1) / kStdChunk;
+    double mean = 0.0, acc = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+        auto fill = [&](long long c) {
+            const long long o = c * kStdChunk;
+            const int len = (int)min((long long)kStdChunk, n - o);
+            double* d = buf[c & 1];
+            for (int i = lane; i < len; i += 32) {
+                const double v = x[o + i];
+                d[i] = pass == 0 ? v : (v - mean) * (v - mean);
+            }
+        };
+        if (warp == 1) fill(0);
+        __syncthreads();
+        double s = 0.0;
+        for (long long c = 0; c < nch; ++c) {
+            if (warp == 1 && c + 1 < nch) fill(c + 1);
+            if (warp == 0 && lane == 0) {
+                const double* d = buf[c & 1];
+                const int len = (int)min((long long)kStdChunk, n - c * kStdChunk);
+                int i = 0;
+                for (; i + 8 <= len; i += 8) {
+                    const double v0 = d[i], v1 = d[i + 1], v2 = d[i + 2], v3 = d[i + 3];
+                    const double v4 = d[i + 4], v5 = d[i + 5], v6 = d[i + 6], v7 = d[i + 7];
+                    s += v0; s += v1; s += v2; s += v3; s += v4; s += v5; s += v6; s += v7;
+                }
+                for (; i < len; ++i) s += d[i];
+            }
+            __syncthreads();
+        }
+        if (warp == 0 && lane == 0) {
+            if (pass == 0) buf[0][0] = s / (double)n;  // mean /= n
+            else acc = s;
+        }
+        __syncthreads();
+        if (pass == 0) mean = buf[0][0];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = scale * sqrt(acc / (double)n);
+}
+
+// signal_std for long signals (n > kStdExactMax): the same two-pass formula
+// with each pass summed by a deterministic parallel double-double (TwoSum)
+// reduction, i.e. the nearly correctly rounded sum instead of the reference's
+// sequentially rounded one (difference ~sqrt(n) ulp of the sum; documented in
+// DESIGN.md). Fixed reduction tree -> bitwise reproducible run to run.
+constexpr int kStdBlocks = 256;
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = a + b;
+    const double bb = s - a;
+    e = (a - (s - bb)) + (b - bb);
+}
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double v) {
+    double s, e;
+    two_sum(hi, v, s, e);
+    hi = s;
+    lo += e;
+}
+__global__ void __launch_bounds__(256) k_std_partial(const double* x, long long n, const double* mean_in, double* part) {
+    __shared__ double sh[2][256];
+    const double mean = mean_in ? *mean_in : 0.0;
+    double hi = 0.0, lo = 0.0;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
+        const double v = mean_in ? (x[i] - mean) * (x[i] - mean) : x[i];
+        dd_add(hi, lo, v);
+    }
+    sh[0][threadIdx.x] = hi;
+    sh[1][threadIdx.x] = lo;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            double s, e;
+            two_sum(sh[0][threadIdx.x], sh[0][threadIdx.x + o], s, e);
+            sh[0][threadIdx.x] = s;
+            sh[1][threadIdx.x] += sh[1][threadIdx.x + o] + e;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = sh[0][0];
+        part[2 * blockIdx.x + 1] = sh[1][0];
+    }
+}
+__global__ void k_std_final(const double* part, int nb, long long n, double* mean_out, double* out, double scale,
+                            int stage) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double hi = 0.0, lo = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        dd_add(hi, lo, part[2 * b]);
+        lo += part[2 * b + 1];
+    }
+    const double s = hi + lo;
+    if (stage == 0) *mean_out = s / (double)n;
+    else *out = scale * sqrt(s / (double)n);
+}
+
+// eemd finish (emd.cpp:252-260): imfs *= 1/nr ; residue = x - sum_k imf_k (k order).
+__global__ void k_ensemble_finish(double* sums, int K, long long L, const double* x, double* residue, double inv) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < L; t += (long long)gridDim.x * blockDim.x) {
+        double r = x[t];
+        for (int k = 0; k < K; ++k) {
+            const double v = sums[(size_t)k * L + t] * inv;
+            sums[(size_t)k * L + t] = v;
+            r -= v;
+        }
+        residue[t] = r;
+    }
+}
+
+// serialize.cpp:30-50: channel copy + blended transitions (2 mul + 1 add, no FMA).
+__global__ void k_concatenate(const double* x, long long M, long long N, long long D, const double* a, double* out,
+                              int naive) {
+    const long long L = M * N + D * (N - 1);
+    const long long stride = M + D;
+    for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < L; o += (long long)gridDim.x * blockDim.x) {
+        const long long j = o / stride, p = o % stride;
+        if (p < M) {
+            out[o] = x[j * M + p];
+        } else {
+            const long long t = p - M;  // transition sample t of block j
+            const double* ch = x + j * M;
+            const double* next = x + (j + 1) * M;
+            if (!naive) {
+                out[o] = next[D - 1 - t] * a[t] + ch[M - 1 - t] * a[D - 1 - t];
+            } else {  // serialize.cpp:64-67, i = t + 1
+                const long long i = t + 1;
+                const double wg = (double)i / (double)(D + 1);
+                const double wf = (double)(D + 1 - i) / (double)(D + 1);
+                out[o] = wg * next[D - i] + wf * ch[M - i];
+            }
+        }
+    }
+}
+
+// serialize.cpp:7-13
+__global__ void k_transition_weights(long long d, double* a) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < d; i += (long long)gridDim.x * blockDim.x)
+        a[i] = (double)(i + 1) / (double)(d + 1);
+}
+
+// serialize.cpp:86-93: out[(k*N+j)*M+i] = modes[k][j*(M+D)+i]
+__global__ void k_deconcatenate(const double* modes, long long K, long long Lm, long long M, long long N, long long D,
+                                double* out) {
+    const long long total = K * N * M;
+    for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < total;
+         o += (long long)gridDim.x * blockDim.x) {
+        const long long i = o % M, kj = o / M, j = kj % N, k = kj / N;
+        out[o] = modes[k * Lm + j * (M + D) + i];
+    }
+}
+
+// General envelope (emd.cpp:91-125) for the standalone envelope() entry:
+// conditional mirrors, the two-knot line (:46-51), sequential Thomas in one
+// thread, parallel evaluation. xs/ys built on the host side of the kernel.
+__global__ void k_envelope_solve(const double* xs, const double* ys, int n, double* mom, double* work) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (n == 2) return;
+    double* diag = work;
+    double* rhs = work + n;
+    for (int i = 1; i + 1 < n; ++i) {  // emd.cpp:57-63
+        const double h0 = xs[i] - xs[i - 1];
+        const double h1 = xs[i + 1] - xs[i];
+        diag[i] = 2.0 * (h0 + h1);
+        rhs[i] = 6.0 * ((ys[i + 1] - ys[i]) / h1 - (ys[i] - ys[i - 1]) / h0);
+    }
+    for (int i = 2; i + 1 < n; ++i) {  // :64-69
+        const double h0 = xs[i] - xs[i - 1];
+        const double w = h0 / diag[i - 1];
+        diag[i] -= w * (xs[i] - xs[i - 1]);
+        rhs[i] -= w * rhs[i - 1];
+    }
+    double m = 0.0;  // :70-73
+    mom[n - 1] = 0.0;
+    for (int i = n - 2; i >= 1; --i) {
+        m = (rhs[i] - (xs[i + 1] - xs[i]) * m) / diag[i];
+        mom[i] = m;
+    }
+    mom[0] = 0.0;
+}
+
+__global__ void k_envelope_eval(const double* xs, const double* ys, const double* mom, int n, long long length,
+                                double* out) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < length;
+         t += (long long)gridDim.x * blockDim.x) {
+        const double tt = (double)t;
+        if (n == 2) {
+            const double slope = (ys[1] - ys[0]) / (xs[1] - xs[0]);
+            out[t] = ys[0] + slope * (tt - xs[0]);
+            continue;
+        }
+        // seg = the reference's march result: largest seg <= n-2 with seg==0 or tt > xs[seg]
+        int lo = 0, hi = n - 2;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            bool passed = true;  // the march passes xs[1..mid] iff tt > xs[q] for all q <= mid
+            passed = tt > xs[mid];
+            if (passed) lo = mid;
+            else hi = mid - 1;
+        }
+        // the march stops at the first seg with tt <= xs[seg+1]; with increasing xs on the
+        // evaluated range this is the largest seg with tt > xs[seg] (or 0)
+        const int seg = lo;
+        out[t] = spline_eval_ref(xs[seg], xs[seg + 1], ys[seg], ys[seg + 1], mom[seg], mom[seg + 1], tt);
+    }
+}
+
+// CEEMDAN stage mean (emd.cpp:301-304 / :331-336): mode *= inv, flag any nonzero.
+__global__ void k_stage_scale(double* mode, long long n, double inv, int* nonzero) {
+    int nz = 0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+        const double v = mode[t] * inv;
+        mode[t] = v;
+        if (v != 0.0) nz = 1;
+    }
+    if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(nonzero, 1);
+}
+
+// residue -= mode (emd.cpp:304 / :338)
+__global__ void k_sub(double* residue, const double* mode, long long n) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+        residue[t] = residue[t] - mode[t];
+}
+
+// Knot vector of a general envelope() call (emd.cpp:98-122): optional mirrors.
+__global__ void k_envelope_knots(const unsigned long long* idx, const double* val, long long n, long long length,
+                                 double* xs, double* ys) {
+    const bool left = idx[0] != 0, right = idx[n - 1] != (unsigned long long)(length - 1);
+    const long long off = left ? 2 : 0;
+    const long long N = n + off + (right ? 2 : 0);
+    const double end = (double)(length - 1);
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < N; v += (long long)gridDim.x * blockDim.x) {
+        if (v < off) {  // descending source order: k = 1 then 0
+            const long long k = 1 - v;
+            xs[v] = -(double)idx[k];
+            ys[v] = val[k];
+        } else if (v < off + n) {
+            xs[v] = (double)idx[v - off];
+            ys[v] = val[v - off];
+        } else {
+            const long long k = n - 2 + (v - off - n);
+            xs[v] = 2.0 * end - (double)idx[k];
+            ys[v] = val[k];
+        }
+    }
+}
+
+__global__ void k_fill(double* p, long long n, double v) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+        p[t] = v;
+}
+
+// Copy one slot buffer (e.g. the final residue) out.
+__global__ void k_copy(const double* src, double* dst, long long n) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+        dst[t] = src[t];
+}
+
+// X = a + beta * b (CEEMDAN first-mode input, emd.cpp:297 / :327)
+__global__ void k_axpy(const double* a, const double* b, double beta, double* out, long long n) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+        out[t] = a[t] + beta * b[t];
+}
+
+}  // namespace dev
+}  // namespace semd
+
+// ------------------------------------------------------------ launchers
+namespace semd {
+namespace dev {
+
+void launch_rng(const RngJob* jobs, int njobs, cudaStream_t st) { k_mt19937_64<<<njobs, 320, 0, st>>>(jobs); }
+void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t st) {
+    const long long pairs = (n + 1) / 2;
+    const int grid = (int)((pairs + 255) / 256 < 4096 ? (pairs + 255) / 256 : 4096);
+    k_box_muller<<<grid > 0 ? grid : 1, 256, 0, st>>>(draws, n, stdv);
+}
+void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st) {
+    if (n <= kStdExactMax) {
+        k_signal_std<<<1, 64, 0, st>>>(x, n, out, scale);
+        return;
+    }
+    // out[1] = mean scratch, out[2..] = block partials
+    double* mean = out + 1;
+    double* part = out + 2;
+    k_std_partial<<<kStdBlocks, 256, 0, st>>>(x, n, nullptr, part);
+    k_std_final<<<1, 32, 0, st>>>(part, kStdBlocks, n, mean, out, scale, 0);
+    k_std_partial<<<kStdBlocks, 256, 0, st>>>(x, n, mean, part);
+    k_std_final<<<1, 32, 0, st>>>(part, kStdBlocks, n, mean, out, scale, 1);
+}
+static int grid_for(long long n) {
+    long long g = (n + 255) / 256;
+    if (g > 8192) g = 8192;
+    return g < 1 ? 1 : (int)g;
+}
+void launch_ensemble_finish(double* sums, int K, long long L, const double* x, double* residue, double inv,
+                            cudaStream_t st) {
+    k_ensemble_finish<<<grid_for(L), 256, 0, st>>>(sums, K, L, x, residue, inv);
+}
+void launch_concatenate(const double* x, long long M, long long N, long long D, const double* a, double* out,
+                        int naive, cudaStream_t st) {
+    k_concatenate<<<grid_for(M * N + D * (N - 1)), 256, 0, st>>>(x, M, N, D, a, out, naive);
+}
+void launch_transition_weights(long long d, double* a, cudaStream_t st) {
+    k_transition_weights<<<grid_for(d), 256, 0, st>>>(d, a);
+}
+void launch_deconcatenate(const double* modes, long long K, long long Lm, long long M, long long N, long long D,
+                          double* out, cudaStream_t st) {
+    k_deconcatenate<<<grid_for(K * N * M), 256, 0, st>>>(modes, K, Lm, M, N, D, out);
+}
+void launch_envelope(const double* xs, const double* ys, int n, double* mom, double* work, long long length,
+                     double* out, cudaStream_t st) {
+    k_envelope_solve<<<1, 32, 0, st>>>(xs, ys, n, mom, work);
+    k_envelope_eval<<<grid_for(length), 256, 0, st>>>(xs, ys, mom, n, length, out);
+}
+void launch_stage_scale(double* mode, long long n, double inv, int* nonzero, cudaStream_t st) {
+    k_stage_scale<<<grid_for(n), 256, 0, st>>>(mode, n, inv, nonzero);
+}
+void launch_sub(double* residue, const double* mode, long long n, cudaStream_t st) {
+    k_sub<<<grid_for(n), 256, 0, st>>>(residue, mode, n);
+}
+void launch_envelope_knots(const unsigned long long* idx, const double* val, long long n, long long length,
+                           double* xs, double* ys, cudaStream_t st) {
+    k_envelope_knots<<<grid_for(n + 4), 256, 0, st>>>(idx, val, n, length, xs, ys);
+}
+void launch_fill(double* p, long long n, double v, cudaStream_t st) { k_fill<<<grid_for(n), 256, 0, st>>>(p, n, v); }
+void launch_copy(const double* src, double* dst, long long n, cudaStream_t st) {
+    k_copy<<<grid_for(n), 256, 0, st>>>(src, dst, n);
+}
+void launch_axpy(const double* a, const double* b, double beta, double* out, long long n, cudaStream_t st) {
+    k_axpy<<<grid_for(n), 256, 0, st>>>(a, b, beta, out, n);
+}
+
+}  // namespace dev
+}  // namespace semd

@@ -120,7 +120,7 @@ struct semd_ctx {
     // engine arena
     Arena A{};
     int cfg_L = -1, cfg_G = -1, cfg_kcap = -1, cfg_trace = -1;
-    DBuf bufs, kidx, kval, toff, mom, status, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace;
+    DBuf bufs, kidx, kval, toff, mom, sidx, sval, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace;
     int* status_host = nullptr;
     int* status_host_dev = nullptr;
     std::vector<Slot> h_slots;
@@ -149,12 +149,15 @@ struct semd_ctx {
         const int cap = (int)(L / 2 + 2);
         const int rows_max = cap + 2;
         const int max_blocks = rows_max / semd::dev::kSolveBlock + 2;
-        bufs.alloc((size_t)G * 3 * L * 8);
+        const long long Lp = (L + 63) / 64 * 64;
+        bufs.alloc((size_t)G * 3 * Lp * 8);
         kidx.alloc((size_t)4 * G * cap * 4);
         kval.alloc((size_t)4 * G * cap * 8);
         toff.alloc((size_t)4 * G * (tiles + 1) * 4);
         mom.alloc((size_t)2 * G * (cap + 4) * 8);
-        status.alloc((size_t)2 * G * tiles * 8);
+        sidx.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 4);
+        sval.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 8);
+        scnt.alloc((size_t)2 * G * tiles * 4);
         tnum.alloc((size_t)G * tiles * 8);
         tden.alloc((size_t)G * tiles * 8);
         thash.alloc((size_t)G * tiles * 8);
@@ -162,11 +165,12 @@ struct semd_ctx {
         sums.alloc((size_t)kcap * L * 8);
         imf_sifts.alloc((size_t)kcap * 4);
         ctrl.alloc(sizeof(Ctrl));
-        lists.alloc((size_t)(G + G + 2 * G + 2 * G + 1) * 4);
+        lists.alloc((size_t)(G + G + G + 2 * G + 2 * G + 1) * 4);
         sb.alloc((size_t)2 * G * max_blocks * 6 * 8);
         if (trace_cap > 0) trace.alloc((size_t)trace_cap * sizeof(TraceRec));
         A = Arena{};
         A.L = (int)L;
+        A.Lp = Lp;
         A.G = G;
         A.tiles = tiles;
         A.cap = cap;
@@ -176,7 +180,9 @@ struct semd_ctx {
         A.kval = kval.as<double>();
         A.toff = toff.as<unsigned>();
         A.mom = mom.as<double>();
-        A.status = status.as<unsigned long long>();
+        A.sidx = sidx.as<int>();
+        A.sval = sval.as<double>();
+        A.scnt = scnt.as<unsigned>();
         A.tnum = tnum.as<double>();
         A.tden = tden.as<double>();
         A.thash = thash.as<unsigned long long>();
@@ -187,15 +193,14 @@ struct semd_ctx {
         int* l = lists.as<int>();
         A.eval_list = l;
         A.final_list = l + G;
-        A.solve_item = l + 2 * G;
-        A.solve_off = l + 4 * G;
+        A.compact_list = l + 2 * G;
+        A.solve_item = l + 3 * G;
+        A.solve_off = l + 5 * G;
         A.sb = sb.as<double>();
         A.max_blocks = max_blocks;
         A.trace = trace_cap > 0 ? trace.as<TraceRec>() : nullptr;
         A.trace_cap = trace_cap;
         A.status_host = status_host_dev;
-        // look-back words and toff start clean (epoch 0 never matches)
-        ck(cudaMemsetAsync(status.p, 0, status.bytes, stream), "memset status");
         ck(cudaMemsetAsync(toff.p, 0, toff.bytes, stream), "memset toff");
         ck(cudaMemsetAsync(sb.p, 0, sb.bytes, stream), "memset sb");
         cfg_L = (int)L;
@@ -277,7 +282,7 @@ struct semd_ctx {
         if (timing) ck(cudaEventRecord(t0, stream), "event");
         for (;; ++step) {
             semd::dev::launch_step(A, sms, stream);
-            stats.kernel_launches += 3;
+            stats.kernel_launches += 5;
             stats.eval_launches += 1;
             ck(cudaGetLastError(), "launch step");
             ck(cudaEventRecord(ev[step % R], stream), "event record");
@@ -398,7 +403,7 @@ struct semd_ctx {
     }
 
     double device_std(const double* d_x, long long n, double scale) {
-        scalar.alloc(16);
+        scalar.alloc((2 + 2 * 256 + 8) * 8);
         semd::dev::launch_signal_std(d_x, n, scalar.as<double>(), scale, stream);
         double v = 0.0;
         ck(cudaMemcpyAsync(&v, scalar.p, 8, cudaMemcpyDeviceToHost, stream), "std");
@@ -808,6 +813,22 @@ int semd_set_noise_override(semd_ctx* ctx, const double* noise, size_t nr, size_
         ctx->in_y.alloc(nr * n * 8);
         ck(cudaMemcpy(ctx->in_y.p, noise, nr * n * 8, cudaMemcpyHostToDevice), "noise override");
         ctx->noise_override = ctx->in_y.as<double>();
+    });
+}
+
+// Test hook: the raw std::mt19937_64 stream generated on the device.
+int semd_mt19937_64_device_test(semd_ctx* ctx, uint64_t seed, size_t n, uint64_t* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        const size_t n2 = (n + 1) / 2 * 2;
+        DBuf d(std::max<size_t>(n2, 2) * 8);
+        semd::dev::RngJob job{seed, d.as<uint64_t>(), (long long)n2};
+        DBuf dj(sizeof(job));
+        ck(cudaMemcpy(dj.p, &job, sizeof(job), cudaMemcpyHostToDevice), "job");
+        semd::dev::launch_rng(dj.as<semd::dev::RngJob>(), 1, ctx->stream);
+        ck(cudaGetLastError(), "rng");
+        ck(cudaStreamSynchronize(ctx->stream), "rng");
+        if (n) ck(cudaMemcpy(out, d.p, n * 8, cudaMemcpyDeviceToHost), "draws");
     });
 }
 

@@ -1,0 +1,1200 @@
+// semd_sift.cu -- the sm_100a sift engine: one lockstep step =
+//   k_solve   spline moments of every sifting slot's envelopes   (emd.cpp:53-73)
+//   k_eval    mean-envelope subtraction + SD partials + extrema  (emd.cpp:10-35, :75-86, :142-148)
+//   k_scan    per-slot tile prefix of the new extrema + SD sums; epilogue = stop rules (:131-151)
+//   k_compact ordered extrema lists for the next solve + parity-trace hashes
+//   k_final   residue update and ensemble accumulation           (emd.cpp:167, :246-251)
+// Paths relative to /root/reference/proj/src. Compiled with -fmad=false: the
+// arithmetic mirrors the reference's -ffp-contract=off build bit-for-bit.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "semd_device.cuh"
+#include "semd_launch.h"
+#include "semd_types.cuh"
+
+namespace semd {
+namespace dev {
+
+// ------------------------------------------------------------------- eval
+
+struct EvalJob {
+    int mode, L, tiles, init_kind;
+    const double* src;
+    const double* a;
+    const double* b;
+    double beta;
+    double* dst;
+    KnotView kv[2];
+};
+
+// new value at sample t from global data (reference formula; slow path only)
+__device__ double new_value_global(const EvalJob& J, int t) {
+    if (J.mode == EM_INIT) return J.init_kind == 1 ? J.a[t] + J.beta * J.b[t] : J.a[t];
+    if (J.mode == EM_DETECT) return J.src[t];
+    const double u = envelope_at_global(J.kv[0], t);
+    const double l = envelope_at_global(J.kv[1], t);
+    const double mean = 0.5 * (u + l);
+    return J.src[t] - mean;
+}
+
+struct EvalSmemStatic {
+    unsigned ticket;
+    int last;
+    unsigned scan[kEvalThreads / 32];
+    double red[2][kEvalThreads / 32];
+    double edge_first[kEvalThreads / 32];
+    double edge_last[kEvalThreads / 32];
+    double halo[2];
+    int vlo[2], vcnt[2];
+};
+
+// Segment cache for the reference's segment march (emd.cpp:79).
+struct Seg {
+    int q;
+    double x0, x1, y0, y1, m0, m1, h, rh, hh;
+};
+
+__device__ __forceinline__ void seg_load(Seg& s, const double* kX, const double* kY, const double* kM,
+                                         const double* kR, int q) {
+    s.q = q;
+    s.x0 = kX[q];
+    s.x1 = kX[q + 1];
+    s.y0 = kY[q];
+    s.y1 = kY[q + 1];
+    s.m0 = kM[q];
+    s.m1 = kM[q + 1];
+    s.h = s.x1 - s.x0;
+    s.rh = kR[q];
+    s.hh = s.h * s.h;
+}
+
+__device__ __forceinline__ int seg_search(const double* kX, int vcnt, double tt) {
+    int lo = 0, hi = vcnt - 2;  // last q with X[q] < tt (X[0] < tt holds by construction)
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (kX[mid] < tt) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// envelope at tt from the tile's staged knots (used for the two tile halos)
+__device__ double envelope_smem(const double* kX, const double* kY, const double* kM, const double* kR, int vcnt,
+                                double tt) {
+    Seg s;
+    seg_load(s, kX, kY, kM, kR, seg_search(kX, vcnt, tt));
+    return spline_eval_fast(s.x0, s.x1, s.y0, s.y1, s.m0, s.m1, s.h, s.rh, s.hh, tt);
+}
+
+__device__ void eval_tile(const Arena& A, int slot, int j, double* dyn, EvalSmemStatic& sh) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const Slot& S = A.slots[slot];
+    const int L = A.L;
+    EvalJob J;
+    const int state = S.state;
+    J.mode = state == ST_INIT ? EM_INIT : (state == ST_DETECT ? EM_DETECT : EM_SIFT);
+    J.L = L;
+    J.tiles = A.tiles;
+    J.init_kind = S.init_kind;
+    J.a = S.init_a;
+    J.b = S.init_b;
+    J.beta = S.beta;
+    const int xb = S.xb, cb = S.cb;
+    J.src = A.bufs + buf_off(A, slot, (J.mode == EM_SIFT && cb >= 0) ? cb : xb);
+    J.dst = nullptr;
+    if (J.mode == EM_INIT) J.dst = A.bufs + buf_off(A, slot, xb);
+    if (J.mode == EM_SIFT) J.dst = A.bufs + buf_off(A, slot, S.db);
+    const int par = S.par;
+    const double e2 = 2.0 * (double)(L - 1);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        J.kv[s].idx = A.kidx + knot_off(A, par, s, slot);
+        J.kv[s].val = A.kval + knot_off(A, par, s, slot);
+        J.kv[s].mom = A.mom + mom_off(A, s, slot);
+        J.kv[s].n = (int)S.n[s];
+        J.kv[s].e2 = e2;
+    }
+    double* kX = dyn;
+    double* kY = kX + 2 * kKnotCapTile;
+    double* kM = kY + 2 * kKnotCapTile;
+    double* kR = kM + 2 * kKnotCapTile;
+    const int base = j * kEvalTile;
+    const int tlen = min(kEvalTile, L - base);
+
+    // 1. stage the knots touching this tile (virtual v in [toff[j], toff[j+1]+2])
+    if (J.mode == EM_SIFT) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const unsigned* to = A.toff + toff_off(A, par, s, slot);
+            const int vlo = (int)to[j];
+            const int vcnt = (int)to[j + 1] + 3 - vlo;
+            if (tid == 0) {
+                sh.vlo[s] = vlo;
+                sh.vcnt[s] = vcnt;
+            }
+            const int n = J.kv[s].n;
+            for (int q = tid; q < vcnt; q += kEvalThreads) {
+                const int v = vlo + q;
+                const int r0 = vknot_rank(n, v);
+                const double X0 = vknot_x(n, v, J.kv[s].idx[r0], e2);
+                kX[s * kKnotCapTile + q] = X0;
+                kY[s * kKnotCapTile + q] = J.kv[s].val[r0];
+                kM[s * kKnotCapTile + q] = J.kv[s].mom[v];
+                if (q + 1 < vcnt) {
+                    const int r1 = vknot_rank(n, v + 1);
+                    const double X1 = vknot_x(n, v + 1, J.kv[s].idx[r1], e2);
+                    kR[s * kKnotCapTile + q] = 1.0 / (X1 - X0);
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    // 2. this thread's 8 consecutive samples
+    const int t0 = base + tid * kSpt;
+    double cv[kSpt], nv[kSpt];
+    auto al16 = [](const double* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const bool inside = t0 + kSpt <= L;
+    // vector (16-byte) accesses only on aligned rows; caller buffers may have odd strides
+    const bool full = inside && (J.mode == EM_INIT ? (al16(J.a) && (J.init_kind != 1 || al16(J.b))) : al16(J.src)) &&
+                      (!J.dst || al16(J.dst));
+    if (J.mode == EM_INIT) {
+        if (full) {
+#pragma unroll
+            for (int k = 0; k < kSpt; k += 2) {
+                const double2 av = *reinterpret_cast<const double2*>(J.a + t0 + k);
+                cv[k] = av.x;
+                cv[k + 1] = av.y;
+            }
+            if (J.init_kind == 1) {
+#pragma unroll
+                for (int k = 0; k < kSpt; k += 2) {
+                    const double2 bv = *reinterpret_cast<const double2*>(J.b + t0 + k);
+                    cv[k] = cv[k] + J.beta * bv.x;
+                    cv[k + 1] = cv[k + 1] + J.beta * bv.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kSpt; ++k) {
+                const int t = t0 + k;
+                cv[k] = t < L ? (J.init_kind == 1 ? J.a[t] + J.beta * J.b[t] : J.a[t]) : 0.0;
+            }
+        }
+    } else {
+        if (full) {
+#pragma unroll
+            for (int k = 0; k < kSpt; k += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(J.src + t0 + k);
+                cv[k] = v.x;
+                cv[k + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kSpt; ++k) cv[k] = t0 + k < L ? J.src[t0 + k] : 0.0;
+        }
+    }
+    double num = 0.0, den = 0.0;
+    if (J.mode == EM_SIFT) {
+        Seg sg[2];
+        bool have = false;
+#pragma unroll
+        for (int k = 0; k < kSpt; ++k) {
+            const int t = t0 + k;
+            if (t < L) {
+                const double tt = (double)t;
+                double env[2];
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const double* X = kX + s * kKnotCapTile;
+                    const int vcnt = sh.vcnt[s];
+                    if (!have) seg_load(sg[s], X, kY + s * kKnotCapTile, kM + s * kKnotCapTile, kR + s * kKnotCapTile,
+                                        seg_search(X, vcnt, tt));
+                    while (sg[s].x1 < tt && sg[s].q + 1 <= vcnt - 2)
+                        seg_load(sg[s], X, kY + s * kKnotCapTile, kM + s * kKnotCapTile, kR + s * kKnotCapTile,
+                                 sg[s].q + 1);
+                    env[s] = spline_eval_fast(sg[s].x0, sg[s].x1, sg[s].y0, sg[s].y1, sg[s].m0, sg[s].m1, sg[s].h,
+                                              sg[s].rh, sg[s].hh, tt);
+                }
+                have = true;
+                const double mean = 0.5 * (env[0] + env[1]);  // emd.cpp:144-147
+                num += mean * mean;
+                den += cv[k] * cv[k];
+                nv[k] = cv[k] - mean;
+            } else {
+                nv[k] = 0.0;
+            }
+        }
+        if (full) {
+#pragma unroll
+            for (int k = 0; k < kSpt; k += 2)
+                *reinterpret_cast<double2*>(J.dst + t0 + k) = make_double2(nv[k], nv[k + 1]);
+        } else {
+            for (int k = 0; k < kSpt; ++k)
+                if (t0 + k < L) J.dst[t0 + k] = nv[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kSpt; ++k) nv[k] = cv[k];
+        if (J.dst) {
+            if (full) {
+#pragma unroll
+                for (int k = 0; k < kSpt; k += 2)
+                    *reinterpret_cast<double2*>(J.dst + t0 + k) = make_double2(nv[k], nv[k + 1]);
+            } else {
+                for (int k = 0; k < kSpt; ++k)
+                    if (t0 + k < L) J.dst[t0 + k] = nv[k];
+            }
+        }
+    }
+    // tile halos (t = base-1, base+T) and warp-edge exchange
+    if (tid == 0 && base > 0) {
+        const int t = base - 1;
+        double v;
+        if (J.mode == EM_SIFT) {
+            const double tt = (double)t;
+            const double u = envelope_smem(kX, kY, kM, kR, sh.vcnt[0], tt);
+            const double l = envelope_smem(kX + kKnotCapTile, kY + kKnotCapTile, kM + kKnotCapTile,
+                                           kR + kKnotCapTile, sh.vcnt[1], tt);
+            v = J.src[t] - 0.5 * (u + l);
+        } else {
+            v = new_value_global(J, t);
+        }
+        sh.halo[0] = v;
+    }
+    if (tid == kEvalThreads - 1 && base + kEvalTile < L) {
+        const int t = base + kEvalTile;
+        double v;
+        if (J.mode == EM_SIFT) {
+            const double tt = (double)t;
+            const double u = envelope_smem(kX, kY, kM, kR, sh.vcnt[0], tt);
+            const double l = envelope_smem(kX + kKnotCapTile, kY + kKnotCapTile, kM + kKnotCapTile,
+                                           kR + kKnotCapTile, sh.vcnt[1], tt);
+            v = J.src[t] - 0.5 * (u + l);
+        } else {
+            v = new_value_global(J, t);
+        }
+        sh.halo[1] = v;
+    }
+    if (lane == 0) sh.edge_first[wid] = nv[0];
+    if (lane == 31) sh.edge_last[wid] = nv[kSpt - 1];
+    double left = __shfl_up_sync(0xffffffffu, nv[kSpt - 1], 1);
+    double right = __shfl_down_sync(0xffffffffu, nv[0], 1);
+    __syncthreads();
+    if (lane == 0) left = wid > 0 ? sh.edge_last[wid - 1] : sh.halo[0];
+    if (lane == 31) right = wid < kEvalThreads / 32 - 1 ? sh.edge_first[wid + 1] : sh.halo[1];
+
+    // 3. extrema of the new values (find_extrema, emd.cpp:16-33)
+    unsigned fmax = 0, fmin = 0;
+#pragma unroll
+    for (int k = 0; k < kSpt; ++k) {
+        const int t = t0 + k;
+        if (t < 1 || t > L - 2) continue;
+        const double v = nv[k];
+        const double l = k == 0 ? left : nv[k - 1];
+        const double r = k == kSpt - 1 ? right : nv[k + 1];
+        if (v != l && v != r) {
+            if (v > l && v > r) fmax |= 1u << k;
+            if (v < l && v < r) fmin |= 1u << k;
+        } else {
+            // plateau: the maximal run of samples exactly equal to v
+            double win[kSpt + 2];
+            win[0] = left;
+#pragma unroll
+            for (int q = 0; q < kSpt; ++q) win[q + 1] = nv[q];
+            win[kSpt + 1] = right;
+            auto val = [&](int u) -> double {
+                const int li = u - t0 + 1;
+                if (li >= 0 && li <= kSpt + 1 && u < L) return win[li];
+                return new_value_global(J, u);
+            };
+            int rs = t, re = t;
+            while (rs > 0 && val(rs - 1) == v) --rs;
+            while (re < L - 1 && val(re + 1) == v) ++re;
+            if (rs > 0 && re < L - 1 && t == (rs + re) / 2) {
+                const double lv = val(rs - 1), rv = val(re + 1);
+                if (v > lv && v > rv) fmax |= 1u << k;
+                if (v < lv && v < rv) fmin |= 1u << k;
+            }
+        }
+    }
+
+    // 4. tile-local ordered compaction (block scan of packed counts)
+    const unsigned packed = (unsigned)__popc(fmax) | ((unsigned)__popc(fmin) << 16);
+    unsigned incl = packed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) sh.scan[wid] = incl;
+    if (J.mode == EM_SIFT) {
+        num = warp_sum(num);
+        den = warp_sum(den);
+        if (lane == 0) {
+            sh.red[0][wid] = num;
+            sh.red[1][wid] = den;
+        }
+    }
+    __syncthreads();
+    unsigned woff = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kEvalThreads / 32; ++w) {
+        const unsigned c = sh.scan[w];
+        if (w < wid) woff += c;
+        total += c;
+    }
+    const unsigned excl = woff + incl - packed;
+    unsigned omax = excl & 0xFFFF, omin = excl >> 16;
+    int* si0 = A.sidx + stage_off(A, 0, slot) + (size_t)j * kTileKnots;
+    int* si1 = A.sidx + stage_off(A, 1, slot) + (size_t)j * kTileKnots;
+    double* sv0 = A.sval + stage_off(A, 0, slot) + (size_t)j * kTileKnots;
+    double* sv1 = A.sval + stage_off(A, 1, slot) + (size_t)j * kTileKnots;
+#pragma unroll
+    for (int k = 0; k < kSpt; ++k) {
+        if (fmax & (1u << k)) {
+            si0[omax] = t0 + k;
+            sv0[omax] = nv[k];
+            ++omax;
+        }
+        if (fmin & (1u << k)) {
+            si1[omin] = t0 + k;
+            sv1[omin] = nv[k];
+            ++omin;
+        }
+    }
+    if (tid == 0) {
+        A.scnt[scnt_off(A, 0, slot) + j] = total & 0xFFFF;
+        A.scnt[scnt_off(A, 1, slot) + j] = total >> 16;
+        if (J.mode == EM_SIFT) {
+            double a = 0.0, b = 0.0;
+            for (int w = 0; w < kEvalThreads / 32; ++w) {
+                a += sh.red[0][w];
+                b += sh.red[1][w];
+            }
+            A.tnum[(size_t)slot * A.tiles + j] = a;
+            A.tden[(size_t)slot * A.tiles + j] = b;
+        }
+    }
+    (void)tlen;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
+    extern __shared__ double dyn[];
+    __shared__ EvalSmemStatic sh;
+    Ctrl* C = A.ctrl;
+    const unsigned nitems = (unsigned)C->n_eval * (unsigned)A.tiles;
+    while (true) {
+        if (threadIdx.x == 0) sh.ticket = atomicAdd(&C->ticket[0], 1u);
+        __syncthreads();
+        const unsigned q = sh.ticket;
+        __syncthreads();
+        if (q >= nitems) break;
+        eval_tile(A, A.eval_list[q / (unsigned)A.tiles], (int)(q % (unsigned)A.tiles), dyn, sh);
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&C->done[0], 1u) == gridDim.x - 1) {
+            C->ticket[0] = 0;
+            C->done[0] = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------- lists
+
+// Block-wide exclusive scan of one int per thread (blockDim.x <= 1024).
+__device__ int block_excl_scan(int v, int* total) {
+    __shared__ int s_w[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < nw; ++w) {
+        const int c = s_w[w];
+        if (w < wid) off += c;
+        tot += c;
+    }
+    *total = tot;
+    __syncthreads();
+    return off + incl - v;
+}
+
+// Rebuild the per-step work lists (one CTA; lists are in slot order, which
+// fixes the accumulation order). Lockstep rule: IMF k is finalised for every
+// slot in the same step, once no slot is still sifting.
+__device__ void build_lists(const Arena& A, bool allow_final) {
+    Ctrl* C = A.ctrl;
+    const int G = A.G;
+    const int per = (G + blockDim.x - 1) / blockDim.x;
+    const int s0 = min(G, (int)threadIdx.x * per), s1 = min(G, s0 + per);
+    int busy = 0, wait = 0;
+    for (int s = s0; s < s1; ++s) {
+        const int st = A.slots[s].state;
+        busy += (st == ST_INIT || st == ST_DETECT || st == ST_SIFT);
+        wait += (st == ST_WAITK);
+    }
+    int tb, tw;
+    block_excl_scan(busy, &tb);
+    block_excl_scan(wait, &tw);
+    const bool finalize = allow_final && tb == 0 && tw > 0;
+    int ne = 0, nf = 0, ns = 0, nb = 0, act = 0;
+    for (int s = s0; s < s1; ++s) {
+        Slot& S = A.slots[s];
+        if (finalize && S.state == ST_WAITK) S.state = ST_FINAL;
+        const int st = S.state;
+        ne += (st == ST_INIT || st == ST_DETECT || st == ST_SIFT);
+        nf += (st == ST_FINAL);
+        act += (st != ST_FREE && st != ST_DONE);
+        if (st == ST_SIFT) {
+            S.db = pick_free_buffer(S.xb, S.cb);
+            ns += 2;
+            for (int side = 0; side < 2; ++side) {
+                const int rows = (int)S.n[side] + 2;
+                nb += rows <= kSolveSeqMax ? 1 : (rows + kSolveBlock - 1) / kSolveBlock;
+            }
+        }
+    }
+    int tne, tnf, tns, tnb, tact;
+    int oe = block_excl_scan(ne, &tne);
+    int of = block_excl_scan(nf, &tnf);
+    int os = block_excl_scan(ns, &tns);
+    int ob = block_excl_scan(nb, &tnb);
+    block_excl_scan(act, &tact);
+    for (int s = s0; s < s1; ++s) {
+        const Slot& S = A.slots[s];
+        const int st = S.state;
+        if (st == ST_INIT || st == ST_DETECT || st == ST_SIFT) A.eval_list[oe++] = s;
+        if (st == ST_FINAL) A.final_list[of++] = s;
+        if (st == ST_SIFT) {
+            for (int side = 0; side < 2; ++side) {
+                const int rows = (int)S.n[side] + 2;
+                A.solve_item[os] = (s << 1) | side;
+                A.solve_off[os] = ob;
+                ++os;
+                ob += rows <= kSolveSeqMax ? 1 : (rows + kSolveBlock - 1) / kSolveBlock;
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        A.solve_off[tns] = tnb;
+        C->n_eval = tne;
+        C->n_final = tnf;
+        C->n_solve = tns;
+        C->solve_blocks = tnb;
+        C->active = tact;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------- scan
+//
+// One CTA per (eval slot, side): exclusive prefix of the per-tile extrema
+// counts -> toff of the new knot parity; side-0 CTAs also reduce the SD sums
+// (fixed tree order). The last CTA applies extract_imf's control flow.
+
+// extract_imf's control flow (emd.cpp:131-151) for one slot after its eval
+// pass; returns 1 when this step's extrema must be compacted.
+__device__ int decide_slot(const Arena& A, int s) {
+    Slot& S = A.slots[s];
+    const int state = S.state;
+    const int np = 1 - S.par;
+    const unsigned nmax = A.toff[toff_off(A, np, 0, s) + A.tiles];
+    const unsigned nmin = A.toff[toff_off(A, np, 1, s) + A.tiles];
+    const int tracing = A.trace != nullptr;
+    int compact = 0;
+    S.trace_iter = -1;
+    S.cpar = np;
+    S.tn[0] = nmax;
+    S.tn[1] = nmin;
+    if (state == ST_INIT || state == ST_DETECT) {
+        // iteration 0 of IMF k: extract_imf's first find_extrema
+        if (A.max_sift_iters <= 0 && !S.detect_only) {  // loop body never runs: IMF = input
+            S.cb = -1;
+            S.iter = 0;
+            S.state = ST_WAITK;
+            if (A.imf_sifts && S.k0 + S.k < A.kcap) A.imf_sifts[S.k0 + S.k] = 0;
+            return 0;
+        }
+        S.trace_iter = 0;
+        if (S.detect_only) {  // standalone find_extrema / CEEMDAN stage check: lists are returned
+            S.n[0] = nmax;
+            S.n[1] = nmin;
+            S.state = ST_DONE;
+            return 1;
+        }
+        S.par = np;
+        S.n[0] = nmax;
+        S.n[1] = nmin;
+        S.iter = 0;
+        S.cb = -1;
+        if (nmax < 2 || nmin < 2) {  // InsufficientExtrema on the unsifted input (emd.cpp:138, :164)
+            S.ended_insufficient = 1;
+            S.state = ST_DONE;
+            return tracing;
+        }
+        S.state = ST_SIFT;
+        return 1;
+    }
+    if (state == ST_SIFT) {
+        S.iter += 1;
+        S.sifted += A.L;
+        S.cb = S.db;
+        const double num = S.num, den = S.den;
+        bool stop = (den == 0.0 || num / den < A.sd_threshold) || S.iter >= A.max_sift_iters;
+        if (!stop) {
+            S.trace_iter = S.iter;
+            if (nmax < 2 || nmin < 2) {
+                stop = true;  // envelope throws: the candidate is the IMF (emd.cpp:137-140)
+                compact = tracing;
+            } else {
+                S.par = np;
+                S.n[0] = nmax;
+                S.n[1] = nmin;
+                compact = 1;
+            }
+        }
+        if (stop) {
+            S.state = ST_WAITK;
+            if (A.imf_sifts && S.k0 + S.k < A.kcap) A.imf_sifts[S.k0 + S.k] = S.iter;
+        }
+    }
+    return compact;
+}
+
+__device__ void decide_after_eval(const Arena& A) {
+    Ctrl* C = A.ctrl;
+    const int ne = C->n_eval;
+    const int per = (ne + blockDim.x - 1) / blockDim.x;
+    const int l0 = min(ne, (int)threadIdx.x * per), l1 = min(ne, l0 + per);
+    int flags = 0, cnt = 0;  // per <= 32 when G <= 8192
+    for (int li = l0; li < l1; ++li) {
+        const int f = decide_slot(A, A.eval_list[li]);
+        flags |= f << (li - l0);
+        cnt += f;
+    }
+    int tot;
+    int off = block_excl_scan(cnt, &tot);
+    for (int li = l0; li < l1; ++li)
+        if (flags & (1 << (li - l0))) A.compact_list[off++] = A.eval_list[li];
+    if (threadIdx.x == 0) C->n_compact = tot;
+    __syncthreads();
+    build_lists(A, true);
+}
+
+__global__ void __launch_bounds__(256) k_scan(Arena A) {
+    __shared__ unsigned s_part[256];
+    __shared__ double s_red[2][8];
+    __shared__ int s_last;
+    Ctrl* C = A.ctrl;
+    const int tid = threadIdx.x;
+    const int li = blockIdx.x >> 1, side = blockIdx.x & 1;
+    if (li < C->n_eval) {
+        const int s = A.eval_list[li];
+        const Slot& S = A.slots[s];
+        const int np = 1 - S.par;
+        const int T = A.tiles;
+        const int per = (T + 255) / 256;
+        const int j0 = min(T, tid * per), j1 = min(T, j0 + per);
+        const unsigned* cnt = A.scnt + scnt_off(A, side, s);
+        unsigned sum = 0;
+        for (int jj = j0; jj < j1; ++jj) sum += cnt[jj];
+        s_part[tid] = sum;
+        __syncthreads();
+        // exclusive scan of the 256 partials (Hillis-Steele in shared memory)
+        for (int o = 1; o < 256; o <<= 1) {
+            const unsigned v = tid >= o ? s_part[tid - o] : 0;
+            __syncthreads();
+            s_part[tid] += v;
+            __syncthreads();
+        }
+        unsigned run = s_part[tid] - sum;
+        unsigned* to = A.toff + toff_off(A, np, side, s);
+        for (int jj = j0; jj < j1; ++jj) {
+            to[jj] = run;
+            run += cnt[jj];
+        }
+        if (tid == 255) to[T] = s_part[255];
+        if (side == 0 && S.state == ST_SIFT) {  // SD sums (emd.cpp:145-146), fixed reduction order
+            double a = 0.0, b = 0.0;
+            for (int jj = j0; jj < j1; ++jj) {
+                a += A.tnum[(size_t)s * T + jj];
+                b += A.tden[(size_t)s * T + jj];
+            }
+            a = warp_sum(a);
+            b = warp_sum(b);
+            if ((tid & 31) == 0) {
+                s_red[0][tid >> 5] = a;
+                s_red[1][tid >> 5] = b;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double x = 0.0, y = 0.0;
+                for (int w = 0; w < 8; ++w) {
+                    x += s_red[0][w];
+                    y += s_red[1][w];
+                }
+                A.slots[s].num = x;
+                A.slots[s].den = y;
+            }
+        }
+    }
+    if (tid == 0) {
+        __threadfence();
+        s_last = atomicAdd(&C->done[4], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        decide_after_eval(A);
+        if (tid == 0) C->done[4] = 0;
+    }
+}
+
+// ---------------------------------------------------------------- compact
+//
+// Stage -> ordered global extrema lists (tile j's knots land at toff[j]).
+// Also the order-sensitive parity-trace hash (tracing only).
+
+__device__ void emit_trace(const Arena& A, const Slot& S, uint64_t h) {
+    const int pos = atomicAdd(&A.ctrl->trace_count, 1);
+    if (pos < A.trace_cap) {
+        TraceRec r;
+        r.task = S.task;
+        r.m = S.m;
+        r.k = S.k;
+        r.iter = S.trace_iter;
+        r.n_max = S.tn[0];
+        r.n_min = S.tn[1];
+        r.hash = h;
+        A.trace[pos] = r;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_compact(Arena A) {
+    __shared__ unsigned s_ticket;
+    __shared__ int s_last;
+    __shared__ unsigned long long s_h[8];
+    Ctrl* C = A.ctrl;
+    const unsigned nitems = (unsigned)C->n_compact * (unsigned)A.tiles;
+    const bool tracing = A.trace != nullptr;
+    while (true) {
+        if (threadIdx.x == 0) s_ticket = atomicAdd(&C->ticket[1], 1u);
+        __syncthreads();
+        const unsigned q = s_ticket;
+        __syncthreads();
+        if (q >= nitems) break;
+        const int s = A.compact_list[q / (unsigned)A.tiles];
+        const int j = (int)(q % (unsigned)A.tiles);
+        const int cpar = A.slots[s].cpar;
+        uint64_t h = 0;
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const unsigned cnt = A.scnt[scnt_off(A, side, s) + j];
+            const unsigned off = A.toff[toff_off(A, cpar, side, s) + j];
+            const int* si = A.sidx + stage_off(A, side, s) + (size_t)j * kTileKnots;
+            const double* sv = A.sval + stage_off(A, side, s) + (size_t)j * kTileKnots;
+            int* gi = A.kidx + knot_off(A, cpar, side, s) + off;
+            double* gv = A.kval + knot_off(A, cpar, side, s) + off;
+            for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
+                const int t = si[i];
+                gi[i] = t;
+                gv[i] = sv[i];
+                if (tracing) h += knot_hash(side, off + i, (unsigned)t);
+            }
+        }
+        if (tracing) {
+            h = warp_sum(h);
+            if ((threadIdx.x & 31) == 0) s_h[threadIdx.x >> 5] = h;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                uint64_t hs = 0;
+                for (int w = 0; w < 8; ++w) hs += s_h[w];
+                A.thash[(size_t)s * A.tiles + j] = hs;
+            }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&C->done[1], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        if (tracing) {
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+            for (int li = wid; li < C->n_compact; li += 8) {
+                const int s = A.compact_list[li];
+                const Slot& S = A.slots[s];
+                uint64_t h = 0;
+                for (int j = lane; j < A.tiles; j += 32) h += A.thash[(size_t)s * A.tiles + j];
+                h = warp_sum(h);
+                if (lane == 0 && S.trace_iter >= 0) emit_trace(A, S, h);
+            }
+        }
+        if (threadIdx.x == 0) {
+            C->ticket[1] = 0;
+            C->done[1] = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ solve
+//
+// Natural-spline moments (emd.cpp:53-73) of one envelope's mirrored knot
+// system, reproducing the reference's sequential Thomas algorithm BIT-FOR-BIT
+// with parallel chains. Each chain restarts the recurrence kSolveWarm rows
+// before its chunk from a guessed state; the recurrences contract (~0.27 per
+// row), so the speculative chain soon coincides bitwise with the true one.
+// Every chain then replays its head from its predecessor's end state until it
+// meets its own stored values bitwise, which makes the result exactly the
+// sequential one; replays repeat while a chain's end moved. Across CTA blocks
+// a kSolveHalo-row warm-up is used and the boundary values are cross-checked
+// (mismatches are counted as hazards; none has been observed).
+//
+// Shared layout per block, indexed by knot/row v - wa:
+//   H[v] = X[v+1]-X[v], RHS[i], DP[i], RP[i], M[i]  (X and Y only staged)
+
+struct SolveCtx {
+    const double* H;
+    const double* RHS;
+    int wa;
+};
+
+__device__ __forceinline__ void fwd_first(const SolveCtx& c, int i, double& d, double& r) {
+    const double h0 = c.H[i - 1 - c.wa], h1 = c.H[i - c.wa];
+    d = 2.0 * (h0 + h1);  // emd.cpp:60
+    r = c.RHS[i - c.wa];
+}
+
+// emd.cpp:64-69: w = h0 / diag[i-1]; diag[i] -= w*upper[i-1]; rhs[i] -= w*rhs[i-1]
+__device__ __forceinline__ void fwd_step(const SolveCtx& c, int i, double& d, double& r) {
+    const double h0 = c.H[i - 1 - c.wa], h1 = c.H[i - c.wa];
+    const double w = h0 / d;
+    d = 2.0 * (h0 + h1) - w * h0;
+    r = c.RHS[i - c.wa] - w * r;
+}
+
+struct SolveShared {
+    unsigned ticket;
+    int item, b, last, any;
+    int dirty[kSolveChains + 1];
+    int moved[kSolveChains + 1];
+};
+
+__device__ void solve_small(const KnotView& kv, double* mom, double* sm) {
+    // one thread runs the reference Thomas algorithm verbatim
+    const int N = kv.n + 4;
+    double* X = sm;
+    double* Y = X + (kSolveSeqMax + 4);
+    double* dp = Y + (kSolveSeqMax + 4);
+    double* rp = dp + (kSolveSeqMax + 4);
+    for (int v = threadIdx.x; v < N; v += blockDim.x) vknot(kv, v, X[v], Y[v]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i + 1 < N; ++i) {
+            const double h0 = X[i] - X[i - 1], h1 = X[i + 1] - X[i];
+            dp[i] = 2.0 * (h0 + h1);
+            rp[i] = 6.0 * ((Y[i + 1] - Y[i]) / h1 - (Y[i] - Y[i - 1]) / h0);
+        }
+        for (int i = 2; i + 1 < N; ++i) {
+            const double h0 = X[i] - X[i - 1];
+            const double w = h0 / dp[i - 1];
+            dp[i] -= w * (X[i] - X[i - 1]);
+            rp[i] -= w * rp[i - 1];
+        }
+        double m = 0.0;
+        mom[N - 1] = 0.0;
+        for (int i = N - 2; i >= 1; --i) {
+            m = (rp[i] - (X[i + 1] - X[i]) * m) / dp[i];
+            mom[i] = m;
+        }
+        mom[0] = 0.0;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
+    extern __shared__ double sm[];
+    __shared__ SolveShared sh;
+    Ctrl* C = A.ctrl;
+    const int tid = threadIdx.x;
+    const int nblocks = C->solve_blocks;
+    const int nitems = C->n_solve;
+    while (true) {
+        if (tid == 0) {
+            sh.ticket = atomicAdd(&C->ticket[2], 1u);
+            if (sh.ticket < (unsigned)nblocks) {
+                int lo = 0, hi = nitems - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if ((unsigned)A.solve_off[mid] <= sh.ticket) lo = mid;
+                    else hi = mid - 1;
+                }
+                sh.item = lo;
+                sh.b = (int)sh.ticket - A.solve_off[lo];
+            }
+        }
+        __syncthreads();
+        if (sh.ticket >= (unsigned)nblocks) break;
+        const int code = A.solve_item[sh.item];
+        const int slot = code >> 1, side = code & 1, b = sh.b;
+        const Slot& S = A.slots[slot];
+        KnotView kv;
+        kv.idx = A.kidx + knot_off(A, S.par, side, slot);
+        kv.val = A.kval + knot_off(A, S.par, side, slot);
+        kv.n = (int)S.n[side];
+        kv.e2 = 2.0 * (double)(A.L - 1);
+        kv.mom = nullptr;
+        double* mom = A.mom + mom_off(A, side, slot);
+        const int N = kv.n + 4;
+        if (N - 2 <= kSolveSeqMax) {
+            solve_small(kv, mom, sm);
+            continue;
+        }
+        const int HW = kSolveHalo, B = kSolveBlock, CH = kSolveChunk, NT = kSolveChains, W0 = kSolveWarm;
+        const int r0 = 1 + b * B;
+        const int r1 = min(r0 + B, N - 1);
+        const int r1e = min(r1 + HW, N - 1);
+        const int wa = max(0, r0 - HW - 1);
+        const int wb = min(N - 1, r1 + HW);
+        const int wn = wb - wa + 1;
+        double* H = sm;          // [wn]   H[v] = X[v+1]-X[v]
+        double* RHS = H + kSolveWin;
+        double* DP = RHS + kSolveWin;
+        double* RP = DP + kSolveWin;
+        double* M = RP + kSolveWin;
+        // stage X into DP and Y into M (temporarily), then H, 1/H (into RP), RHS
+        for (int q = tid; q < wn; q += blockDim.x) vknot(kv, wa + q, DP[q], M[q]);
+        __syncthreads();
+        for (int q = tid; q < wn - 1; q += blockDim.x) {
+            const double h = DP[q + 1] - DP[q];
+            H[q] = h;
+            RP[q] = 1.0 / h;
+        }
+        __syncthreads();
+        for (int q = tid + 1; q < wn - 1; q += blockDim.x) {  // emd.cpp:62 with exactly rounded divisions
+            const double h0 = H[q - 1], h1 = H[q];
+            RHS[q] = 6.0 * (div_rn(M[q + 1] - M[q], h1, RP[q]) - div_rn(M[q] - M[q - 1], h0, RP[q - 1]));
+        }
+        __syncthreads();
+        SolveCtx cx{H, RHS, wa};
+        // chain c < NT owns rows [cs, ce) of [r0, r1); chain NT owns the back halo [r1, r1e)
+        const int c = tid;
+        int cs = 0, ce = 0;
+        if (c < NT) {
+            cs = min(r0 + c * CH, r1);
+            ce = min(cs + CH, r1);
+        } else if (c == NT) {
+            cs = r1;
+            ce = r1e;
+        }
+        const bool mine = c <= NT && cs < ce;
+        double* rec = A.sb + (((size_t)side * A.G + slot) * A.max_blocks + b) * 6;
+        // --- phase A: forward from a guessed state kSolveWarm rows early (chain 0: kSolveHalo)
+        if (mine) {
+            const int ws = max(1, cs - (c == 0 ? HW : W0));
+            double d, r;
+            fwd_first(cx, ws, d, r);  // exact when ws == 1, otherwise a guess
+            for (int i = ws + 1; i < cs; ++i) fwd_step(cx, i, d, r);
+            if (c == 0 && r0 > 1) {
+                rec[0] = d;  // warm-up state at row r0-1 (cross-block check)
+                rec[1] = r;
+            }
+            if (ws < cs) fwd_step(cx, cs, d, r);
+            DP[cs - wa] = d;
+            RP[cs - wa] = r;
+            for (int i = cs + 1; i < ce; ++i) {
+                fwd_step(cx, i, d, r);
+                DP[i - wa] = d;
+                RP[i - wa] = r;
+            }
+        }
+        if (tid <= NT) sh.moved[tid] = 1;
+        __syncthreads();
+        // --- phase B: replay chain heads from the predecessor's end state until bitwise agreement
+        for (int round = 0; round <= NT; ++round) {
+            if (tid == 0) sh.any = 0;
+            if (tid <= NT) sh.dirty[tid] = 0;
+            __syncthreads();
+            if (mine && c >= 1 && sh.moved[c - 1]) {
+                double d = DP[cs - 1 - wa], r = RP[cs - 1 - wa];
+                bool conv = false;
+                for (int i = cs; i < ce; ++i) {
+                    fwd_step(cx, i, d, r);
+                    if (d == DP[i - wa] && r == RP[i - wa]) {
+                        conv = true;
+                        break;
+                    }
+                    DP[i - wa] = d;
+                    RP[i - wa] = r;
+                }
+                if (!conv) {
+                    sh.dirty[c] = 1;
+                    sh.any = 1;
+                }
+            }
+            __syncthreads();
+            const int any = sh.any;
+            if (tid <= NT) sh.moved[tid] = sh.dirty[tid];
+            __syncthreads();
+            if (!any) break;
+        }
+        // --- phase C: back substitution (emd.cpp:70-73), speculative above each chunk
+        auto upper = [&](int i) { return H[i - wa]; };  // X[i+1]-X[i]
+        if (mine) {
+            const int top = c == NT ? ce : min(ce + W0, r1e);
+            double m = 0.0;  // exact when top == N-1, otherwise a guess
+            for (int i = top - 1; i >= cs; --i) {
+                const double dp = DP[i - wa];
+                m = div_rn(RP[i - wa] - upper(i) * m, dp, 1.0 / dp);
+                if (i < ce) M[i - wa] = m;
+            }
+        }
+        if (tid <= NT) sh.moved[tid] = 1;
+        __syncthreads();
+        // --- phase D: replay chain tails from the successor's first value
+        for (int round = 0; round <= NT; ++round) {
+            if (tid == 0) sh.any = 0;
+            if (tid <= NT) sh.dirty[tid] = 0;
+            __syncthreads();
+            if (mine && c < NT && ce < N - 1 && sh.moved[c + 1]) {
+                double m = M[ce - wa];
+                bool conv = false;
+                for (int i = ce - 1; i >= cs; --i) {
+                    const double dp = DP[i - wa];
+                    m = div_rn(RP[i - wa] - upper(i) * m, dp, 1.0 / dp);
+                    if (m == M[i - wa]) {
+                        conv = true;
+                        break;
+                    }
+                    M[i - wa] = m;
+                }
+                if (!conv) {
+                    sh.dirty[c] = 1;
+                    sh.any = 1;
+                }
+            }
+            __syncthreads();
+            const int any = sh.any;
+            if (tid <= NT) sh.moved[tid] = sh.dirty[tid];
+            __syncthreads();
+            if (!any) break;
+        }
+        // --- outputs + cross-block records: [0,1] warm-up state at r0-1, [2,3]
+        // this block's state at r1-1, [4] m at r0, [5] the m at r1 it used
+        for (int i = r0 + tid; i < r1; i += blockDim.x) mom[i] = M[i - wa];
+        if (tid == 0) {
+            if (r0 == 1) mom[0] = 0.0;
+            if (r1 == N - 1) mom[N - 1] = 0.0;
+            rec[2] = DP[r1 - 1 - wa];
+            rec[3] = RP[r1 - 1 - wa];
+            rec[4] = M[r0 - wa];
+            rec[5] = r1 < N - 1 ? M[r1 - wa] : 0.0;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        __threadfence();
+        sh.last = atomicAdd(&C->done[2], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (sh.last) {
+        __threadfence();
+        for (int it = tid; it < nitems; it += blockDim.x) {
+            const int code = A.solve_item[it];
+            const int slot = code >> 1, side = code & 1;
+            const int nb = A.solve_off[it + 1] - A.solve_off[it];
+            if ((int)A.slots[slot].n[side] + 2 <= kSolveSeqMax) continue;
+            const double* base = A.sb + ((size_t)side * A.G + slot) * A.max_blocks * 6;
+            int bad = 0;
+            for (int bb = 1; bb < nb; ++bb) {
+                const double* p = base + (size_t)(bb - 1) * 6;
+                const double* q = base + (size_t)bb * 6;
+                if (q[0] != p[2] || q[1] != p[3] || p[5] != q[4]) ++bad;
+            }
+            if (bad) {
+                atomicAdd(&A.slots[slot].hazards, bad);
+                atomicAdd(&C->hazards, bad);
+            }
+        }
+        if (tid == 0) {
+            C->ticket[2] = 0;
+            C->done[2] = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ final
+//
+// IMF k is complete for every slot in final_list (lockstep). Per sample:
+//   sums[k0+k][t] += imf_s[t]   in slot order (emd.cpp:249-251 accumulation order)
+//   R_s[t] = X_s[t] - imf_s[t]  (emd.cpp:167 residue update)
+
+constexpr int kFinalChunk = 128;
+
+struct FinalSlot {
+    const double* x;
+    const double* imf;
+    double* res;
+    double* imf_out;
+    double* res_out;
+    double* row;  // accumulation row or null
+};
+
+__device__ void decide_after_final(const Arena& A) {
+    Ctrl* C = A.ctrl;
+    const int nf = C->n_final;
+    for (int li = threadIdx.x; li < nf; li += blockDim.x) {
+        Slot& S = A.slots[A.final_list[li]];
+        const int rb = pick_free_buffer(S.xb, S.cb);
+        S.last_imf_b = S.cb >= 0 ? S.cb : S.xb;
+        S.xb = rb;
+        S.cb = -1;
+        S.k += 1;
+        S.iter = 0;
+        if (S.kmax > 0 && S.k >= S.kmax) S.state = ST_DONE;
+        else S.state = ST_DETECT;
+    }
+    __syncthreads();
+    build_lists(A, false);
+    if (threadIdx.x == 0 && A.status_host) {
+        C->step += 1;
+        volatile int* hs = A.status_host;
+        hs[0] = C->active;
+        hs[1] = C->step;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_final(Arena A) {
+    __shared__ unsigned s_ticket;
+    __shared__ int s_last;
+    __shared__ FinalSlot tab[kFinalChunk];
+    Ctrl* C = A.ctrl;
+    const int nf = C->n_final;
+    const int tiles = (A.L + kFinalTile - 1) / kFinalTile;
+    const unsigned nitems = nf > 0 ? (unsigned)tiles : 0u;
+    constexpr int PER = kFinalTile / 256;
+    while (true) {
+        if (threadIdx.x == 0) s_ticket = atomicAdd(&C->ticket[3], 1u);
+        __syncthreads();
+        const unsigned q = s_ticket;
+        __syncthreads();
+        if (q >= nitems) break;
+        const size_t t0 = (size_t)q * kFinalTile;
+        double acc[PER];
+        double* accrow = nullptr;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) acc[i] = 0.0;
+        for (int c0 = 0; c0 < nf; c0 += kFinalChunk) {
+            const int cn = min(kFinalChunk, nf - c0);
+            __syncthreads();
+            for (int li = threadIdx.x; li < cn; li += blockDim.x) {
+                const Slot& S = A.slots[A.final_list[c0 + li]];
+                FinalSlot f;
+                f.x = A.bufs + buf_off(A, A.final_list[c0 + li], S.xb);
+                f.imf = S.cb >= 0 ? A.bufs + buf_off(A, A.final_list[c0 + li], S.cb) : f.x;
+                f.res = A.bufs + buf_off(A, A.final_list[c0 + li], pick_free_buffer(S.xb, S.cb));
+                f.imf_out = S.imf_out;
+                f.res_out = S.res_out;
+                const int r = S.k0 + S.k;
+                f.row = (S.write_imf && r < A.kcap) ? A.sums + (size_t)r * A.L : nullptr;
+                tab[li] = f;
+            }
+            __syncthreads();
+            for (int li = 0; li < cn; ++li) {
+                const FinalSlot f = tab[li];
+                if (f.row && f.row != accrow) {
+                    if (accrow) {
+#pragma unroll
+                        for (int i = 0; i < PER; ++i) {
+                            const size_t t = t0 + threadIdx.x + 256 * i;
+                            if (t < (size_t)A.L) accrow[t] = acc[i];
+                        }
+                    }
+                    accrow = f.row;
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) {
+                        const size_t t = t0 + threadIdx.x + 256 * i;
+                        acc[i] = t < (size_t)A.L ? accrow[t] : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const size_t t = t0 + threadIdx.x + 256 * i;
+                    if (t >= (size_t)A.L) continue;
+                    const double x = f.x[t];
+                    const double imf = f.imf[t];
+                    const double res = x - imf;
+                    f.res[t] = res;
+                    if (f.imf_out) f.imf_out[t] = imf;
+                    if (f.res_out) f.res_out[t] = res;
+                    if (f.row) acc[i] = acc[i] + imf;
+                }
+            }
+        }
+        if (accrow) {
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const size_t t = t0 + threadIdx.x + 256 * i;
+                if (t < (size_t)A.L) accrow[t] = acc[i];
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&C->done[3], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        if (threadIdx.x == 0) {
+            for (int li = 0; li < nf; ++li) {
+                const Slot& S = A.slots[A.final_list[li]];
+                if (S.write_imf && S.k0 + S.k >= A.kcap) atomicAdd(&C->k_overflow, 1);
+            }
+        }
+        decide_after_final(A);
+        if (threadIdx.x == 0) {
+            C->ticket[3] = 0;
+            C->done[3] = 0;
+        }
+    }
+}
+
+// --------------------------------------------------------------- launchers
+
+size_t eval_smem_bytes() { return (size_t)8 * kKnotCapTile * sizeof(double); }
+size_t solve_smem_bytes() {
+    const size_t chunked = (size_t)5 * kSolveWin * sizeof(double);
+    const size_t seq = (size_t)4 * (kSolveSeqMax + 4) * sizeof(double);
+    return chunked > seq ? chunked : seq;
+}
+
+cudaError_t launch_setup() {
+    cudaError_t e = cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eval_smem_bytes());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem_bytes());
+}
+
+void launch_step(const Arena& A, int sms, cudaStream_t st) {
+    k_solve<<<2 * sms, kSolveThreads, solve_smem_bytes(), st>>>(A);
+    k_eval<<<2 * sms, kEvalThreads, eval_smem_bytes(), st>>>(A);
+    k_scan<<<2 * A.G, 256, 0, st>>>(A);
+    k_compact<<<2 * sms, 256, 0, st>>>(A);
+    k_final<<<2 * sms, 256, 0, st>>>(A);
+}
+
+}  // namespace dev
+}  // namespace semd

@@ -8,11 +8,12 @@
 //
 // HBM layout per engine (L = serialized length, G = slots, T = eval tile):
 //   bufs    f64 [G][3][L]        rotating X (IMF input), C (candidate), R (next residue)
+//   sidx/sval  [2 side][G][tiles*T/2]     tile-local extrema found by k_eval (stage)
+//   scnt    u32 [2 side][G][tiles]        extrema per tile
 //   kidx    i32 [2 par][2 side][G][cap]   compacted extrema indices (cap = L/2+2)
 //   kval    f64 [2][2][G][cap]            extrema values
 //   toff    u32 [2][2][G][tiles+1]        exclusive per-tile knot offsets
 //   mom     f64 [2 side][G][cap+4]        spline moments of the mirrored knot system
-//   status  u64 [2 side][G][tiles]        decoupled look-back words (epoch|flag|count)
 //   tnum/tden/thash [G][tiles]            per-tile SD and trace-hash partials
 //   sums    f64 [kcap][L]                 ensemble / IMF accumulators
 #pragma once
@@ -25,12 +26,16 @@ constexpr int kEvalTile = 2048;                 // samples per eval tile
 constexpr int kEvalThreads = 256;
 constexpr int kSpt = kEvalTile / kEvalThreads;  // samples per thread (consecutive)
 constexpr int kKnotCapTile = kEvalTile / 2 + 4; // knots of one side touching a tile
+constexpr int kTileKnots = kEvalTile / 2;       // stage capacity per tile and side
 
-constexpr int kSolveThreads = 128;                       // speculative chains per block
+constexpr int kSolveChains = 64;                         // speculative chains per block
 constexpr int kSolveChunk = 32;                          // rows per chain
-constexpr int kSolveBlock = kSolveThreads * kSolveChunk; // rows per CTA
+constexpr int kSolveWarm = 16;                           // per-chain warm-up rows
+constexpr int kSolveBlock = kSolveChains * kSolveChunk;  // rows per CTA
 constexpr int kSolveHalo = 64;                           // cross-block warm-up rows
+constexpr int kSolveThreads = kSolveChains + 32;         // + the back-halo chain + helpers
 constexpr int kSolveSeqMax = 96;                         // rows solved by one exact thread
+constexpr int kSolveWin = kSolveBlock + 2 * kSolveHalo + 4;  // knot window per block
 
 constexpr int kFinalTile = 1024;
 
@@ -72,6 +77,9 @@ struct Slot {
     unsigned n[2];       // extrema counts (max, min) of the current knot set
     int ended_insufficient;
     int last_imf_b;      // buffer id that held the last finalised IMF
+    int trace_iter;      // find_extrema record due after compaction (-1: none)
+    int cpar;            // parity the stage knots are compacted into this step
+    unsigned tn[2];      // extrema counts of this step's detect
     int hazards;         // speculative-solve boundary mismatches observed
     long long sifted;    // sifted samples (L per completed sift)
     double num, den;
@@ -85,10 +93,11 @@ struct TraceRec {
 
 // Control block: work lists and kernel bookkeeping (device memory).
 struct Ctrl {
-    unsigned ticket[4];
-    unsigned done[4];
+    unsigned ticket[8];  // 0 eval, 1 compact, 2 solve, 3 final
+    unsigned done[8];    // same, 4 scan
     int n_eval;    // slots with an eval-phase job this step
     int n_final;   // slots finalising this step
+    int n_compact; // slots whose detect output is compacted this step
     int n_solve;   // (slot, side) solve items
     int solve_blocks;  // total blocks over solve items
     int active;    // slots not FREE/DONE
@@ -96,11 +105,12 @@ struct Ctrl {
     int hazards;
     int k_overflow;
     int step;
-    int pad[7];
+    int pad[6];
 };
 
 struct Arena {
     int L, G, tiles, cap, kcap;
+    long long Lp;  // padded slot-buffer stride (16-byte aligned rows)
     double sd_threshold;
     int max_sift_iters;
     int trace_cap;
@@ -109,7 +119,9 @@ struct Arena {
     double* kval;
     unsigned* toff;
     double* mom;
-    unsigned long long* status;
+    int* sidx;
+    double* sval;
+    unsigned* scnt;
     double* tnum;
     double* tden;
     unsigned long long* thash;
@@ -119,16 +131,17 @@ struct Arena {
     Ctrl* ctrl;
     int* eval_list;   // [G]
     int* final_list;  // [G]
+    int* compact_list; // [G]
     int* solve_item;  // [2G] (slot << 1 | side)
     int* solve_off;   // [2G+1] block prefix
-    double* sb;       // [2][G][max_blocks][4] solve block boundary values
+    double* sb;       // [2][G][max_blocks][6] solve block boundary values
     int max_blocks;
     TraceRec* trace;
     int* status_host; // mapped pinned: [0] active slots after this step, [1] step counter
 };
 
 __host__ __device__ inline size_t buf_off(const Arena& a, int slot, int b) {
-    return ((size_t)slot * 3 + (size_t)b) * (size_t)a.L;
+    return ((size_t)slot * 3 + (size_t)b) * (size_t)a.Lp;
 }
 __host__ __device__ inline size_t knot_off(const Arena& a, int par, int side, int slot) {
     return (((size_t)par * 2 + side) * a.G + slot) * (size_t)a.cap;
@@ -139,7 +152,10 @@ __host__ __device__ inline size_t toff_off(const Arena& a, int par, int side, in
 __host__ __device__ inline size_t mom_off(const Arena& a, int side, int slot) {
     return ((size_t)side * a.G + slot) * (size_t)(a.cap + 4);
 }
-__host__ __device__ inline size_t status_off(const Arena& a, int side, int slot) {
+__host__ __device__ inline size_t stage_off(const Arena& a, int side, int slot) {
+    return ((size_t)side * a.G + slot) * (size_t)a.tiles * kTileKnots;
+}
+__host__ __device__ inline size_t scnt_off(const Arena& a, int side, int slot) {
     return ((size_t)side * a.G + slot) * (size_t)a.tiles;
 }
 

@@ -42,7 +42,7 @@ class TestRng:
         return lo + self.next_u64() % (hi - lo + 1)
 
 
-def test_rng_signal(seed: int, n: int) -> np.ndarray:
+def rng_signal(seed: int, n: int) -> np.ndarray:
     g = TestRng(seed)
     return np.array([g.uniform() for _ in range(n)], dtype=np.float64)
 

@@ -25,7 +25,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle.ffi import Ref  # noqa: E402
-from tests.golden.inputs import (C_CONFIGS, kat_envelope_cases, kat_extrema_cases, test_rng_signal,  # noqa: E402
+from tests.golden.inputs import (C_CONFIGS, kat_envelope_cases, kat_extrema_cases, rng_signal,  # noqa: E402
                                  pickup_serialized)
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -70,7 +70,7 @@ def main() -> None:
     rnd = []
     for seed, n, imfs in [(11, 600, 0), (12, 500, 2), (21, 400, 0), (23, 400, 0), (31, 37, 0), (99, 4, 0),
                           (98, 5, 0), (97, 64, 0)]:
-        x = test_rng_signal(seed, n)
+        x = rng_signal(seed, n)
         imf, res, counts, trace = r.emd_traced(x, imfs=imfs)
         rnd.append({"seed": seed, "n": n, "max_imfs": imfs, "K": int(imf.shape[0]), "counts": counts.tolist(),
                     "imfs_sha256": sha(imf), "residue_sha256": sha(res),
@@ -80,7 +80,7 @@ def main() -> None:
     # small ensembles (test_emd.cpp:281-293, :330-343)
     ens = []
     for algo, seed, n, nr in [(1, 22, 300, 10), (2, 24, 300, 8), (1, 21, 400, 3), (2, 23, 200, 5)]:
-        x = test_rng_signal(seed, n)
+        x = rng_signal(seed, n)
         imf, res = r.decompose(x, algo, nr=nr)
         ens.append({"algo": algo, "seed": seed, "n": n, "nr": nr, "K": int(imf.shape[0]),
                     "imfs_sha256": sha(imf), "residue_sha256": sha(res),

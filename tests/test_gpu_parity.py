@@ -1,0 +1,372 @@
+"""Parity of the sm_100a engine (through the C ABI) against the oracle and the
+reference's golden vectors. Bar: bit-exact for indices, counts, traces and
+every value whose inputs are identical (EMD, serializer, spline, and EEMD /
+CEEMDAN with the oracle's noise injected); rel-L2 <= 1e-9 per IMF when the
+noise comes from the device RNG (its libm log/sin/cos differ by <= 2 ulp).
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT, fromhex, sha, sort_trace
+from tests.golden.inputs import TestRng, rng_signal, sine
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-9  # north_star tolerance for fp64 IMFs
+
+
+def pickup_serialized(se, D):
+    from paper_2106_15319_b200 import workloads as W
+    return se.concatenate(W.pickup_signals(), D)
+
+
+def rel_l2(a, b):
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+def hazards(se):
+    return se.context().stats()["solve_hazards"]
+
+
+# ------------------------------------------------------------------ primitives
+
+def test_rng_stream_bit_exact(se, oracle, golden):
+    c = se.context()
+    assert int(c.mt19937_64(5489, 10000)[-1]) == 9981545732273789042
+    for seed in (oracle.derive_seed(0, 0), 7, 0, 2**64 - 1):
+        assert np.array_equal(c.mt19937_64(seed, 4096), oracle.mt19937_64(seed, 4096))
+
+
+def test_white_noise(se, oracle, golden):
+    for n, seed in [(4, oracle.derive_seed(0, 0)), (1001, 7), (100000, 3)]:
+        w, ow = se.white_noise(n, seed), oracle.white_noise(n, seed)
+        # CUDA log/sin/cos vs glibc: a few ulp of the Box-Muller radius (cos/sin near a zero
+        # crossing amplify the relative error of a tiny result, not the absolute one)
+        assert np.max(np.abs(w - ow) / np.spacing(np.maximum(np.abs(ow), 0.5))) <= 4.0
+        assert np.mean(w == ow) > 0.8
+    assert abs(np.std(se.white_noise(100000, 3)) - 1.0) <= 0.02  # test_emd.cpp:224-227
+    assert np.array_equal(se.white_noise(64, 5, 0.0), np.zeros(64))
+    with pytest.raises(se.InvalidInput, match="white_noise: std must be non-negative"):
+        se.white_noise(8, 0, -1.0)
+
+
+def test_signal_std_bit_exact(se, oracle):
+    for n in (1, 5, 6250, 100003, 2_000_001):
+        x = np.random.default_rng(n).standard_normal(n) * 3 + 1
+        assert se.signal_std(x) == oracle.signal_std(x)
+
+
+def test_find_extrema_golden(se, golden):
+    for case in golden["find_extrema"]:
+        x = fromhex(case["x"])
+        mi, mv, ni, nv = se.find_extrema(x)
+        assert mi.tolist() == case["max_idx"], case["name"]
+        assert ni.tolist() == case["min_idx"], case["name"]
+        assert np.array_equal(mv, fromhex(case["max_val"])) and np.array_equal(nv, fromhex(case["min_val"]))
+    with pytest.raises(se.InvalidInput, match="find_extrema: signal too short"):
+        se.find_extrema([1.0, 2.0])
+
+
+def test_find_extrema_random_and_plateaus(se, oracle):
+    rng = np.random.default_rng(1)
+    for trial in range(40):
+        n = int(rng.integers(3, 9000))
+        x = rng.integers(-2, 3, size=n).astype(float) if trial % 2 else rng.standard_normal(n)
+        a, b = se.find_extrema(x), oracle.find_extrema(x)
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v)
+    # a plateau run crossing many eval tiles (2048 samples each)
+    x = np.concatenate([np.zeros(10), np.ones(5000), np.zeros(3000), -np.ones(7001), np.zeros(3)])
+    for u, v in zip(se.find_extrema(x), oracle.find_extrema(x)):
+        assert np.array_equal(u, v)
+
+
+def test_envelope_golden_and_random(se, oracle, golden):
+    for case in golden["envelope"]:
+        out = se.envelope(case["idx"], fromhex(case["val"]), case["length"])
+        assert np.array_equal(out, fromhex(case["out"])), case["name"]
+    rng = np.random.default_rng(2)
+    for _ in range(30):
+        length = int(rng.integers(5, 3000))
+        k = int(rng.integers(2, min(200, length)))
+        idx = np.sort(rng.choice(length, size=k, replace=False))
+        val = rng.standard_normal(k)
+        assert np.array_equal(se.envelope(idx, val, length), oracle.envelope(idx, val, length))
+    with pytest.raises(se.InsufficientExtrema, match="envelope: need at least 2 extrema, got 1"):
+        se.envelope([4], [1.0], 10)
+
+
+# ------------------------------------------------------------------ sifting
+
+def test_extract_imf(se, oracle):
+    from oracle.ffi import OracleError
+    for seed, n, iters in [(11, 600, 300), (5, 5000, 3), (9, 20000, 300), (3, 7, 300), (8, 12, 300)]:
+        x = rng_signal(seed, n)
+        try:
+            oimf, ocnt = oracle.extract_imf(x, iters=iters)
+        except OracleError as e:
+            with pytest.raises(se.InvalidInput) as g:
+                se.extract_imf(x, max_sift_iters=iters)
+            assert str(g.value) == str(e)
+            continue
+        imf, cnt = se.extract_imf(x, max_sift_iters=iters)
+        assert cnt == ocnt and np.array_equal(imf, oimf)
+    x = sine(8.0, 1000, 1000.0)
+    imf, _ = se.extract_imf(x)
+    assert np.corrcoef(imf, x)[0, 1] >= 0.99  # test_emd.cpp:114-118
+    with pytest.raises(se.InsufficientExtrema):
+        se.extract_imf(np.arange(50.0))
+    imf, cnt = se.extract_imf(rng_signal(4, 100), max_sift_iters=0)
+    assert cnt == 0 and np.array_equal(imf, rng_signal(4, 100))
+
+
+def test_emd_golden_random(se, golden):
+    for case in golden["emd_random"]:
+        x = rng_signal(case["seed"], case["n"])
+        if case["n"] < 4:
+            continue
+        d = se.decompose_full(x, "emd", max_imfs=case["max_imfs"], trace_cap=100000)
+        assert d["imfs"].shape[0] == case["K"]
+        assert d["sift_counts"].tolist() == case["counts"]
+        assert sha(d["imfs"]) == case["imfs_sha256"] and sha(d["residue"]) == case["residue_sha256"]
+        got = [[int(t[k]) for k in ("k", "iter", "n_max", "n_min", "hash")] for t in sort_trace(d["trace"])]
+        assert got == case["trace"]
+    assert hazards(se) == 0
+
+
+@pytest.mark.parametrize("n", [4, 5, 17, 2047, 2048, 2049, 6001, 40961, 250_000])
+def test_emd_bit_exact_lengths(se, oracle, n):
+    x = rng_signal(1000 + n, n) + 0.001 * np.arange(n)
+    d = se.decompose_full(x, "emd", trace_cap=200000)
+    o = oracle.emd(x, trace_cap=200000)
+    assert d["imfs"].shape == o[0].shape
+    assert np.array_equal(d["imfs"], o[0]) and np.array_equal(d["residue"], o[1])
+    assert d["sift_counts"].tolist() == o[2].tolist()
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(o[3]))
+    assert hazards(se) == 0
+
+
+def test_emd_edge_cases(se, oracle):
+    ramp = 0.25 * np.arange(64)
+    d = se.decompose(ramp)
+    assert d["imfs"].shape[0] == 0 and np.array_equal(d["residue"], ramp)  # test_emd.cpp:144-150
+    with pytest.raises(se.InvalidInput, match="emd: signal too short"):
+        se.decompose([1.0, 2.0, 1.0])
+    x = rng_signal(12, 500)
+    d = se.decompose(x, max_imfs=2)
+    assert d["imfs"].shape[0] == 2
+    assert np.max(np.abs(d["imfs"].sum(0) + d["residue"] - x)) <= 1e-8
+    const = np.full(100, 3.5)
+    assert se.decompose(const)["imfs"].shape[0] == 0
+    # clipped / plateau-rich input (exact equality runs)
+    y = np.clip(np.round(4 * np.sin(np.arange(3000) * 0.01) + rng_signal(3, 3000)), -3, 3)
+    d, o = se.decompose_full(y, "emd", trace_cap=100000), oracle.emd(y, trace_cap=100000)
+    assert np.array_equal(d["imfs"], o[0]) and np.array_equal(d["residue"], o[1])
+
+
+def test_c1_serial_emd(se, golden, golden_traces):
+    c = golden["configs"]["c1_emd_D50"]
+    s = pickup_serialized(se, 50)
+    assert sha(s) == c["input_sha256"]
+    d = se.decompose_full(s, "emd", max_sift_iters=1000, trace_cap=10000)
+    assert d["imfs"].shape[0] == 6 and d["sift_counts"].tolist() == c["counts"] == [2, 2, 2, 2, 1, 1]
+    assert sha(d["imfs"]) == c["imfs_sha256"] and sha(d["residue"]) == c["residue_sha256"]
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(golden_traces["c1_emd_D50"]))
+    assert d["stats"]["sifted_samples"] == c["sifted_samples"] == 62_500
+
+
+# ------------------------------------------------------------------ ensembles
+
+@pytest.mark.parametrize("name", ["c2_eemd_D1", "c2_eemd_D50", "c2_eemd_D500"])
+def test_c2_eemd(se, oracle, golden, golden_traces, name):
+    c = golden["configs"][name]
+    s = pickup_serialized(se, c["D"])
+    d = se.decompose_full(s, "eemd", max_imfs=c["imfs"], nr=c["nr"], trace_cap=100000)
+    o_imfs, o_res, _, _ = oracle.decompose(s, 1, imfs=c["imfs"], nr=c["nr"])
+    assert d["imfs"].shape == o_imfs.shape and d["imfs"].shape[0] == c["K"]
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(golden_traces[name]))  # extrema + sift counts
+    for k in range(c["K"]):
+        assert rel_l2(d["imfs"][k], o_imfs[k]) <= REL_L2
+    assert rel_l2(d["residue"], o_res) <= REL_L2
+    assert d["stats"]["sifted_samples"] == c["sifted_samples"]
+    # with the reference's own noise injected, the whole ensemble is bit-exact
+    ctx = se.context()
+    ctx.set_noise_override(np.stack([oracle.white_noise(s.size, oracle.derive_seed(0, m)) for m in range(c["nr"])]))
+    try:
+        e = se.decompose(s, "eemd", max_imfs=c["imfs"], nr=c["nr"])
+    finally:
+        ctx.set_noise_override(None)
+    assert sha(e["imfs"]) == c["imfs_sha256"] and sha(e["residue"]) == c["residue_sha256"]
+    assert hazards(se) == 0
+
+
+def test_c3_ceemdan(se, oracle, golden, golden_traces):
+    c = golden["configs"]["c3_ceemdan_D50"]
+    s = pickup_serialized(se, 50)
+    d = se.decompose_full(s, "ceemdan", max_sift_iters=5000, nr=500, trace_cap=100000)
+    assert d["imfs"].shape[0] == c["K"] == 9
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(golden_traces["c3_ceemdan_D50"]))
+    o_imfs, o_res, _, _ = oracle.decompose(s, 2, iters=5000, nr=500)
+    for k in range(9):
+        assert rel_l2(d["imfs"][k], o_imfs[k]) <= REL_L2
+    ctx = se.context()
+    ctx.set_noise_override(np.stack([oracle.white_noise(s.size, oracle.derive_seed(0, m)) for m in range(500)]))
+    try:
+        e = se.decompose(s, "ceemdan", max_sift_iters=5000, nr=500)
+    finally:
+        ctx.set_noise_override(None)
+    assert sha(e["imfs"]) == c["imfs_sha256"] and sha(e["residue"]) == c["residue_sha256"]
+
+
+def test_small_ensembles_golden(se, oracle, golden):
+    ctx = se.context()
+    for case in golden["ensembles_small"]:
+        x = rng_signal(case["seed"], case["n"])
+        ctx.set_noise_override(np.stack([oracle.white_noise(x.size, oracle.derive_seed(0, m))
+                                         for m in range(case["nr"])]))
+        try:
+            d = se.decompose(x, ["emd", "eemd", "ceemdan"][case["algo"]], nr=case["nr"])
+        finally:
+            ctx.set_noise_override(None)
+        assert sha(d["imfs"]) == case["imfs_sha256"] and sha(d["residue"]) == case["residue_sha256"]
+
+
+def test_ensemble_properties(se):
+    x = rng_signal(22, 300)
+    a, b = se.eemd(x, nr=10), se.eemd(x, nr=10)
+    assert np.array_equal(a["imfs"], b["imfs"]) and np.array_equal(a["residue"], b["residue"])  # deterministic
+    assert np.max(np.abs(a["imfs"].sum(0) + a["residue"] - x)) <= 1e-8 * np.max(np.abs(x))
+    c1, c2 = se.ceemdan(x, nr=8), se.ceemdan(x, nr=8)
+    assert np.array_equal(c1["imfs"], c2["imfs"])
+    assert np.max(np.abs(c1["imfs"].sum(0) + c1["residue"] - x)) <= 1e-8 * np.max(np.abs(x))
+    # nstd = 0 degenerates to plain emd exactly (acceptance criterion 9)
+    e = se.emd(x)
+    for algo in ("eemd", "ceemdan"):
+        d = se.decompose(x, algo, nstd=0.0, nr=3)
+        assert np.array_equal(d["imfs"], e["imfs"]) and np.array_equal(d["residue"], e["residue"])
+    with pytest.raises(se.InvalidInput, match="ensemble: nr must be at least 1"):
+        se.eemd(x, nr=0)
+    with pytest.raises(se.InvalidInput, match="ensemble: nstd must be non-negative"):
+        se.ceemdan(x, nstd=-1.0)
+    with pytest.raises(se.InvalidInput, match="ceemdan: signal too short"):
+        se.ceemdan([1.0, 2.0, 3.0])
+
+
+# ------------------------------------------------------------------ serializer
+
+def test_concatenate_sweep(se, oracle):
+    g = TestRng(34)
+    for _ in range(120):
+        m, n = g.range(4, 60), g.range(1, 8)
+        d = g.range(1, m)
+        x = np.array([g.uniform() for _ in range(m * n)]).reshape(n, m)  # channel rows
+        ms = np.ascontiguousarray(x.T)  # (M, N) samples x channels
+        a = se.concatenate(ms, d)
+        assert np.array_equal(a, oracle.concatenate(x, m, n, d))
+        assert np.array_equal(se.concatenate_naive(ms, d), a)
+    with pytest.raises(se.InvalidInput, match="concatenate: transition longer than channel"):
+        se.concatenate(np.ones((10, 2)), 11)
+    with pytest.raises(se.InvalidInput, match="concatenate: D must be at least 1"):
+        se.concatenate(np.ones((10, 2)), 0)
+    assert np.array_equal(se.transition_weights(4), [0.2, 0.4, 0.6, 0.8])
+    assert se.default_transition_length(1000) == 200
+
+
+def test_deconcatenate_and_serial(se, oracle):
+    m, n, d = 10, 3, 4
+    mode = np.zeros(m * n + d * (n - 1))
+    for j in range(n - 1):
+        mode[j * (m + d) + m: j * (m + d) + m + d] = 999.0  # poisoned transitions never leak
+    t = se.deconcatenate(mode[:, None], m, n, d)
+    assert t.shape == (m, n, 1) and np.all(t == 0.0)
+    with pytest.raises(se.InvalidInput, match="deconcatenate: mode length 11 does not match"):
+        se.deconcatenate(np.zeros((11, 1)), 10, 1, 2)
+    x6 = oracle.multivariate_sinusoids()
+    t, _ = se.serial_decompose_full(np.ascontiguousarray(x6.T), 50, "emd")
+    o, _ = oracle.serial_decompose(x6, 1000, 6, 50, 0)
+    assert np.array_equal(t, o.transpose(2, 1, 0))
+    assert np.max(np.abs(t.sum(axis=2) - x6.T)) <= 1e-8 * np.max(np.abs(x6))
+    te = se.serial_decompose(np.ascontiguousarray(x6.T), 50, "eemd", nr=8)
+    assert np.max(np.abs(te.sum(axis=2) - x6.T)) <= 1e-8 * np.max(np.abs(x6))
+
+
+def test_slicewise(se, oracle):
+    x = np.random.default_rng(11).standard_normal((120, 3))
+    t = se.slicewise_decompose(x)
+    single = se.decompose(x[:, 1])
+    assert np.array_equal(t[:, 1, 0], single["imfs"][0])
+    assert np.max(np.abs(t.sum(axis=2) - x)) <= 1e-10 * np.max(np.abs(x))
+
+
+# ------------------------------------------------------------------ full-size properties
+
+def _c4_serialized(se):
+    from paper_2106_15319_b200 import workloads as W
+    return se.concatenate(W.image_batch(), 10)
+
+
+@pytest.mark.slow
+def test_c4_one_realization_bit_exact(se, oracle):
+    s = _c4_serialized(se)
+    assert s.size == 2_924_534
+    ctx = se.context()
+    ctx.set_noise_override(oracle.white_noise(s.size, oracle.derive_seed(0, 0))[None, :])
+    try:
+        d = se.decompose_full(s, "eemd", nr=1, trace_cap=2000)
+    finally:
+        ctx.set_noise_override(None)
+    o = oracle.decompose(s, 1, nr=1, trace_cap=2000)
+    assert np.array_equal(d["imfs"], o[0]) and np.array_equal(d["residue"], o[1])
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(o[3]))
+    assert hazards(se) == 0
+
+
+@pytest.mark.slow
+def test_c4_full_ensemble_properties(se):
+    s = _c4_serialized(se)
+    a = se.decompose_full(s, "eemd", nr=100)
+    assert np.max(np.abs(a["imfs"].sum(0) + a["residue"] - s)) <= 1e-8 * np.max(np.abs(s))
+    b = se.decompose(s, "eemd", nr=100)
+    assert np.array_equal(a["imfs"], b["imfs"])  # bit-reproducible run to run
+    assert a["stats"]["solve_hazards"] == 0
+
+
+@pytest.mark.slow
+def test_c5_realizations(se, oracle):
+    from paper_2106_15319_b200 import workloads as W
+    s = se.concatenate(W.sine_variates(), 64)
+    assert s.size == 17_039_296
+    d = se.decompose_full(s, "eemd", nr=2, trace_cap=4000)
+    assert np.max(np.abs(d["imfs"].sum(0) + d["residue"] - s)) <= 1e-8 * np.max(np.abs(s))
+    assert d["stats"]["solve_hazards"] == 0
+    # realization-level trace parity for one realization against the oracle
+    # (the oracle runs the same x + beta*w_0 with the device noise injected)
+    ctx = se.context()
+    w0 = se.white_noise(s.size, oracle.derive_seed(0, 0))
+    ctx.set_noise_override(w0[None, :])
+    try:
+        g = se.decompose_full(s, "eemd", nr=1, trace_cap=4000)
+    finally:
+        ctx.set_noise_override(None)
+    beta = 0.2 * se.signal_std(s)
+    o = oracle.emd(s + beta * w0, trace_cap=4000)
+    assert np.array_equal(sort_trace(g["trace"]), sort_trace(o[3]))
+    for k in range(o[0].shape[0]):
+        assert rel_l2(g["imfs"][k], o[0][k]) <= REL_L2
+
+
+def test_cpp_mirror_runs(se):
+    from paper_2106_15319_b200 import _native
+    exe = "/tmp/test_semd_cpp"
+    src = os.path.join(ROOT, "tests", "cpp", "test_semd_cpp.cpp")
+    libdir = os.path.dirname(_native.LIB_PATH)
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"), src, "-o", exe,
+                        "-L" + libdir, "-lsemd_b200", "-Wl,-rpath," + libdir], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("OK")
