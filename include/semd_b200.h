@@ -159,6 +159,10 @@ int semd_eemd_partial_device(semd_ctx* ctx, const double* d_x, size_t n, const s
 /* imfs *= 1/nr; residue = x - sum_k imfs_k (emd.cpp:252-260). */
 int semd_ensemble_finish_device(semd_ctx* ctx, const double* d_x, size_t n, double* d_sums, size_t K, int32_t nr,
                                 double* d_residue);
+/* serialize.cpp:30-50 / :73-95 on device buffers (same layouts as the host versions). */
+int semd_concatenate_device(semd_ctx* ctx, const double* d_x, size_t M, size_t N, size_t D, double* d_out);
+int semd_deconcatenate_device(semd_ctx* ctx, const double* d_modes, size_t K, size_t L, size_t M, size_t N, size_t D,
+                              double* d_out);
 int semd_serial_decompose_device(semd_ctx* ctx, int algo, const double* d_x, size_t M, size_t N, size_t D,
                                  const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* d_tensor,
                                  size_t k_cap, size_t* modes_out);

@@ -86,6 +86,9 @@ SIGNATURES = {
                                            C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, _szp]),
     "semd_ensemble_finish_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int32,
                                               C.c_void_p]),
+    "semd_concatenate_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p]),
+    "semd_deconcatenate_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t,
+                                            C.c_size_t, C.c_void_p]),
     "semd_serial_decompose_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
                                                C.POINTER(SiftCfg), C.POINTER(EnsCfg), C.c_void_p, C.c_size_t,
                                                _szp]),

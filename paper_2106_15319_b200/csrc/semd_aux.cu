@@ -371,19 +371,25 @@ void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t s
     const long long pairs = (n + 1) / 2;
     const int grid = (int)((pairs + 255) / 256 < 4096 ? (pairs + 255) / 256 : 4096);
     k_box_muller<<<grid > 0 ? grid : 1, 256, 0, st>>>(draws, n, stdv);
+    count_launches(1);
 }
 void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st) {
     if (n <= kStdExactMax) {
         k_signal_std<<<1, 64, 0, st>>>(x, n, out, scale);
+        count_launches(1);
         return;
     }
     // out[1] = mean scratch, out[2..] = block partials
     double* mean = out + 1;
     double* part = out + 2;
     k_std_partial<<<kStdBlocks, 256, 0, st>>>(x, n, nullptr, part);
+    count_launches(1);
     k_std_final<<<1, 32, 0, st>>>(part, kStdBlocks, n, mean, out, scale, 0);
+    count_launches(1);
     k_std_partial<<<kStdBlocks, 256, 0, st>>>(x, n, mean, part);
+    count_launches(1);
     k_std_final<<<1, 32, 0, st>>>(part, kStdBlocks, n, mean, out, scale, 1);
+    count_launches(1);
 }
 static int grid_for(long long n) {
     long long g = (n + 255) / 256;
@@ -393,39 +399,50 @@ static int grid_for(long long n) {
 void launch_ensemble_finish(double* sums, int K, long long L, const double* x, double* residue, double inv,
                             cudaStream_t st) {
     k_ensemble_finish<<<grid_for(L), 256, 0, st>>>(sums, K, L, x, residue, inv);
+    count_launches(1);
 }
 void launch_concatenate(const double* x, long long M, long long N, long long D, const double* a, double* out,
                         int naive, cudaStream_t st) {
     k_concatenate<<<grid_for(M * N + D * (N - 1)), 256, 0, st>>>(x, M, N, D, a, out, naive);
+    count_launches(1);
 }
 void launch_transition_weights(long long d, double* a, cudaStream_t st) {
     k_transition_weights<<<grid_for(d), 256, 0, st>>>(d, a);
+    count_launches(1);
 }
 void launch_deconcatenate(const double* modes, long long K, long long Lm, long long M, long long N, long long D,
                           double* out, cudaStream_t st) {
     k_deconcatenate<<<grid_for(K * N * M), 256, 0, st>>>(modes, K, Lm, M, N, D, out);
+    count_launches(1);
 }
 void launch_envelope(const double* xs, const double* ys, int n, double* mom, double* work, long long length,
                      double* out, cudaStream_t st) {
     k_envelope_solve<<<1, 32, 0, st>>>(xs, ys, n, mom, work);
+    count_launches(1);
     k_envelope_eval<<<grid_for(length), 256, 0, st>>>(xs, ys, mom, n, length, out);
+    count_launches(1);
 }
 void launch_stage_scale(double* mode, long long n, double inv, int* nonzero, cudaStream_t st) {
     k_stage_scale<<<grid_for(n), 256, 0, st>>>(mode, n, inv, nonzero);
+    count_launches(1);
 }
 void launch_sub(double* residue, const double* mode, long long n, cudaStream_t st) {
     k_sub<<<grid_for(n), 256, 0, st>>>(residue, mode, n);
+    count_launches(1);
 }
 void launch_envelope_knots(const unsigned long long* idx, const double* val, long long n, long long length,
                            double* xs, double* ys, cudaStream_t st) {
     k_envelope_knots<<<grid_for(n + 4), 256, 0, st>>>(idx, val, n, length, xs, ys);
+    count_launches(1);
 }
 void launch_fill(double* p, long long n, double v, cudaStream_t st) { k_fill<<<grid_for(n), 256, 0, st>>>(p, n, v); }
 void launch_copy(const double* src, double* dst, long long n, cudaStream_t st) {
     k_copy<<<grid_for(n), 256, 0, st>>>(src, dst, n);
+    count_launches(1);
 }
 void launch_axpy(const double* a, const double* b, double beta, double* out, long long n, cudaStream_t st) {
     k_axpy<<<grid_for(n), 256, 0, st>>>(a, b, beta, out, n);
+    count_launches(1);
 }
 
 }  // namespace dev

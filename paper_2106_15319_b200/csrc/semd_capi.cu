@@ -276,13 +276,37 @@ struct semd_ctx {
         *(volatile int*)status_host = c.active;
     }
 
+    // per-step sift-kernel events (timing mode): a ring, harvested every R steps
+    std::vector<cudaEvent_t> tev;
+    void harvest(int from, int to) {  // accumulate eval durations of steps [from, to)
+        for (int s = from; s < to; ++s) {
+            float ms = 0.f;
+            const int i = (s % kTimedRing) * 2;
+            ck(cudaEventSynchronize(tev[i + 1]), "timing event");
+            ck(cudaEventElapsedTime(&ms, tev[i], tev[i + 1]), "timing");
+            stats.eval_ms += ms;
+        }
+    }
+    static constexpr int kTimedRing = 64;
+
     void run(int max_steps) {
         const int LAG = 3, R = 16;
-        int step = 0;
-        if (timing) ck(cudaEventRecord(t0, stream), "event");
+        int step = 0, harvested = 0;
+        if (timing && tev.empty()) {
+            tev.resize(2 * kTimedRing);
+            for (auto& e : tev) ck(cudaEventCreate(&e), "event");
+        }
         for (;; ++step) {
-            semd::dev::launch_step(A, sms, stream);
-            stats.kernel_launches += 5;
+            cudaEvent_t eb = nullptr, ee = nullptr;
+            if (timing) {
+                if (step - harvested >= kTimedRing - 1) {
+                    harvest(harvested, step - LAG);
+                    harvested = step - LAG;
+                }
+                eb = tev[(step % kTimedRing) * 2];
+                ee = tev[(step % kTimedRing) * 2 + 1];
+            }
+            semd::dev::launch_step(A, sms, stream, eb, ee);
             stats.eval_launches += 1;
             ck(cudaGetLastError(), "launch step");
             ck(cudaEventRecord(ev[step % R], stream), "event record");
@@ -293,13 +317,7 @@ struct semd_ctx {
             if (step > max_steps) raise(SEMD_CUDA_ERROR, "engine did not converge within %d steps", max_steps);
         }
         ck(cudaStreamSynchronize(stream), "engine run");
-        if (timing) {
-            ck(cudaEventRecord(t1, stream), "event");
-            ck(cudaEventSynchronize(t1), "event");
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, t0, t1);
-            stats.eval_ms += ms;
-        }
+        if (timing) harvest(harvested, step + 1);
         stats.steps += step + 1;
         ck(cudaMemcpy(h_slots.data(), A.slots, (size_t)A.G * sizeof(Slot), cudaMemcpyDeviceToHost), "download slots");
         Ctrl c{};
@@ -329,9 +347,11 @@ struct semd_ctx {
         return (int)std::min<long long>((long long)(A.kcap + 2) * it + 64, 1LL << 30);
     }
 
+    unsigned long long launches_at_reset = 0;
     void reset_stats(int slots_used) {
         stats = semd_stats{};
         stats.slots = slots_used;
+        launches_at_reset = semd::dev::launch_count();
     }
 
     double* buf(int slot, int b) { return A.bufs + semd::dev::buf_off(A, slot, b); }
@@ -777,6 +797,7 @@ void semd_ctx_destroy(semd_ctx* ctx) {
 int semd_get_stats(semd_ctx* ctx, semd_stats* out) {
     return guard([&] {
         if (!ctx || !out) raise(SEMD_INVALID_INPUT, "null argument");
+        ctx->stats.kernel_launches = semd::dev::launch_count() - ctx->launches_at_reset;
         *out = ctx->stats;
     });
 }
@@ -1088,6 +1109,26 @@ int semd_concatenate(semd_ctx* ctx, const double* x, size_t M, size_t N, size_t 
 }
 int semd_concatenate_naive(semd_ctx* ctx, const double* x, size_t M, size_t N, size_t D, double* out) {
     return concat_host(ctx, x, M, N, D, out, 1);
+}
+
+int semd_concatenate_device(semd_ctx* ctx, const double* d_x, size_t M, size_t N, size_t D, double* d_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        concat_device(ctx, d_x, M, N, D, d_out, 0);
+        ck(cudaStreamSynchronize(ctx->stream), "concatenate");
+    });
+}
+
+int semd_deconcatenate_device(semd_ctx* ctx, const double* d_modes, size_t K, size_t L, size_t M, size_t N, size_t D,
+                              double* d_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        validate_deconcat(K, L, M, N, D);
+        semd::dev::launch_deconcatenate(d_modes, (long long)K, (long long)L, (long long)M, (long long)N, (long long)D,
+                                        d_out, ctx->stream);
+        ck(cudaGetLastError(), "deconcatenate");
+        ck(cudaStreamSynchronize(ctx->stream), "deconcatenate");
+    });
 }
 
 int semd_deconcatenate(semd_ctx* ctx, const double* modes, size_t K, size_t L, size_t M, size_t N, size_t D,

@@ -18,7 +18,10 @@ struct RngJob {
 size_t eval_smem_bytes();
 size_t solve_smem_bytes();
 cudaError_t launch_setup();
-void launch_step(const Arena& A, int sms, cudaStream_t st);
+void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begin = nullptr,
+                 cudaEvent_t eval_end = nullptr);
+unsigned long long launch_count();  // kernels launched by this library (all contexts)
+void count_launches(int n);
 void launch_rng(const RngJob* jobs, int njobs, cudaStream_t st);
 void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t st);
 void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st);

@@ -1188,12 +1188,19 @@ cudaError_t launch_setup() {
     return cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem_bytes());
 }
 
-void launch_step(const Arena& A, int sms, cudaStream_t st) {
+static unsigned long long g_launches = 0;
+unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+void count_launches(int n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+
+void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begin, cudaEvent_t eval_end) {
     k_solve<<<2 * sms, kSolveThreads, solve_smem_bytes(), st>>>(A);
+    if (eval_begin) cudaEventRecord(eval_begin, st);
     k_eval<<<2 * sms, kEvalThreads, eval_smem_bytes(), st>>>(A);
+    if (eval_end) cudaEventRecord(eval_end, st);
     k_scan<<<2 * A.G, 256, 0, st>>>(A);
     k_compact<<<2 * sms, 256, 0, st>>>(A);
     k_final<<<2 * sms, 256, 0, st>>>(A);
+    count_launches(5);
 }
 
 }  // namespace dev
