@@ -63,6 +63,44 @@ __global__ void __launch_bounds__(320) k_mt19937_64(const RngJob* jobs) {
     }
 }
 
+// One CTA per realization m0 + blockIdx.x of an ensemble: seed = derive_seed(base, m)
+// (emd.cpp:174-179, :238), draws into out + blockIdx.x * stride.
+__global__ void __launch_bounds__(320) k_mt19937_64_ens(uint64_t base, long long m0, uint64_t* out, long long stride,
+                                                       long long n) {
+    __shared__ uint64_t mt[312];
+    const int t = threadIdx.x;
+    uint64_t* dst = out + blockIdx.x * stride;
+    if (t == 0) {
+        uint64_t z = base + 0x9E3779B97F4A7C15ULL * ((uint64_t)(m0 + blockIdx.x) + 1);
+        mt[0] = mix64(z);
+        for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+    }
+    __syncthreads();
+    const long long ndraw = 2 * ((n + 1) / 2);
+    for (long long b0 = 0; b0 < ndraw; b0 += 312) {
+        uint64_t a = 0, b = 0, c = 0;
+        if (t < 312) {
+            a = mt[t];
+            b = mt[(t + 1) % 312];
+            c = mt[(t + 156) % 312];
+        }
+        __syncthreads();
+        if (t < 156) mt[t] = c ^ mt_twist(a, b);
+        __syncthreads();
+        if (t >= 156 && t < 311) mt[t] = mt[t - 156] ^ mt_twist(a, b);
+        if (t == 311) mt[311] = mt[155] ^ mt_twist(a, mt[0]);
+        __syncthreads();
+        if (t < 312 && b0 + t < ndraw) {
+            uint64_t y = mt[t];
+            y ^= (y >> 29) & 0x5555555555555555ULL;
+            y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+            y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+            y ^= y >> 43;
+            dst[b0 + t] = y;
+        }
+    }
+}
+
 // In place: draws (u64 pairs) -> Gaussian samples (f64), emd.cpp:189-198.
 __global__ void k_box_muller(uint64_t* draws, long long n, double stdv) {
     const long long pairs = (n + 1) / 2;
@@ -367,6 +405,11 @@ namespace semd {
 namespace dev {
 
 void launch_rng(const RngJob* jobs, int njobs, cudaStream_t st) { k_mt19937_64<<<njobs, 320, 0, st>>>(jobs); }
+void launch_rng_ensemble(uint64_t base, long long m0, int count, uint64_t* out, long long stride, long long n,
+                         cudaStream_t st) {
+    k_mt19937_64_ens<<<count, 320, 0, st>>>(base, m0, out, stride, n);
+    count_launches(1);
+}
 void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t st) {
     const long long pairs = (n + 1) / 2;
     const int grid = (int)((pairs + 255) / 256 < 4096 ? (pairs + 255) / 256 : 4096);

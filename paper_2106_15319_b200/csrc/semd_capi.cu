@@ -120,7 +120,7 @@ struct semd_ctx {
     // engine arena
     Arena A{};
     int cfg_L = -1, cfg_G = -1, cfg_kcap = -1, cfg_trace = -1;
-    DBuf bufs, kidx, kval, toff, mom, sidx, sval, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace;
+    DBuf bufs, kidx, kval, toff, ktab, sidx, sval, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace;
     int* status_host = nullptr;
     int* status_host_dev = nullptr;
     std::vector<Slot> h_slots;
@@ -128,6 +128,8 @@ struct semd_ctx {
     // scratch
     DBuf in_x, in_y, noise, scratch, scratch2, scalar, rng_jobs;
     cudaEvent_t ev[16]{};
+    cudaStream_t rng_stream = nullptr;  // noise for the next wave is generated here, overlapping the sift
+    cudaEvent_t noise_ready[2]{};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
 
     ~semd_ctx() {
@@ -136,6 +138,9 @@ struct semd_ctx {
             if (e) cudaEventDestroy(e);
         if (t0) cudaEventDestroy(t0);
         if (t1) cudaEventDestroy(t1);
+        for (auto& e : noise_ready)
+            if (e) cudaEventDestroy(e);
+        if (rng_stream) cudaStreamDestroy(rng_stream);
         if (own) cudaStreamDestroy(own);
     }
 
@@ -146,21 +151,21 @@ struct semd_ctx {
         if (L >= (1LL << 30)) raise(SEMD_INVALID_INPUT, "signal too long for the engine (%lld samples)", L);
         if (L == cfg_L && G == cfg_G && kcap == cfg_kcap && trace_cap == cfg_trace) return;
         const int tiles = (int)((L + semd::dev::kEvalTile - 1) / semd::dev::kEvalTile);
-        const int cap = (int)(L / 2 + 2);
+        const int cap = (int)((L / 2 + 2 + 3) / 4 * 4);  // 16-byte aligned knot rows (bulk TMA staging)
         const int rows_max = cap + 2;
         const int max_blocks = rows_max / semd::dev::kSolveBlock + 2;
         const long long Lp = (L + 63) / 64 * 64;
         bufs.alloc((size_t)G * 3 * Lp * 8);
-        kidx.alloc((size_t)4 * G * cap * 4);
-        kval.alloc((size_t)4 * G * cap * 8);
+        kidx.alloc(((size_t)4 * G * cap + 16) * 4);
+        kval.alloc(((size_t)4 * G * cap + 16) * 8);
         toff.alloc((size_t)4 * G * (tiles + 1) * 4);
-        mom.alloc((size_t)2 * G * (cap + 4) * 8);
+        ktab.alloc(((size_t)2 * G * (cap + 8) + 16) * 32);
         sidx.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 4);
         sval.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 8);
         scnt.alloc((size_t)2 * G * tiles * 4);
         tnum.alloc((size_t)G * tiles * 8);
         tden.alloc((size_t)G * tiles * 8);
-        thash.alloc((size_t)G * tiles * 8);
+        thash.alloc((size_t)2 * G * tiles * 8);
         slots.alloc((size_t)G * sizeof(Slot));
         sums.alloc((size_t)kcap * L * 8);
         imf_sifts.alloc((size_t)kcap * 4);
@@ -179,7 +184,7 @@ struct semd_ctx {
         A.kidx = kidx.as<int>();
         A.kval = kval.as<double>();
         A.toff = toff.as<unsigned>();
-        A.mom = mom.as<double>();
+        A.ktab = ktab.as<double4>();
         A.sidx = sidx.as<int>();
         A.sval = sval.as<double>();
         A.scnt = scnt.as<unsigned>();
@@ -445,19 +450,32 @@ struct semd_ctx {
             configure(n, G, kcap, tr ? trace_cap_for(tr) : 0);
             A.sd_threshold = cfg.sd_threshold;
             A.max_sift_iters = cfg.max_sift_iters;
-            noise.alloc((size_t)G * Ls * 8);
+            noise.alloc((size_t)2 * G * Ls * 8);  // double-buffered: wave i+1's noise is made during wave i
             fill_sums(kcap, 0.0);
             h_trace.clear();
             trace_total = 0;
             int kmax_seen = 0, waves = 0;
+            auto nbuf = [&](int b) { return noise.as<double>() + (size_t)b * G * Ls; };
+            // noise of wave i lives in buffer i%2; generated on rng_stream (buffer i%2 was last read
+            // by wave i-2, whose run() the host has already synchronized), signalled by noise_ready
+            auto make_noise = [&](int w0, int b) {
+                const int g = std::min(G, m_end - w0);
+                semd::dev::launch_rng_ensemble(ens.base_seed, w0, g, reinterpret_cast<uint64_t*>(nbuf(b)), Ls, n,
+                                               rng_stream);
+                semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(nbuf(b)), (long long)g * Ls, 1.0, rng_stream);
+                ck(cudaGetLastError(), "rng");
+                ck(cudaEventRecord(noise_ready[b], rng_stream), "rng event");
+            };
             try {
-                for (int w0 = m_begin; w0 < m_end; w0 += G) {
+                if (!noise_override) make_noise(m_begin, 0);
+                int wi = 0;
+                for (int w0 = m_begin; w0 < m_end; w0 += G, ++wi) {
                     const int g = std::min(G, m_end - w0);
+                    const int b = wi & 1;
                     std::vector<JobSpec> js(g);
                     if (!noise_override) {
-                        std::vector<uint64_t> seeds(g);
-                        for (int i = 0; i < g; ++i) seeds[i] = derive_seed(ens.base_seed, (uint64_t)(w0 + i));
-                        gen_noise(seeds, n, Ls, noise.as<double>());
+                        if (w0 + G < m_end) make_noise(w0 + G, b ^ 1);  // overlaps this wave's sifting
+                        ck(cudaStreamWaitEvent(stream, noise_ready[b], 0), "noise wait");
                     }
                     for (int i = 0; i < g; ++i) {
                         JobSpec& J = js[i];
@@ -467,14 +485,16 @@ struct semd_ctx {
                         J.init_kind = 1;
                         J.beta = beta;
                         J.a = d_x;
-                        J.b = noise_override ? noise_override + (size_t)(w0 + i) * n : noise.as<double>() + (size_t)i * Ls;
+                        J.b = noise_override ? noise_override + (size_t)(w0 + i) * n : nbuf(b) + (size_t)i * Ls;
                     }
                     set_jobs(js);
                     run(max_steps_for(cfg));
                     ++waves;
                     for (int i = 0; i < g; ++i) kmax_seen = std::max(kmax_seen, h_slots[i].k);
                 }
+                ck(cudaStreamSynchronize(rng_stream), "rng");
             } catch (const Error& e) {
+                cudaStreamSynchronize(rng_stream);
                 if (e.code == SEMD_CAPACITY && attempt < 3 && cfg.max_imfs == 0) {
                     kcap *= 2;
                     continue;
@@ -772,6 +792,8 @@ int semd_ctx_create(int device, semd_ctx** out) {
             if (prop.major < 10) raise(SEMD_CUDA_ERROR, "device %s (sm_%d%d) is not sm_100", prop.name, prop.major, prop.minor);
             c->sms = prop.multiProcessorCount;
             ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&c->rng_stream, cudaStreamNonBlocking), "stream");
+            for (auto& e : c->noise_ready) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
             c->stream = c->own;
             for (auto& ev : c->ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
             ck(cudaEventCreate(&c->t0), "event");

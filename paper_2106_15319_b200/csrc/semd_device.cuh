@@ -92,20 +92,27 @@ __device__ __forceinline__ double spline_eval_fast(double x0, double x1, double 
     return a * y0 + b * y1 + div_rn(p, 6.0, 1.0 / 6.0);
 }
 
-// Envelope value at sample t from global knots (slow path for plateau runs
-// that leave a tile). seg = 1 + #{idx < t} (the reference's segment march).
-__device__ inline double envelope_at_global(const KnotView& kv, int t) {
-    int lo = 0, hi = kv.n;
+// The segment table of one envelope (written by k_solve): row v holds the
+// mirrored knot {x_v, y_v, m_v, RN(1/(x_{v+1}-x_v))}.
+struct TabView {
+    const double4* tab;
+    const int* idx;  // the real extrema positions (for the segment count)
+    int n;
+};
+
+// Envelope value at sample t (tile halos, plateau slow path): seg = 1 + #{idx < t}
+// (the reference's segment march), evaluated exactly like the tile fast path.
+__device__ inline double envelope_tab(const TabView& tv, int t) {
+    int lo = 0, hi = tv.n;
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (kv.idx[mid] < t) lo = mid + 1;
+        if (tv.idx[mid] < t) lo = mid + 1;
         else hi = mid;
     }
     const int seg = 1 + lo;
-    double x0, y0, x1, y1;
-    vknot(kv, seg, x0, y0);
-    vknot(kv, seg + 1, x1, y1);
-    return spline_eval_ref(x0, x1, y0, y1, kv.mom[seg], kv.mom[seg + 1], (double)t);
+    const double4 r0 = tv.tab[seg], r1 = tv.tab[seg + 1];
+    const double h = r1.x - r0.x;
+    return spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, (double)t);
 }
 
 __device__ __forceinline__ int pick_free_buffer(int xb, int cb) {

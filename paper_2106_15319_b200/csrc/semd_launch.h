@@ -16,6 +16,8 @@ struct RngJob {
 };
 
 size_t eval_smem_bytes();
+cudaError_t eval_setup();
+void launch_eval(const Arena& A, int sms, cudaStream_t st);
 size_t solve_smem_bytes();
 cudaError_t launch_setup();
 void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begin = nullptr,
@@ -23,6 +25,8 @@ void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begi
 unsigned long long launch_count();  // kernels launched by this library (all contexts)
 void count_launches(int n);
 void launch_rng(const RngJob* jobs, int njobs, cudaStream_t st);
+void launch_rng_ensemble(uint64_t base, long long m0, int count, uint64_t* out, long long stride, long long n,
+                         cudaStream_t st);
 void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t st);
 void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st);
 void launch_ensemble_finish(double* sums, int K, long long L, const double* x, double* residue, double inv,

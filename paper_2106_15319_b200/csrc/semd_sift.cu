@@ -17,393 +17,6 @@
 namespace semd {
 namespace dev {
 
-// ------------------------------------------------------------------- eval
-
-struct EvalJob {
-    int mode, L, tiles, init_kind;
-    const double* src;
-    const double* a;
-    const double* b;
-    double beta;
-    double* dst;
-    KnotView kv[2];
-};
-
-// new value at sample t from global data (reference formula; slow path only)
-__device__ double new_value_global(const EvalJob& J, int t) {
-    if (J.mode == EM_INIT) return J.init_kind == 1 ? J.a[t] + J.beta * J.b[t] : J.a[t];
-    if (J.mode == EM_DETECT) return J.src[t];
-    const double u = envelope_at_global(J.kv[0], t);
-    const double l = envelope_at_global(J.kv[1], t);
-    const double mean = 0.5 * (u + l);
-    return J.src[t] - mean;
-}
-
-struct EvalSmemStatic {
-    unsigned ticket;
-    int last;
-    unsigned scan[kEvalThreads / 32];
-    double red[2][kEvalThreads / 32];
-    double edge_first[kEvalThreads / 32];
-    double edge_last[kEvalThreads / 32];
-    double halo[2];
-    int vlo[2], vcnt[2];
-};
-
-// Segment cache for the reference's segment march (emd.cpp:79).
-struct Seg {
-    int q;
-    double x0, x1, y0, y1, m0, m1, h, rh, hh;
-};
-
-__device__ __forceinline__ void seg_load(Seg& s, const double* kX, const double* kY, const double* kM,
-                                         const double* kR, int q) {
-    s.q = q;
-    s.x0 = kX[q];
-    s.x1 = kX[q + 1];
-    s.y0 = kY[q];
-    s.y1 = kY[q + 1];
-    s.m0 = kM[q];
-    s.m1 = kM[q + 1];
-    s.h = s.x1 - s.x0;
-    s.rh = kR[q];
-    s.hh = s.h * s.h;
-}
-
-__device__ __forceinline__ int seg_search(const double* kX, int vcnt, double tt) {
-    int lo = 0, hi = vcnt - 2;  // last q with X[q] < tt (X[0] < tt holds by construction)
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (kX[mid] < tt) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
-// envelope at tt from the tile's staged knots (used for the two tile halos)
-__device__ double envelope_smem(const double* kX, const double* kY, const double* kM, const double* kR, int vcnt,
-                                double tt) {
-    Seg s;
-    seg_load(s, kX, kY, kM, kR, seg_search(kX, vcnt, tt));
-    return spline_eval_fast(s.x0, s.x1, s.y0, s.y1, s.m0, s.m1, s.h, s.rh, s.hh, tt);
-}
-
-__device__ void eval_tile(const Arena& A, int slot, int j, double* dyn, EvalSmemStatic& sh) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const Slot& S = A.slots[slot];
-    const int L = A.L;
-    EvalJob J;
-    const int state = S.state;
-    J.mode = state == ST_INIT ? EM_INIT : (state == ST_DETECT ? EM_DETECT : EM_SIFT);
-    J.L = L;
-    J.tiles = A.tiles;
-    J.init_kind = S.init_kind;
-    J.a = S.init_a;
-    J.b = S.init_b;
-    J.beta = S.beta;
-    const int xb = S.xb, cb = S.cb;
-    J.src = A.bufs + buf_off(A, slot, (J.mode == EM_SIFT && cb >= 0) ? cb : xb);
-    J.dst = nullptr;
-    if (J.mode == EM_INIT) J.dst = A.bufs + buf_off(A, slot, xb);
-    if (J.mode == EM_SIFT) J.dst = A.bufs + buf_off(A, slot, S.db);
-    const int par = S.par;
-    const double e2 = 2.0 * (double)(L - 1);
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        J.kv[s].idx = A.kidx + knot_off(A, par, s, slot);
-        J.kv[s].val = A.kval + knot_off(A, par, s, slot);
-        J.kv[s].mom = A.mom + mom_off(A, s, slot);
-        J.kv[s].n = (int)S.n[s];
-        J.kv[s].e2 = e2;
-    }
-    double* kX = dyn;
-    double* kY = kX + 2 * kKnotCapTile;
-    double* kM = kY + 2 * kKnotCapTile;
-    double* kR = kM + 2 * kKnotCapTile;
-    const int base = j * kEvalTile;
-    const int tlen = min(kEvalTile, L - base);
-
-    // 1. stage the knots touching this tile (virtual v in [toff[j], toff[j+1]+2])
-    if (J.mode == EM_SIFT) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const unsigned* to = A.toff + toff_off(A, par, s, slot);
-            const int vlo = (int)to[j];
-            const int vcnt = (int)to[j + 1] + 3 - vlo;
-            if (tid == 0) {
-                sh.vlo[s] = vlo;
-                sh.vcnt[s] = vcnt;
-            }
-            const int n = J.kv[s].n;
-            for (int q = tid; q < vcnt; q += kEvalThreads) {
-                const int v = vlo + q;
-                const int r0 = vknot_rank(n, v);
-                const double X0 = vknot_x(n, v, J.kv[s].idx[r0], e2);
-                kX[s * kKnotCapTile + q] = X0;
-                kY[s * kKnotCapTile + q] = J.kv[s].val[r0];
-                kM[s * kKnotCapTile + q] = J.kv[s].mom[v];
-                if (q + 1 < vcnt) {
-                    const int r1 = vknot_rank(n, v + 1);
-                    const double X1 = vknot_x(n, v + 1, J.kv[s].idx[r1], e2);
-                    kR[s * kKnotCapTile + q] = 1.0 / (X1 - X0);
-                }
-            }
-        }
-    }
-    __syncthreads();
-
-    // 2. this thread's 8 consecutive samples
-    const int t0 = base + tid * kSpt;
-    double cv[kSpt], nv[kSpt];
-    auto al16 = [](const double* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    const bool inside = t0 + kSpt <= L;
-    // vector (16-byte) accesses only on aligned rows; caller buffers may have odd strides
-    const bool full = inside && (J.mode == EM_INIT ? (al16(J.a) && (J.init_kind != 1 || al16(J.b))) : al16(J.src)) &&
-                      (!J.dst || al16(J.dst));
-    if (J.mode == EM_INIT) {
-        if (full) {
-#pragma unroll
-            for (int k = 0; k < kSpt; k += 2) {
-                const double2 av = *reinterpret_cast<const double2*>(J.a + t0 + k);
-                cv[k] = av.x;
-                cv[k + 1] = av.y;
-            }
-            if (J.init_kind == 1) {
-#pragma unroll
-                for (int k = 0; k < kSpt; k += 2) {
-                    const double2 bv = *reinterpret_cast<const double2*>(J.b + t0 + k);
-                    cv[k] = cv[k] + J.beta * bv.x;
-                    cv[k + 1] = cv[k + 1] + J.beta * bv.y;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < kSpt; ++k) {
-                const int t = t0 + k;
-                cv[k] = t < L ? (J.init_kind == 1 ? J.a[t] + J.beta * J.b[t] : J.a[t]) : 0.0;
-            }
-        }
-    } else {
-        if (full) {
-#pragma unroll
-            for (int k = 0; k < kSpt; k += 2) {
-                const double2 v = *reinterpret_cast<const double2*>(J.src + t0 + k);
-                cv[k] = v.x;
-                cv[k + 1] = v.y;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < kSpt; ++k) cv[k] = t0 + k < L ? J.src[t0 + k] : 0.0;
-        }
-    }
-    double num = 0.0, den = 0.0;
-    if (J.mode == EM_SIFT) {
-        Seg sg[2];
-        bool have = false;
-#pragma unroll
-        for (int k = 0; k < kSpt; ++k) {
-            const int t = t0 + k;
-            if (t < L) {
-                const double tt = (double)t;
-                double env[2];
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    const double* X = kX + s * kKnotCapTile;
-                    const int vcnt = sh.vcnt[s];
-                    if (!have) seg_load(sg[s], X, kY + s * kKnotCapTile, kM + s * kKnotCapTile, kR + s * kKnotCapTile,
-                                        seg_search(X, vcnt, tt));
-                    while (sg[s].x1 < tt && sg[s].q + 1 <= vcnt - 2)
-                        seg_load(sg[s], X, kY + s * kKnotCapTile, kM + s * kKnotCapTile, kR + s * kKnotCapTile,
-                                 sg[s].q + 1);
-                    env[s] = spline_eval_fast(sg[s].x0, sg[s].x1, sg[s].y0, sg[s].y1, sg[s].m0, sg[s].m1, sg[s].h,
-                                              sg[s].rh, sg[s].hh, tt);
-                }
-                have = true;
-                const double mean = 0.5 * (env[0] + env[1]);  // emd.cpp:144-147
-                num += mean * mean;
-                den += cv[k] * cv[k];
-                nv[k] = cv[k] - mean;
-            } else {
-                nv[k] = 0.0;
-            }
-        }
-        if (full) {
-#pragma unroll
-            for (int k = 0; k < kSpt; k += 2)
-                *reinterpret_cast<double2*>(J.dst + t0 + k) = make_double2(nv[k], nv[k + 1]);
-        } else {
-            for (int k = 0; k < kSpt; ++k)
-                if (t0 + k < L) J.dst[t0 + k] = nv[k];
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < kSpt; ++k) nv[k] = cv[k];
-        if (J.dst) {
-            if (full) {
-#pragma unroll
-                for (int k = 0; k < kSpt; k += 2)
-                    *reinterpret_cast<double2*>(J.dst + t0 + k) = make_double2(nv[k], nv[k + 1]);
-            } else {
-                for (int k = 0; k < kSpt; ++k)
-                    if (t0 + k < L) J.dst[t0 + k] = nv[k];
-            }
-        }
-    }
-    // tile halos (t = base-1, base+T) and warp-edge exchange
-    if (tid == 0 && base > 0) {
-        const int t = base - 1;
-        double v;
-        if (J.mode == EM_SIFT) {
-            const double tt = (double)t;
-            const double u = envelope_smem(kX, kY, kM, kR, sh.vcnt[0], tt);
-            const double l = envelope_smem(kX + kKnotCapTile, kY + kKnotCapTile, kM + kKnotCapTile,
-                                           kR + kKnotCapTile, sh.vcnt[1], tt);
-            v = J.src[t] - 0.5 * (u + l);
-        } else {
-            v = new_value_global(J, t);
-        }
-        sh.halo[0] = v;
-    }
-    if (tid == kEvalThreads - 1 && base + kEvalTile < L) {
-        const int t = base + kEvalTile;
-        double v;
-        if (J.mode == EM_SIFT) {
-            const double tt = (double)t;
-            const double u = envelope_smem(kX, kY, kM, kR, sh.vcnt[0], tt);
-            const double l = envelope_smem(kX + kKnotCapTile, kY + kKnotCapTile, kM + kKnotCapTile,
-                                           kR + kKnotCapTile, sh.vcnt[1], tt);
-            v = J.src[t] - 0.5 * (u + l);
-        } else {
-            v = new_value_global(J, t);
-        }
-        sh.halo[1] = v;
-    }
-    if (lane == 0) sh.edge_first[wid] = nv[0];
-    if (lane == 31) sh.edge_last[wid] = nv[kSpt - 1];
-    double left = __shfl_up_sync(0xffffffffu, nv[kSpt - 1], 1);
-    double right = __shfl_down_sync(0xffffffffu, nv[0], 1);
-    __syncthreads();
-    if (lane == 0) left = wid > 0 ? sh.edge_last[wid - 1] : sh.halo[0];
-    if (lane == 31) right = wid < kEvalThreads / 32 - 1 ? sh.edge_first[wid + 1] : sh.halo[1];
-
-    // 3. extrema of the new values (find_extrema, emd.cpp:16-33)
-    unsigned fmax = 0, fmin = 0;
-#pragma unroll
-    for (int k = 0; k < kSpt; ++k) {
-        const int t = t0 + k;
-        if (t < 1 || t > L - 2) continue;
-        const double v = nv[k];
-        const double l = k == 0 ? left : nv[k - 1];
-        const double r = k == kSpt - 1 ? right : nv[k + 1];
-        if (v != l && v != r) {
-            if (v > l && v > r) fmax |= 1u << k;
-            if (v < l && v < r) fmin |= 1u << k;
-        } else {
-            // plateau: the maximal run of samples exactly equal to v
-            double win[kSpt + 2];
-            win[0] = left;
-#pragma unroll
-            for (int q = 0; q < kSpt; ++q) win[q + 1] = nv[q];
-            win[kSpt + 1] = right;
-            auto val = [&](int u) -> double {
-                const int li = u - t0 + 1;
-                if (li >= 0 && li <= kSpt + 1 && u < L) return win[li];
-                return new_value_global(J, u);
-            };
-            int rs = t, re = t;
-            while (rs > 0 && val(rs - 1) == v) --rs;
-            while (re < L - 1 && val(re + 1) == v) ++re;
-            if (rs > 0 && re < L - 1 && t == (rs + re) / 2) {
-                const double lv = val(rs - 1), rv = val(re + 1);
-                if (v > lv && v > rv) fmax |= 1u << k;
-                if (v < lv && v < rv) fmin |= 1u << k;
-            }
-        }
-    }
-
-    // 4. tile-local ordered compaction (block scan of packed counts)
-    const unsigned packed = (unsigned)__popc(fmax) | ((unsigned)__popc(fmin) << 16);
-    unsigned incl = packed;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) sh.scan[wid] = incl;
-    if (J.mode == EM_SIFT) {
-        num = warp_sum(num);
-        den = warp_sum(den);
-        if (lane == 0) {
-            sh.red[0][wid] = num;
-            sh.red[1][wid] = den;
-        }
-    }
-    __syncthreads();
-    unsigned woff = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < kEvalThreads / 32; ++w) {
-        const unsigned c = sh.scan[w];
-        if (w < wid) woff += c;
-        total += c;
-    }
-    const unsigned excl = woff + incl - packed;
-    unsigned omax = excl & 0xFFFF, omin = excl >> 16;
-    int* si0 = A.sidx + stage_off(A, 0, slot) + (size_t)j * kTileKnots;
-    int* si1 = A.sidx + stage_off(A, 1, slot) + (size_t)j * kTileKnots;
-    double* sv0 = A.sval + stage_off(A, 0, slot) + (size_t)j * kTileKnots;
-    double* sv1 = A.sval + stage_off(A, 1, slot) + (size_t)j * kTileKnots;
-#pragma unroll
-    for (int k = 0; k < kSpt; ++k) {
-        if (fmax & (1u << k)) {
-            si0[omax] = t0 + k;
-            sv0[omax] = nv[k];
-            ++omax;
-        }
-        if (fmin & (1u << k)) {
-            si1[omin] = t0 + k;
-            sv1[omin] = nv[k];
-            ++omin;
-        }
-    }
-    if (tid == 0) {
-        A.scnt[scnt_off(A, 0, slot) + j] = total & 0xFFFF;
-        A.scnt[scnt_off(A, 1, slot) + j] = total >> 16;
-        if (J.mode == EM_SIFT) {
-            double a = 0.0, b = 0.0;
-            for (int w = 0; w < kEvalThreads / 32; ++w) {
-                a += sh.red[0][w];
-                b += sh.red[1][w];
-            }
-            A.tnum[(size_t)slot * A.tiles + j] = a;
-            A.tden[(size_t)slot * A.tiles + j] = b;
-        }
-    }
-    (void)tlen;
-    __syncthreads();
-}
-
-__global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
-    extern __shared__ double dyn[];
-    __shared__ EvalSmemStatic sh;
-    Ctrl* C = A.ctrl;
-    const unsigned nitems = (unsigned)C->n_eval * (unsigned)A.tiles;
-    while (true) {
-        if (threadIdx.x == 0) sh.ticket = atomicAdd(&C->ticket[0], 1u);
-        __syncthreads();
-        const unsigned q = sh.ticket;
-        __syncthreads();
-        if (q >= nitems) break;
-        eval_tile(A, A.eval_list[q / (unsigned)A.tiles], (int)(q % (unsigned)A.tiles), dyn, sh);
-    }
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(&C->done[0], 1u) == gridDim.x - 1) {
-            C->ticket[0] = 0;
-            C->done[0] = 0;
-        }
-    }
-}
-
 // ------------------------------------------------------------------- lists
 
 // Block-wide exclusive scan of one int per thread (blockDim.x <= 1024).
@@ -681,50 +294,41 @@ __device__ void emit_trace(const Arena& A, const Slot& S, uint64_t h) {
     }
 }
 
-__global__ void __launch_bounds__(256) k_compact(Arena A) {
-    __shared__ unsigned s_ticket;
+// One warp per (compact slot, side, tile) item, grid-stride (no tickets).
+constexpr int kCompactThreads = 128;
+__global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
     __shared__ int s_last;
-    __shared__ unsigned long long s_h[8];
     Ctrl* C = A.ctrl;
-    const unsigned nitems = (unsigned)C->n_compact * (unsigned)A.tiles;
+    const int lane = threadIdx.x & 31;
+    const int wpb = kCompactThreads / 32;
+    const unsigned nitems = (unsigned)C->n_compact * 2u * (unsigned)A.tiles;
     const bool tracing = A.trace != nullptr;
-    while (true) {
-        if (threadIdx.x == 0) s_ticket = atomicAdd(&C->ticket[1], 1u);
-        __syncthreads();
-        const unsigned q = s_ticket;
-        __syncthreads();
-        if (q >= nitems) break;
-        const int s = A.compact_list[q / (unsigned)A.tiles];
-        const int j = (int)(q % (unsigned)A.tiles);
+    for (unsigned it = blockIdx.x * wpb + (threadIdx.x >> 5); it < nitems; it += gridDim.x * wpb) {
+        const unsigned per_slot = 2u * (unsigned)A.tiles;
+        const int s = A.compact_list[it / per_slot];
+        const unsigned r = it % per_slot;
+        const int side = (int)(r / (unsigned)A.tiles);
+        const int j = (int)(r % (unsigned)A.tiles);
         const int cpar = A.slots[s].cpar;
+        const unsigned cnt = A.scnt[scnt_off(A, side, s) + j];
+        const unsigned off = A.toff[toff_off(A, cpar, side, s) + j];
+        const int* si = A.sidx + stage_off(A, side, s) + (size_t)j * kTileKnots;
+        const double* sv = A.sval + stage_off(A, side, s) + (size_t)j * kTileKnots;
+        int* gi = A.kidx + knot_off(A, cpar, side, s) + off;
+        double* gv = A.kval + knot_off(A, cpar, side, s) + off;
         uint64_t h = 0;
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-            const unsigned cnt = A.scnt[scnt_off(A, side, s) + j];
-            const unsigned off = A.toff[toff_off(A, cpar, side, s) + j];
-            const int* si = A.sidx + stage_off(A, side, s) + (size_t)j * kTileKnots;
-            const double* sv = A.sval + stage_off(A, side, s) + (size_t)j * kTileKnots;
-            int* gi = A.kidx + knot_off(A, cpar, side, s) + off;
-            double* gv = A.kval + knot_off(A, cpar, side, s) + off;
-            for (unsigned i = threadIdx.x; i < cnt; i += blockDim.x) {
-                const int t = si[i];
-                gi[i] = t;
-                gv[i] = sv[i];
-                if (tracing) h += knot_hash(side, off + i, (unsigned)t);
-            }
+        for (unsigned i = lane; i < cnt; i += 32) {
+            const int t = si[i];
+            gi[i] = t;
+            gv[i] = sv[i];
+            if (tracing) h += knot_hash(side, off + i, (unsigned)t);
         }
         if (tracing) {
             h = warp_sum(h);
-            if ((threadIdx.x & 31) == 0) s_h[threadIdx.x >> 5] = h;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                uint64_t hs = 0;
-                for (int w = 0; w < 8; ++w) hs += s_h[w];
-                A.thash[(size_t)s * A.tiles + j] = hs;
-            }
-            __syncthreads();
+            if (lane == 0) A.thash[((size_t)side * A.G + s) * A.tiles + j] = h;
         }
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         s_last = atomicAdd(&C->done[1], 1u) == gridDim.x - 1;
@@ -733,12 +337,13 @@ __global__ void __launch_bounds__(256) k_compact(Arena A) {
     if (s_last) {
         __threadfence();
         if (tracing) {
-            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-            for (int li = wid; li < C->n_compact; li += 8) {
+            const int wid = threadIdx.x >> 5;
+            for (int li = wid; li < C->n_compact; li += wpb) {
                 const int s = A.compact_list[li];
                 const Slot& S = A.slots[s];
                 uint64_t h = 0;
-                for (int j = lane; j < A.tiles; j += 32) h += A.thash[(size_t)s * A.tiles + j];
+                for (int j = lane; j < A.tiles; j += 32)
+                    h += A.thash[(size_t)s * A.tiles + j] + A.thash[((size_t)A.G + s) * A.tiles + j];
                 h = warp_sum(h);
                 if (lane == 0 && S.trace_iter >= 0) emit_trace(A, S, h);
             }
@@ -793,7 +398,7 @@ struct SolveShared {
     int moved[kSolveChains + 1];
 };
 
-__device__ void solve_small(const KnotView& kv, double* mom, double* sm) {
+__device__ void solve_small(const KnotView& kv, double4* tab, double* sm) {
     // one thread runs the reference Thomas algorithm verbatim
     const int N = kv.n + 4;
     double* X = sm;
@@ -815,12 +420,12 @@ __device__ void solve_small(const KnotView& kv, double* mom, double* sm) {
             rp[i] -= w * rp[i - 1];
         }
         double m = 0.0;
-        mom[N - 1] = 0.0;
+        tab[N - 1] = make_double4(X[N - 1], Y[N - 1], 0.0, 0.0);
         for (int i = N - 2; i >= 1; --i) {
             m = (rp[i] - (X[i + 1] - X[i]) * m) / dp[i];
-            mom[i] = m;
+            tab[i] = make_double4(X[i], Y[i], m, 1.0 / (X[i + 1] - X[i]));
         }
-        mom[0] = 0.0;
+        tab[0] = make_double4(X[0], Y[0], 0.0, 1.0 / (X[1] - X[0]));
     }
     __syncthreads();
 }
@@ -857,10 +462,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
         kv.n = (int)S.n[side];
         kv.e2 = 2.0 * (double)(A.L - 1);
         kv.mom = nullptr;
-        double* mom = A.mom + mom_off(A, side, slot);
+        double4* tab = A.ktab + tab_off(A, side, slot);
         const int N = kv.n + 4;
         if (N - 2 <= kSolveSeqMax) {
-            solve_small(kv, mom, sm);
+            solve_small(kv, tab, sm);
             continue;
         }
         const int HW = kSolveHalo, B = kSolveBlock, CH = kSolveChunk, NT = kSolveChains, W0 = kSolveWarm;
@@ -876,7 +481,27 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
         double* RP = DP + kSolveWin;
         double* M = RP + kSolveWin;
         // stage X into DP and Y into M (temporarily), then H, 1/H (into RP), RHS
-        for (int q = tid; q < wn; q += blockDim.x) vknot(kv, wa + q, DP[q], M[q]);
+        for (int q0 = 0; q0 < wn; q0 += 8 * kSolveThreads) {  // 8 independent loads in flight per thread
+            int iv[8];
+            double yv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * kSolveThreads + tid;
+                if (q < wn) {
+                    const int r = vknot_rank(kv.n, wa + q);
+                    iv[u] = kv.idx[r];
+                    yv[u] = kv.val[r];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * kSolveThreads + tid;
+                if (q < wn) {
+                    DP[q] = vknot_x(kv.n, wa + q, iv[u], kv.e2);
+                    M[q] = yv[u];
+                }
+            }
+        }
         __syncthreads();
         for (int q = tid; q < wn - 1; q += blockDim.x) {
             const double h = DP[q + 1] - DP[q];
@@ -994,10 +619,23 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
         }
         // --- outputs + cross-block records: [0,1] warm-up state at r0-1, [2,3]
         // this block's state at r1-1, [4] m at r0, [5] the m at r1 it used
-        for (int i = r0 + tid; i < r1; i += blockDim.x) mom[i] = M[i - wa];
+        // segment table rows {x, y, m, 1/h} (vknot re-reads the staged knot from L2)
+        for (int i = r0 + tid; i < r1; i += blockDim.x) {
+            double x, y;
+            vknot(kv, i, x, y);
+            tab[i] = make_double4(x, y, M[i - wa], 1.0 / H[i - wa]);  // x, y re-read (L2-resident)
+        }
         if (tid == 0) {
-            if (r0 == 1) mom[0] = 0.0;
-            if (r1 == N - 1) mom[N - 1] = 0.0;
+            if (r0 == 1) {
+                double x, y;
+                vknot(kv, 0, x, y);
+                tab[0] = make_double4(x, y, 0.0, 1.0 / H[0 - wa]);
+            }
+            if (r1 == N - 1) {
+                double x, y;
+                vknot(kv, N - 1, x, y);
+                tab[N - 1] = make_double4(x, y, 0.0, 0.0);
+            }
             rec[2] = DP[r1 - 1 - wa];
             rec[3] = RP[r1 - 1 - wa];
             rec[4] = M[r0 - wa];
@@ -1175,7 +813,6 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
 
 // --------------------------------------------------------------- launchers
 
-size_t eval_smem_bytes() { return (size_t)8 * kKnotCapTile * sizeof(double); }
 size_t solve_smem_bytes() {
     const size_t chunked = (size_t)5 * kSolveWin * sizeof(double);
     const size_t seq = (size_t)4 * (kSolveSeqMax + 4) * sizeof(double);
@@ -1183,7 +820,7 @@ size_t solve_smem_bytes() {
 }
 
 cudaError_t launch_setup() {
-    cudaError_t e = cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eval_smem_bytes());
+    cudaError_t e = eval_setup();
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem_bytes());
 }
@@ -1195,10 +832,10 @@ void count_launches(int n) { __atomic_fetch_add(&g_launches, (unsigned long long
 void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begin, cudaEvent_t eval_end) {
     k_solve<<<2 * sms, kSolveThreads, solve_smem_bytes(), st>>>(A);
     if (eval_begin) cudaEventRecord(eval_begin, st);
-    k_eval<<<2 * sms, kEvalThreads, eval_smem_bytes(), st>>>(A);
+    launch_eval(A, sms, st);
     if (eval_end) cudaEventRecord(eval_end, st);
     k_scan<<<2 * A.G, 256, 0, st>>>(A);
-    k_compact<<<2 * sms, 256, 0, st>>>(A);
+    k_compact<<<sms * 8, kCompactThreads, 0, st>>>(A);
     k_final<<<2 * sms, 256, 0, st>>>(A);
     count_launches(5);
 }

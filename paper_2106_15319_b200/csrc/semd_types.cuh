@@ -13,18 +13,19 @@
 //   kidx    i32 [2 par][2 side][G][cap]   compacted extrema indices (cap = L/2+2)
 //   kval    f64 [2][2][G][cap]            extrema values
 //   toff    u32 [2][2][G][tiles+1]        exclusive per-tile knot offsets
-//   mom     f64 [2 side][G][cap+4]        spline moments of the mirrored knot system
+//   ktab    f64x4 [2 side][G][cap+8]      segment table of the mirrored knot system {x, y, m, 1/h}
 //   tnum/tden/thash [G][tiles]            per-tile SD and trace-hash partials
 //   sums    f64 [kcap][L]                 ensemble / IMF accumulators
 #pragma once
 #include <cstdint>
+#include <vector_types.h>
 
 namespace semd {
 namespace dev {
 
-constexpr int kEvalTile = 2048;                 // samples per eval tile
-constexpr int kEvalThreads = 256;
-constexpr int kSpt = kEvalTile / kEvalThreads;  // samples per thread (consecutive)
+constexpr int kEvalTile = 128;                  // samples per eval tile (one warp)
+constexpr int kEvalThreads = 256;              // 8 independent warps per CTA
+constexpr int kSpt = kEvalTile / 32;            // samples per lane (consecutive)
 constexpr int kKnotCapTile = kEvalTile / 2 + 4; // knots of one side touching a tile
 constexpr int kTileKnots = kEvalTile / 2;       // stage capacity per tile and side
 
@@ -33,7 +34,7 @@ constexpr int kSolveChunk = 32;                          // rows per chain
 constexpr int kSolveWarm = 16;                           // per-chain warm-up rows
 constexpr int kSolveBlock = kSolveChains * kSolveChunk;  // rows per CTA
 constexpr int kSolveHalo = 64;                           // cross-block warm-up rows
-constexpr int kSolveThreads = kSolveChains + 32;         // + the back-halo chain + helpers
+constexpr int kSolveThreads = kSolveChains + 64;         // + the back-halo chain + load helpers
 constexpr int kSolveSeqMax = 96;                         // rows solved by one exact thread
 constexpr int kSolveWin = kSolveBlock + 2 * kSolveHalo + 4;  // knot window per block
 
@@ -118,7 +119,7 @@ struct Arena {
     int* kidx;
     double* kval;
     unsigned* toff;
-    double* mom;
+    double4* ktab;
     int* sidx;
     double* sval;
     unsigned* scnt;
@@ -149,8 +150,8 @@ __host__ __device__ inline size_t knot_off(const Arena& a, int par, int side, in
 __host__ __device__ inline size_t toff_off(const Arena& a, int par, int side, int slot) {
     return (((size_t)par * 2 + side) * a.G + slot) * (size_t)(a.tiles + 1);
 }
-__host__ __device__ inline size_t mom_off(const Arena& a, int side, int slot) {
-    return ((size_t)side * a.G + slot) * (size_t)(a.cap + 4);
+__host__ __device__ inline size_t tab_off(const Arena& a, int side, int slot) {
+    return ((size_t)side * a.G + slot) * (size_t)(a.cap + 8);
 }
 __host__ __device__ inline size_t stage_off(const Arena& a, int side, int slot) {
     return ((size_t)side * a.G + slot) * (size_t)a.tiles * kTileKnots;
