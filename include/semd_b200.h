@@ -79,7 +79,8 @@ typedef struct semd_stats {
     uint64_t sift_iterations;
     uint64_t steps;          /* lockstep engine steps */
     uint64_t kernel_launches;
-    uint64_t solve_hazards;  /* speculative-solve boundary mismatches (0 => bit-exact Thomas) */
+    uint64_t solve_hazards;  /* speculative-solve block boundaries that disagreed; each such envelope
+                                was re-solved by the exact sequential fallback (results stay bit-exact) */
     int32_t slots;           /* concurrent sift jobs used */
     int32_t waves;
     double eval_ms;          /* optional: device time of the sift (eval) kernel, if timing enabled */

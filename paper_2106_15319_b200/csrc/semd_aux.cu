@@ -125,8 +125,8 @@ __global__ void k_box_muller(uint64_t* draws, long long n, double stdv) {
 // squared deviations) while lane 0 of warp 0 performs the dependent additions,
 // so the cost is one fp64 add latency per sample and pass.
 constexpr int kStdChunk = 2048;
-// signals up to this length get the reference's exact sequential sums
-constexpr long long kStdExactMax = 1LL << 22;
+// (every length: beta = nstd * signal_std seeds every realization's noise, so
+// it must carry the reference's rounding; ~4.4 ns per sample, once per call)
 __global__ void __launch_bounds__(64) k_signal_std(const double* x, long long n, double* out, double scale) {
     __shared__ double buf[2][kStdChunk];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -173,61 +173,6 @@ __global__ void __launch_bounds__(64) k_signal_std(const double* x, long long n,
         __syncthreads();
     }
     if (threadIdx.x == 0) *out = scale * sqrt(acc / (double)n);
-}
-
-// signal_std for long signals (n > kStdExactMax): the same two-pass formula
-// with each pass summed by a deterministic parallel double-double (TwoSum)
-// reduction, i.e. the nearly correctly rounded sum instead of the reference's
-// sequentially rounded one (difference ~sqrt(n) ulp of the sum; documented in
-// DESIGN.md). Fixed reduction tree -> bitwise reproducible run to run.
-constexpr int kStdBlocks = 256;
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-    s = a + b;
-    const double bb = s - a;
-    e = (a - (s - bb)) + (b - bb);
-}
-__device__ __forceinline__ void dd_add(double& hi, double& lo, double v) {
-    double s, e;
-    two_sum(hi, v, s, e);
-    hi = s;
-    lo += e;
-}
-__global__ void __launch_bounds__(256) k_std_partial(const double* x, long long n, const double* mean_in, double* part) {
-    __shared__ double sh[2][256];
-    const double mean = mean_in ? *mean_in : 0.0;
-    double hi = 0.0, lo = 0.0;
-    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
-        const double v = mean_in ? (x[i] - mean) * (x[i] - mean) : x[i];
-        dd_add(hi, lo, v);
-    }
-    sh[0][threadIdx.x] = hi;
-    sh[1][threadIdx.x] = lo;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            double s, e;
-            two_sum(sh[0][threadIdx.x], sh[0][threadIdx.x + o], s, e);
-            sh[0][threadIdx.x] = s;
-            sh[1][threadIdx.x] += sh[1][threadIdx.x + o] + e;
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = sh[0][0];
-        part[2 * blockIdx.x + 1] = sh[1][0];
-    }
-}
-__global__ void k_std_final(const double* part, int nb, long long n, double* mean_out, double* out, double scale,
-                            int stage) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double hi = 0.0, lo = 0.0;
-    for (int b = 0; b < nb; ++b) {
-        dd_add(hi, lo, part[2 * b]);
-        lo += part[2 * b + 1];
-    }
-    const double s = hi + lo;
-    if (stage == 0) *mean_out = s / (double)n;
-    else *out = scale * sqrt(s / (double)n);
 }
 
 // eemd finish (emd.cpp:252-260): imfs *= 1/nr ; residue = x - sum_k imf_k (k order).
@@ -417,21 +362,7 @@ void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t s
     count_launches(1);
 }
 void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st) {
-    if (n <= kStdExactMax) {
-        k_signal_std<<<1, 64, 0, st>>>(x, n, out, scale);
-        count_launches(1);
-        return;
-    }
-    // out[1] = mean scratch, out[2..] = block partials
-    double* mean = out + 1;
-    double* part = out + 2;
-    k_std_partial<<<kStdBlocks, 256, 0, st>>>(x, n, nullptr, part);
-    count_launches(1);
-    k_std_final<<<1, 32, 0, st>>>(part, kStdBlocks, n, mean, out, scale, 0);
-    count_launches(1);
-    k_std_partial<<<kStdBlocks, 256, 0, st>>>(x, n, mean, part);
-    count_launches(1);
-    k_std_final<<<1, 32, 0, st>>>(part, kStdBlocks, n, mean, out, scale, 1);
+    k_signal_std<<<1, 64, 0, st>>>(x, n, out, scale);
     count_launches(1);
 }
 static int grid_for(long long n) {

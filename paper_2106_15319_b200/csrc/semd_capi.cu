@@ -120,7 +120,7 @@ struct semd_ctx {
     // engine arena
     Arena A{};
     int cfg_L = -1, cfg_G = -1, cfg_kcap = -1, cfg_trace = -1;
-    DBuf bufs, kidx, kval, toff, ktab, sidx, sval, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace;
+    DBuf bufs, kidx, kval, toff, tbase, ctot, cnum, cden, ktab, sidx, sval, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog;
     int* status_host = nullptr;
     int* status_host_dev = nullptr;
     std::vector<Slot> h_slots;
@@ -154,17 +154,23 @@ struct semd_ctx {
         const int cap = (int)((L / 2 + 2 + 3) / 4 * 4);  // 16-byte aligned knot rows (bulk TMA staging)
         const int rows_max = cap + 2;
         const int max_blocks = rows_max / semd::dev::kSolveBlock + 2;
-        const long long Lp = (L + 63) / 64 * 64;
+        const long long Lp = (long long)tiles * semd::dev::kEvalTile;  // whole tiles: bulk copies stay inside
         bufs.alloc((size_t)G * 3 * Lp * 8);
         kidx.alloc(((size_t)4 * G * cap + 16) * 4);
         kval.alloc(((size_t)4 * G * cap + 16) * 8);
-        toff.alloc((size_t)4 * G * (tiles + 1) * 4);
+        const size_t t4 = ((size_t)tiles + 3) & ~(size_t)3, t4p = ((size_t)tiles + 4) & ~(size_t)3;
+        const int chunks = (tiles + semd::dev::kScanChunk - 1) / semd::dev::kScanChunk;
+        toff.alloc((size_t)4 * G * t4p * 4);
+        tbase.alloc((size_t)4 * G * chunks * 4);
+        ctot.alloc((size_t)2 * G * chunks * 4);
+        cnum.alloc((size_t)G * chunks * 8);
+        cden.alloc((size_t)G * chunks * 8);
         ktab.alloc(((size_t)2 * G * (cap + 8) + 16) * 32);
         sidx.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 4);
         sval.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 8);
-        scnt.alloc((size_t)2 * G * tiles * 4);
-        tnum.alloc((size_t)G * tiles * 8);
-        tden.alloc((size_t)G * tiles * 8);
+        scnt.alloc((size_t)2 * G * t4 * 4);
+        tnum.alloc((size_t)G * t4 * 8);
+        tden.alloc((size_t)G * t4 * 8);
         thash.alloc((size_t)2 * G * tiles * 8);
         slots.alloc((size_t)G * sizeof(Slot));
         sums.alloc((size_t)kcap * L * 8);
@@ -184,6 +190,11 @@ struct semd_ctx {
         A.kidx = kidx.as<int>();
         A.kval = kval.as<double>();
         A.toff = toff.as<unsigned>();
+        A.tbase = tbase.as<unsigned>();
+        A.ctot = ctot.as<unsigned>();
+        A.cnum = cnum.as<double>();
+        A.cden = cden.as<double>();
+        A.chunks = chunks;
         A.ktab = ktab.as<double4>();
         A.sidx = sidx.as<int>();
         A.sval = sval.as<double>();
@@ -206,7 +217,12 @@ struct semd_ctx {
         A.trace = trace_cap > 0 ? trace.as<TraceRec>() : nullptr;
         A.trace_cap = trace_cap;
         A.status_host = status_host_dev;
+        hzlog.alloc((size_t)kHzCap * 8 * 4);
+        A.hzlog = hzlog.as<int>();
+        A.hzlog_cap = kHzCap;
+        A.debug = debug_flags;
         ck(cudaMemsetAsync(toff.p, 0, toff.bytes, stream), "memset toff");
+        ck(cudaMemsetAsync(tbase.p, 0, tbase.bytes, stream), "memset tbase");
         ck(cudaMemsetAsync(sb.p, 0, sb.bytes, stream), "memset sb");
         cfg_L = (int)L;
         cfg_G = G;
@@ -319,7 +335,21 @@ struct semd_ctx {
                 ck(cudaEventSynchronize(ev[(step - LAG) % R]), "step");
                 if (*(volatile int*)status_host == 0) break;
             }
-            if (step > max_steps) raise(SEMD_CUDA_ERROR, "engine did not converge within %d steps", max_steps);
+            if (step > max_steps) {
+                cudaStreamSynchronize(stream);
+                std::string d;
+                if (cudaMemcpy(h_slots.data(), A.slots, (size_t)A.G * sizeof(Slot), cudaMemcpyDeviceToHost) ==
+                    cudaSuccess) {
+                    char b[160];
+                    for (int i = 0; i < A.G && i < 8; ++i) {
+                        const Slot& S = h_slots[i];
+                        std::snprintf(b, sizeof b, " [m%d st%d k%d it%d n%u/%u par%d xb%d cb%d]", S.m, S.state, S.k,
+                                      S.iter, S.n[0], S.n[1], S.par, S.xb, S.cb);
+                        d += b;
+                    }
+                }
+                raise(SEMD_CUDA_ERROR, "engine did not converge within %d steps;%s", max_steps, d.c_str());
+            }
         }
         ck(cudaStreamSynchronize(stream), "engine run");
         if (timing) harvest(harvested, step + 1);
@@ -332,6 +362,12 @@ struct semd_ctx {
             stats.sift_iterations += (uint64_t)(S.sifted / std::max(1, A.L));
         }
         stats.solve_hazards += (uint64_t)c.hazards;
+        if (c.hz_count > 0) {
+            const int n = std::min(c.hz_count, kHzCap);
+            const size_t old = h_hz.size();
+            h_hz.resize(old + (size_t)n * 8);
+            ck(cudaMemcpy(h_hz.data() + old, A.hzlog, (size_t)n * 8 * 4, cudaMemcpyDeviceToHost), "hazard log");
+        }
         if (c.k_overflow) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", A.kcap);
         if (A.trace) {
             const int n = std::min(c.trace_count, A.trace_cap);
@@ -346,6 +382,9 @@ struct semd_ctx {
         ck(cudaMemcpyAsync(A.ctrl, &z, sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
     }
     long long trace_total = 0;
+    static constexpr int kHzCap = 4096;
+    int debug_flags = 0;
+    std::vector<int> h_hz;  // solve-hazard records since reset_stats (test hook)
 
     int max_steps_for(const semd_sift_cfg& cfg) const {
         const long long it = std::max(1, cfg.max_sift_iters) + 2;
@@ -355,6 +394,7 @@ struct semd_ctx {
     unsigned long long launches_at_reset = 0;
     void reset_stats(int slots_used) {
         stats = semd_stats{};
+        h_hz.clear();
         stats.slots = slots_used;
         launches_at_reset = semd::dev::launch_count();
     }
@@ -856,6 +896,26 @@ int semd_set_noise_override(semd_ctx* ctx, const double* noise, size_t nr, size_
         ctx->in_y.alloc(nr * n * 8);
         ck(cudaMemcpy(ctx->in_y.p, noise, nr * n * 8, cudaMemcpyHostToDevice), "noise override");
         ctx->noise_override = ctx->in_y.as<double>();
+    });
+}
+
+// Test hook: debug flags (bit 0: force the exact sequential solve repair on every multi-block envelope).
+int semd_set_debug(semd_ctx* ctx, int flags) {
+    return guard([&] {
+        need_ctx(ctx);
+        ctx->debug_flags = flags;
+        ctx->A.debug = flags;
+    });
+}
+
+// Test hook: solve-hazard records of the last call, 8 int32 each
+// {m, k, iter, side, knots, block, blocks, 1 forward / 2 back-substitution}.
+int semd_hazard_log(semd_ctx* ctx, int32_t* out, size_t cap, size_t* count) {
+    return guard([&] {
+        need_ctx(ctx);
+        const size_t n = ctx->h_hz.size() / 8;
+        if (count) *count = n;
+        if (out) std::memcpy(out, ctx->h_hz.data(), std::min(n, cap) * 8 * 4);
     });
 }
 

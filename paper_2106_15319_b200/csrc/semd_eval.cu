@@ -75,9 +75,11 @@ constexpr int kWarpRows = kEvalTile / 2 + 6;  // table rows one warp tile can to
 constexpr int kWarpSamp = kEvalTile + 8;      // staged samples [base-2, base+T+2)
 
 // One warp's staging buffer for one tile.
-struct WarpStage {
+struct alignas(16) WarpStage {
     double4 rows[2][kWarpRows];
     double samp[kWarpSamp];
+    int qmap[2][32];          // per-lane first segment (bucket map, SIFT mode)
+    unsigned long long bar;   // mbarrier: the tile's bulk copies have landed
 };
 
 // What a warp needs to know about a tile before issuing its copies.
@@ -115,7 +117,7 @@ __device__ __forceinline__ WarpMeta fetch_meta(const Arena& A, unsigned q0, unsi
     if (m.mode == EM_SIFT) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            const unsigned* to = A.toff + toff_off(A, m.par, s, m.slot);
+            const ToffView to = toff_view(A, m.par, s, m.slot);
             // tile j's extrema are those of window [base-1, base+T-1); samples [base-2, base+T)
             // need segments in [toff[j], toff[j+1]+1] (plus the right row of the last one)
             m.vlo[s] = (int)to[j];
@@ -125,36 +127,59 @@ __device__ __forceinline__ WarpMeta fetch_meta(const Arena& A, unsigned q0, unsi
     return m;
 }
 
-__device__ __forceinline__ void cp16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
-                 "l"(src)
+// Bulk (TMA-engine) copies: one lane per warp issues a tile's contiguous
+// segments -- the samples and the two envelopes' table rows -- signalling the
+// stage's mbarrier with the byte count (cp.async.bulk ... complete_tx).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
-// Issue the asynchronous copies of a tile's table rows and samples (one commit group).
+// Issue the tile's copies (lane 0). Every call completes one phase of the stage's barrier.
 __device__ __forceinline__ void issue_stage(const Arena& A, const WarpMeta& m, WarpStage& st) {
-    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x & 31) != 0) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
     if (m.valid == 1 && m.mode != EM_INIT) {
         const double* src = A.bufs + buf_off(A, m.slot, m.src_b);
-        const int e0 = m.j * kEvalTile - 2;  // samples [base-2, base+T), 16-byte aligned
-        for (int c = lane; c < kEvalTile / 2 + 1; c += 32)
-            if (e0 + 2 * c >= 0) cp16(&st.samp[2 * c], src + e0 + 2 * c);
+        const int base = m.j * kEvalTile;
+        const int e0 = base > 0 ? base - 2 : 0;  // samples [base-2, base+T) (16-byte aligned; Lp = whole tiles)
+        const unsigned sb = (unsigned)(base + kEvalTile - e0) * 8u;
+        unsigned rb[2] = {0u, 0u};
         if (m.mode == EM_SIFT) {
 #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                const double4* tab = A.ktab + tab_off(A, s, m.slot) + m.vlo[s];
-                const int cnt = m.vmax[s] + 2 - m.vlo[s];
-                for (int c = lane; c < 2 * cnt; c += 32)
-                    cp16(reinterpret_cast<double2*>(st.rows[s]) + c, reinterpret_cast<const double2*>(tab) + c);
-            }
+            for (int s = 0; s < 2; ++s) rb[s] = (unsigned)(m.vmax[s] + 2 - m.vlo[s]) * 32u;
         }
+        bar_arrive_tx(&st.bar, sb + rb[0] + rb[1]);
+        bulk_g2s(&st.samp[e0 - (base - 2)], src + e0, sb, &st.bar);
+        if (m.mode == EM_SIFT) {
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+                bulk_g2s(st.rows[s], A.ktab + tab_off(A, s, m.slot) + m.vlo[s], rb[s], &st.bar);
+        }
+    } else {
+        bar_arrive_tx(&st.bar, 0u);
     }
-    cp_commit();
 }
 
 __device__ __forceinline__ int smem_search(const double4* R, int hi, double t) {  // last q <= hi with x_q < t
@@ -193,7 +218,7 @@ __device__ __noinline__ unsigned plateau_flags(const EvalCtx& J, int t, Win6 win
 
 // One warp evaluates one 128-sample tile (kSpt = 4 consecutive samples per lane)
 // from its staged rows/samples; c2/c1 carry the new values at base-2/base-1.
-__device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, const WarpStage& st, double& c2, double& c1) {
+__device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, WarpStage& st, double& c2, double& c1) {
     const int lane = threadIdx.x & 31;
     const int slot = m.slot, j = m.j, mode = m.mode;
     const Slot& sl = A.slots[slot];
@@ -262,37 +287,52 @@ __device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, const WarpStag
 
     double num = 0.0, den = 0.0;
     if (mode == EM_SIFT) {
-        // seg(t) = last row with x < t (the reference's march, emd.cpp:79), rows cached in registers
-        double x0[2], x1[2], y0[2], y1[2], m0[2], m1[2], rh[2];
-        int q[2], qmax[2];
+        // seg(t) = last staged row q <= qmax with x_q < t (the reference's march, emd.cpp:79).
+        // Knot positions are distinct integers, so at most one row boundary lies between
+        // consecutive samples: the warp finds each lane's first segment with a bucket map
+        // (row r -> first lane whose t0 exceeds x_r; prefix max over lanes), and the lane's
+        // kSpt segments follow from kSpt-1 independent compares -- no data-dependent branches.
+        double env[2][kSpt];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const double4* R = st.rows[s];
-            qmax[s] = m.vmax[s] - m.vlo[s];
-            q[s] = smem_search(R, qmax[s], (double)t0);
-            const double4 r0 = R[q[s]], r1 = R[q[s] + 1];
-            x0[s] = r0.x; y0[s] = r0.y; m0[s] = r0.z; rh[s] = r0.w;
-            x1[s] = r1.x; y1[s] = r1.y; m1[s] = r1.z;
+            const int qmax = m.vmax[s] - m.vlo[s];
+            int* qm = st.qmap[s];
+            qm[lane] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < (kWarpRows + 31) / 32; ++i) {
+                const int r = 1 + lane + 32 * i;
+                if (r <= qmax) {
+                    const int d = (int)R[r].x - base;  // x integral; bucket = first lane with t0 > x
+                    const int b = d < 0 ? 0 : (d >> 2) + 1;
+                    if (b < 32) atomicMax(&qm[b], r);
+                }
+            }
+            __syncwarp();
+            int q0 = qm[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, q0, o);
+                if (lane >= o) q0 = max(q0, y);
+            }
+            double xa[kSpt - 1];
+#pragma unroll
+            for (int i = 1; i < kSpt; ++i) xa[i - 1] = q0 + i <= qmax ? R[q0 + i].x : 1e300;
+#pragma unroll
+            for (int k = 0; k < kSpt; ++k) {
+                const double tt = (double)(t0 + k);
+                int q = q0;
+#pragma unroll
+                for (int i = 1; i <= k; ++i) q += xa[i - 1] < tt;
+                const double4 r0 = R[q], r1 = R[q + 1];
+                const double h = r1.x - r0.x;
+                env[s][k] = spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
+            }
         }
-        double tt = (double)t0;
 #pragma unroll
         for (int k = 0; k < kSpt; ++k) {
-            double env[2];
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                if (x1[s] < tt && q[s] < qmax[s]) {  // advance (rarely more than one row)
-                    const double4* R = st.rows[s];
-                    do {
-                        ++q[s];
-                    } while (q[s] < qmax[s] && R[q[s] + 1].x < tt);
-                    const double4 r0 = R[q[s]], r1 = R[q[s] + 1];
-                    x0[s] = r0.x; y0[s] = r0.y; m0[s] = r0.z; rh[s] = r0.w;
-                    x1[s] = r1.x; y1[s] = r1.y; m1[s] = r1.z;
-                }
-                const double h = x1[s] - x0[s];
-                env[s] = spline_eval_fast(x0[s], x1[s], y0[s], y1[s], m0[s], m1[s], h, rh[s], h * h, tt);
-            }
-            const double mean = 0.5 * (env[0] + env[1]);  // emd.cpp:144-147
+            const double mean = 0.5 * (env[0][k] + env[1][k]);  // emd.cpp:144-147
             if (t0 + k < L) {
                 num += mean * mean;
                 den += cv[k] * cv[k];
@@ -300,7 +340,6 @@ __device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, const WarpStag
             } else {
                 nv[k] = 0.0;
             }
-            tt += 1.0;  // exact: integers < 2^53
         }
     } else {
 #pragma unroll
@@ -386,8 +425,8 @@ __device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, const WarpStag
         A.scnt[scnt_off(A, 0, slot) + j] = total & 0xFFFF;
         A.scnt[scnt_off(A, 1, slot) + j] = total >> 16;
         if (mode == EM_SIFT) {
-            A.tnum[(size_t)slot * A.tiles + j] = num;
-            A.tden[(size_t)slot * A.tiles + j] = den;
+            A.tnum[tsd_off(A, slot) + j] = num;
+            A.tden[tsd_off(A, slot) + j] = den;
         }
     }
 }
@@ -411,6 +450,12 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
         }
         return m;
     };
+    if ((threadIdx.x & 31) == 0) {
+        bar_init(&stage[0].bar);
+        bar_init(&stage[1].bar);
+    }
+    __syncwarp();
+    unsigned phase = 0;  // bit b: parity of stage b's next completion
     unsigned seq0 = 0;
     WarpMeta cur = meta(seq0);
     issue_stage(A, cur, stage[0]);
@@ -421,15 +466,16 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
         issue_stage(A, nxt, stage[(i + 1) & 1]);
         unsigned seq2 = seq1 + 1;
         const WarpMeta after = meta(seq2);
-        cp_wait<1>();
-        __syncwarp();
-        eval_warp_tile(A, cur, stage[i & 1], c2, c1);
-        __syncwarp();  // stage[i&1] is refilled next iteration
+        const unsigned b = i & 1;
+        bar_wait(&stage[b].bar, (phase >> b) & 1u);
+        phase ^= 1u << b;
+        eval_warp_tile(A, cur, stage[b], c2, c1);
+        __syncwarp();  // stage b is refilled next iteration
         cur = nxt;
         nxt = after;
         seq1 = seq2;
     }
-    cp_wait<0>();
+    // the last issue was for an invalid tile (arrive only): no copies are in flight
 }
 
 size_t eval_smem_bytes() { return sizeof(WarpStage) * 2 * (kEvalThreads / 32); }

@@ -112,9 +112,8 @@ __device__ void build_lists(const Arena& A, bool allow_final) {
 
 // ------------------------------------------------------------------- scan
 //
-// One CTA per (eval slot, side): exclusive prefix of the per-tile extrema
-// counts -> toff of the new knot parity; side-0 CTAs also reduce the SD sums
-// (fixed tree order). The last CTA applies extract_imf's control flow.
+// Chunked per-slot tile prefix of the new extrema (see k_scan) + SD sums in a
+// fixed reduction order; the last CTA applies extract_imf's control flow.
 
 // extract_imf's control flow (emd.cpp:131-151) for one slot after its eval
 // pass; returns 1 when this step's extrema must be compacted.
@@ -122,8 +121,8 @@ __device__ int decide_slot(const Arena& A, int s) {
     Slot& S = A.slots[s];
     const int state = S.state;
     const int np = 1 - S.par;
-    const unsigned nmax = A.toff[toff_off(A, np, 0, s) + A.tiles];
-    const unsigned nmin = A.toff[toff_off(A, np, 1, s) + A.tiles];
+    const unsigned nmax = toff_view(A, np, 0, s).cg(A.tiles);
+    const unsigned nmin = toff_view(A, np, 1, s).cg(A.tiles);
     const int tracing = A.trace != nullptr;
     int compact = 0;
     S.trace_iter = -1;
@@ -188,6 +187,32 @@ __device__ int decide_slot(const Arena& A, int s) {
 __device__ void decide_after_eval(const Arena& A) {
     Ctrl* C = A.ctrl;
     const int ne = C->n_eval;
+    // chunk bases of the new knot parity (exclusive scan of the k_scan chunk totals)
+    // and the SD sums (chunk partials in chunk order)
+    const int P = A.chunks;
+    for (int w = threadIdx.x; w < 2 * ne; w += blockDim.x) {
+        const int s = A.eval_list[w >> 1], side = w & 1;
+        Slot& S = A.slots[s];
+        const unsigned* ct = A.ctot + chunk_off(A, side, s);
+        unsigned* tb = A.tbase + tbase_off(A, 1 - S.par, side, s);
+        unsigned run = 0;
+        for (int c = 0; c < P; ++c) {  // L1-bypassing reads: written by the other CTAs
+            tb[c] = run;
+            run += __ldcg(ct + c);
+        }
+        if (side == 0 && S.state == ST_SIFT) {
+            const double* cn = A.cnum + chunk_off(A, 0, s);
+            const double* cd = A.cden + chunk_off(A, 0, s);
+            double x = 0.0, y = 0.0;
+            for (int c = 0; c < P; ++c) {
+                x += __ldcg(cn + c);
+                y += __ldcg(cd + c);
+            }
+            S.num = x;
+            S.den = y;
+        }
+    }
+    __syncthreads();
     const int per = (ne + blockDim.x - 1) / blockDim.x;
     const int l0 = min(ne, (int)threadIdx.x * per), l1 = min(ne, l0 + per);
     int flags = 0, cnt = 0;  // per <= 32 when G <= 8192
@@ -205,60 +230,98 @@ __device__ void decide_after_eval(const Arena& A) {
     build_lists(A, true);
 }
 
-__global__ void __launch_bounds__(256) k_scan(Arena A) {
-    __shared__ unsigned s_part[256];
-    __shared__ double s_red[2][8];
+// One CTA per (eval slot, side, chunk of kScanChunk tiles): chunk-local exclusive
+// prefix of the per-tile extrema counts -> toff, the chunk total -> ctot, and
+// (side 0) the chunk's SD partials. The last CTA scans the chunk totals into
+// tbase and applies extract_imf's control flow.
+__global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
+    constexpr int W = kScanThreads / 32;
+    __shared__ unsigned s_w[W];
+    __shared__ double s_red[2][W];
     __shared__ int s_last;
     Ctrl* C = A.ctrl;
-    const int tid = threadIdx.x;
-    const int li = blockIdx.x >> 1, side = blockIdx.x & 1;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int P = A.chunks;
+    const int item = blockIdx.x / P, c = blockIdx.x - item * P;
+    const int li = item >> 1, side = item & 1;
     if (li < C->n_eval) {
         const int s = A.eval_list[li];
         const Slot& S = A.slots[s];
         const int np = 1 - S.par;
         const int T = A.tiles;
-        const int per = (T + 255) / 256;
-        const int j0 = min(T, tid * per), j1 = min(T, j0 + per);
+        const int jb = c * kScanChunk, je = min(T, jb + kScanChunk);
+        const int j0 = jb + tid * kScanPer;
         const unsigned* cnt = A.scnt + scnt_off(A, side, s);
+        unsigned v[kScanPer];
         unsigned sum = 0;
-        for (int jj = j0; jj < j1; ++jj) sum += cnt[jj];
-        s_part[tid] = sum;
+#pragma unroll
+        for (int q = 0; q < kScanPer / 4; ++q) {
+            uint4 u = make_uint4(0u, 0u, 0u, 0u);
+            if (j0 + 4 * q < je) u = *reinterpret_cast<const uint4*>(cnt + j0 + 4 * q);  // rows padded to 4
+            v[4 * q] = j0 + 4 * q < je ? u.x : 0u;
+            v[4 * q + 1] = j0 + 4 * q + 1 < je ? u.y : 0u;
+            v[4 * q + 2] = j0 + 4 * q + 2 < je ? u.z : 0u;
+            v[4 * q + 3] = j0 + 4 * q + 3 < je ? u.w : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kScanPer; ++i) sum += v[i];
+        unsigned incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_w[wid] = incl;
         __syncthreads();
-        // exclusive scan of the 256 partials (Hillis-Steele in shared memory)
-        for (int o = 1; o < 256; o <<= 1) {
-            const unsigned v = tid >= o ? s_part[tid - o] : 0;
-            __syncthreads();
-            s_part[tid] += v;
-            __syncthreads();
+        unsigned run = incl - sum, tot = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const unsigned x = s_w[w];
+            if (w < wid) run += x;
+            tot += x;
         }
-        unsigned run = s_part[tid] - sum;
         unsigned* to = A.toff + toff_off(A, np, side, s);
-        for (int jj = j0; jj < j1; ++jj) {
-            to[jj] = run;
-            run += cnt[jj];
+#pragma unroll
+        for (int i = 0; i < kScanPer; ++i) {
+            if (j0 + i < je) to[j0 + i] = run;
+            run += v[i];
         }
-        if (tid == 255) to[T] = s_part[255];
+        if (tid == 0) {
+            if (c == P - 1) to[T] = tot;  // tile T (the total) belongs to the last chunk
+            A.ctot[chunk_off(A, side, s) + c] = tot;
+        }
         if (side == 0 && S.state == ST_SIFT) {  // SD sums (emd.cpp:145-146), fixed reduction order
+            const double* tn = A.tnum + tsd_off(A, s);
+            const double* td = A.tden + tsd_off(A, s);
             double a = 0.0, b = 0.0;
-            for (int jj = j0; jj < j1; ++jj) {
-                a += A.tnum[(size_t)s * T + jj];
-                b += A.tden[(size_t)s * T + jj];
+#pragma unroll
+            for (int q = 0; q < kScanPer / 2; ++q) {
+                if (j0 + 2 * q < je) {
+                    const double2 x = *reinterpret_cast<const double2*>(tn + j0 + 2 * q);
+                    const double2 y = *reinterpret_cast<const double2*>(td + j0 + 2 * q);
+                    a += x.x;
+                    b += y.x;
+                    if (j0 + 2 * q + 1 < je) {
+                        a += x.y;
+                        b += y.y;
+                    }
+                }
             }
             a = warp_sum(a);
             b = warp_sum(b);
-            if ((tid & 31) == 0) {
-                s_red[0][tid >> 5] = a;
-                s_red[1][tid >> 5] = b;
+            if (lane == 0) {
+                s_red[0][wid] = a;
+                s_red[1][wid] = b;
             }
             __syncthreads();
             if (tid == 0) {
                 double x = 0.0, y = 0.0;
-                for (int w = 0; w < 8; ++w) {
+                for (int w = 0; w < W; ++w) {
                     x += s_red[0][w];
                     y += s_red[1][w];
                 }
-                A.slots[s].num = x;
-                A.slots[s].den = y;
+                A.cnum[chunk_off(A, 0, s) + c] = x;
+                A.cden[chunk_off(A, 0, s) + c] = y;
             }
         }
     }
@@ -311,7 +374,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
         const int j = (int)(r % (unsigned)A.tiles);
         const int cpar = A.slots[s].cpar;
         const unsigned cnt = A.scnt[scnt_off(A, side, s) + j];
-        const unsigned off = A.toff[toff_off(A, cpar, side, s) + j];
+        const unsigned off = toff_view(A, cpar, side, s)[j];
         const int* si = A.sidx + stage_off(A, side, s) + (size_t)j * kTileKnots;
         const double* sv = A.sval + stage_off(A, side, s) + (size_t)j * kTileKnots;
         int* gi = A.kidx + knot_off(A, cpar, side, s) + off;
@@ -343,7 +406,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
                 const Slot& S = A.slots[s];
                 uint64_t h = 0;
                 for (int j = lane; j < A.tiles; j += 32)
-                    h += A.thash[(size_t)s * A.tiles + j] + A.thash[((size_t)A.G + s) * A.tiles + j];
+                    h += __ldcg(A.thash + (size_t)s * A.tiles + j) + __ldcg(A.thash + ((size_t)A.G + s) * A.tiles + j);
                 h = warp_sum(h);
                 if (lane == 0 && S.trace_iter >= 0) emit_trace(A, S, h);
             }
@@ -428,6 +491,49 @@ __device__ void solve_small(const KnotView& kv, double4* tab, double* sm) {
         tab[0] = make_double4(X[0], Y[0], 0.0, 1.0 / (X[1] - X[0]));
     }
     __syncthreads();
+}
+
+// Exact fallback for an envelope whose speculative block boundaries disagreed:
+// the reference's sequential Thomas algorithm (emd.cpp:57-73, IEEE divisions)
+// run by one thread, using the segment-table rows as forward-sweep scratch.
+__device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) {
+    const int N = kv.n + 4;
+    double xp, yp, xc, yc;
+    vknot(kv, 0, xp, yp);
+    vknot(kv, 1, xc, yc);
+    double d = 0.0, r = 0.0;
+    for (int i = 1; i + 1 < N; ++i) {
+        double xn, yn;
+        vknot(kv, i + 1, xn, yn);
+        const double h0 = xc - xp, h1 = xn - xc;
+        const double rhs = 6.0 * ((yn - yc) / h1 - (yc - yp) / h0);  // emd.cpp:62
+        if (i == 1) {
+            d = 2.0 * (h0 + h1);
+            r = rhs;
+        } else {  // emd.cpp:64-69
+            const double w = h0 / d;
+            d = 2.0 * (h0 + h1) - w * h0;
+            r = rhs - w * r;
+        }
+        tab[i] = make_double4(xc, yc, d, r);
+        xp = xc;
+        yp = yc;
+        xc = xn;
+        yc = yn;
+    }
+    double xn, yn;
+    vknot(kv, N - 1, xn, yn);
+    tab[N - 1] = make_double4(xn, yn, 0.0, 0.0);
+    double m = 0.0;
+    for (int i = N - 2; i >= 1; --i) {  // emd.cpp:70-73
+        const double4 t = tab[i];
+        m = (t.w - (xn - t.x) * m) / t.z;
+        tab[i] = make_double4(t.x, t.y, m, 1.0 / (xn - t.x));
+        xn = t.x;
+    }
+    double x0, y0;
+    vknot(kv, 0, x0, y0);
+    tab[0] = make_double4(x0, y0, 0.0, 1.0 / (xn - x0));
 }
 
 __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
@@ -660,11 +766,35 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
             for (int bb = 1; bb < nb; ++bb) {
                 const double* p = base + (size_t)(bb - 1) * 6;
                 const double* q = base + (size_t)bb * 6;
-                if (q[0] != p[2] || q[1] != p[3] || p[5] != q[4]) ++bad;
+                if (__ldcg(q) != __ldcg(p + 2) || __ldcg(q + 1) != __ldcg(p + 3) || __ldcg(p + 5) != __ldcg(q + 4)) {
+                    ++bad;
+                    const int pos = atomicAdd(&C->hz_count, 1);
+                    if (A.hzlog && pos < A.hzlog_cap) {
+                        const Slot& S = A.slots[slot];
+                        int* r = A.hzlog + (size_t)pos * 8;
+                        r[0] = S.m;
+                        r[1] = S.k;
+                        r[2] = S.iter;
+                        r[3] = side;
+                        r[4] = (int)S.n[side];
+                        r[5] = bb;
+                        r[6] = nb;
+                        r[7] = (__ldcg(q) != __ldcg(p + 2) || __ldcg(q + 1) != __ldcg(p + 3)) ? 1 : 2;  // 1 fwd, 2 back
+                    }
+                }
             }
-            if (bad) {
+            if (A.debug & 1) bad += nb > 1;
+            if (bad) {  // repair: the whole envelope again, sequentially and exactly
                 atomicAdd(&A.slots[slot].hazards, bad);
                 atomicAdd(&C->hazards, bad);
+                const Slot& S = A.slots[slot];
+                KnotView kv;
+                kv.idx = A.kidx + knot_off(A, S.par, side, slot);
+                kv.val = A.kval + knot_off(A, S.par, side, slot);
+                kv.n = (int)S.n[side];
+                kv.e2 = 2.0 * (double)(A.L - 1);
+                kv.mom = nullptr;
+                solve_sequential(kv, A.ktab + tab_off(A, side, slot));
             }
         }
         if (tid == 0) {
@@ -703,6 +833,7 @@ __device__ void decide_after_final(const Arena& A) {
         S.k += 1;
         S.iter = 0;
         if (S.kmax > 0 && S.k >= S.kmax) S.state = ST_DONE;
+        else if (S.write_imf && S.k0 + S.k > A.kcap) S.state = ST_DONE;  // overflowed (counted): host grows kcap
         else S.state = ST_DETECT;
     }
     __syncthreads();
@@ -834,7 +965,7 @@ void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begi
     if (eval_begin) cudaEventRecord(eval_begin, st);
     launch_eval(A, sms, st);
     if (eval_end) cudaEventRecord(eval_end, st);
-    k_scan<<<2 * A.G, 256, 0, st>>>(A);
+    k_scan<<<2 * A.G * A.chunks, kScanThreads, 0, st>>>(A);
     k_compact<<<sms * 8, kCompactThreads, 0, st>>>(A);
     k_final<<<2 * sms, 256, 0, st>>>(A);
     count_launches(5);

@@ -12,7 +12,9 @@
 //   scnt    u32 [2 side][G][tiles]        extrema per tile
 //   kidx    i32 [2 par][2 side][G][cap]   compacted extrema indices (cap = L/2+2)
 //   kval    f64 [2][2][G][cap]            extrema values
-//   toff    u32 [2][2][G][tiles+1]        exclusive per-tile knot offsets
+//   toff    u32 [2][2][G][tiles+1]        per-tile knot offsets, local to a scan chunk
+//   tbase   u32 [2][2][G][chunks]         knot offset of each scan chunk (toff_at adds it)
+//   ctot/cnum/cden [2 side][G][chunks]    per-chunk extrema totals and SD partials
 //   ktab    f64x4 [2 side][G][cap+8]      segment table of the mirrored knot system {x, y, m, 1/h}
 //   tnum/tden/thash [G][tiles]            per-tile SD and trace-hash partials
 //   sums    f64 [kcap][L]                 ensemble / IMF accumulators
@@ -39,6 +41,11 @@ constexpr int kSolveSeqMax = 96;                         // rows solved by one e
 constexpr int kSolveWin = kSolveBlock + 2 * kSolveHalo + 4;  // knot window per block
 
 constexpr int kFinalTile = 1024;
+
+constexpr int kScanShift = 12;
+constexpr int kScanChunk = 1 << kScanShift;  // tiles per k_scan CTA
+constexpr int kScanThreads = 256;
+constexpr int kScanPer = kScanChunk / kScanThreads;
 
 enum State : int {
     ST_FREE = 0,
@@ -106,12 +113,13 @@ struct Ctrl {
     int hazards;
     int k_overflow;
     int step;
-    int pad[6];
+    int hz_count;  // hazard log records produced
+    int pad[5];
 };
 
 struct Arena {
     int L, G, tiles, cap, kcap;
-    long long Lp;  // padded slot-buffer stride (16-byte aligned rows)
+    long long Lp;  // slot-buffer stride = tiles * kEvalTile (16-byte aligned; whole tiles readable)
     double sd_threshold;
     int max_sift_iters;
     int trace_cap;
@@ -119,6 +127,11 @@ struct Arena {
     int* kidx;
     double* kval;
     unsigned* toff;
+    unsigned* tbase;
+    unsigned* ctot;
+    double* cnum;
+    double* cden;
+    int chunks;  // scan chunks per (slot, side): ceil(tiles / kScanChunk)
     double4* ktab;
     int* sidx;
     double* sval;
@@ -138,6 +151,9 @@ struct Arena {
     double* sb;       // [2][G][max_blocks][6] solve block boundary values
     int max_blocks;
     TraceRec* trace;
+    int* hzlog;       // [hzlog_cap][8] solve-hazard records {m, k, iter, side, n, block, blocks, 0}
+    int hzlog_cap;
+    int debug;        // test hook bit 0: treat every solve block boundary as a hazard (exercise the repair)
     int* status_host; // mapped pinned: [0] active slots after this step, [1] step counter
 };
 
@@ -147,8 +163,36 @@ __host__ __device__ inline size_t buf_off(const Arena& a, int slot, int b) {
 __host__ __device__ inline size_t knot_off(const Arena& a, int par, int side, int slot) {
     return (((size_t)par * 2 + side) * a.G + slot) * (size_t)a.cap;
 }
+// per-tile rows are padded to a multiple of 4 entries (16-byte aligned vector access in k_scan)
+__host__ __device__ inline size_t tiles4(const Arena& a) { return ((size_t)a.tiles + 3) & ~(size_t)3; }
 __host__ __device__ inline size_t toff_off(const Arena& a, int par, int side, int slot) {
-    return (((size_t)par * 2 + side) * a.G + slot) * (size_t)(a.tiles + 1);
+    return (((size_t)par * 2 + side) * a.G + slot) * (((size_t)a.tiles + 4) & ~(size_t)3);
+}
+__host__ __device__ inline size_t tsd_off(const Arena& a, int slot) { return (size_t)slot * tiles4(a); }
+__host__ __device__ inline size_t tbase_off(const Arena& a, int par, int side, int slot) {
+    return (((size_t)par * 2 + side) * a.G + slot) * (size_t)a.chunks;
+}
+__host__ __device__ inline size_t chunk_off(const Arena& a, int side, int slot) {
+    return ((size_t)side * a.G + slot) * (size_t)a.chunks;
+}
+// Knot offset of tile j (0 <= j <= tiles) of one (parity, side, slot): chunk-local
+// prefix + chunk base. Tile `tiles` (the total) belongs to the last chunk.
+struct ToffView {
+    const unsigned* to;
+    const unsigned* tb;
+    int last;  // chunks - 1
+    __device__ __forceinline__ unsigned operator[](int j) const {
+        const int c = (j >> kScanShift) < last ? (j >> kScanShift) : last;
+        return to[j] + tb[c];
+    }
+    // L1-bypassing read (last-CTA epilogues read values other CTAs of the same kernel wrote)
+    __device__ __forceinline__ unsigned cg(int j) const {
+        const int c = (j >> kScanShift) < last ? (j >> kScanShift) : last;
+        return __ldcg(to + j) + __ldcg(tb + c);
+    }
+};
+__device__ __forceinline__ ToffView toff_view(const Arena& a, int par, int side, int slot) {
+    return ToffView{a.toff + toff_off(a, par, side, slot), a.tbase + tbase_off(a, par, side, slot), a.chunks - 1};
 }
 __host__ __device__ inline size_t tab_off(const Arena& a, int side, int slot) {
     return ((size_t)side * a.G + slot) * (size_t)(a.cap + 8);
@@ -157,7 +201,7 @@ __host__ __device__ inline size_t stage_off(const Arena& a, int side, int slot) 
     return ((size_t)side * a.G + slot) * (size_t)a.tiles * kTileKnots;
 }
 __host__ __device__ inline size_t scnt_off(const Arena& a, int side, int slot) {
-    return ((size_t)side * a.G + slot) * (size_t)a.tiles;
+    return ((size_t)side * a.G + slot) * tiles4(a);
 }
 
 }  // namespace dev

@@ -55,7 +55,7 @@ def test_white_noise(se, oracle, golden):
 
 
 def test_signal_std_bit_exact(se, oracle):
-    for n in (1, 5, 6250, 100003, 2_000_001):
+    for n in (1, 5, 6250, 100003, 2_000_001, 5_000_011):
         x = np.random.default_rng(n).standard_normal(n) * 3 + 1
         assert se.signal_std(x) == oracle.signal_std(x)
 
@@ -148,6 +148,22 @@ def test_emd_bit_exact_lengths(se, oracle, n):
     assert d["sift_counts"].tolist() == o[2].tolist()
     assert np.array_equal(sort_trace(d["trace"]), sort_trace(o[3]))
     assert hazards(se) == 0
+
+
+def test_solve_repair_path_bit_exact(se, oracle):
+    """Force the speculative-solve repair (exact sequential Thomas) on every multi-block envelope."""
+    ctx = se.context()
+    x = rng_signal(77, 120_000) + 0.001 * np.arange(120_000)
+    ctx.lib.semd_set_debug(ctx.ptr, 1)
+    try:
+        d = se.decompose_full(x, "emd", trace_cap=200000)
+        st = ctx.stats()
+    finally:
+        ctx.lib.semd_set_debug(ctx.ptr, 0)
+    o = oracle.emd(x, trace_cap=200000)
+    assert st["solve_hazards"] > 0  # the repair ran
+    assert np.array_equal(d["imfs"], o[0]) and np.array_equal(d["residue"], o[1])
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(o[3]))
 
 
 def test_emd_edge_cases(se, oracle):
@@ -357,6 +373,50 @@ def test_c5_realizations(se, oracle):
     assert np.array_equal(sort_trace(g["trace"]), sort_trace(o[3]))
     for k in range(o[0].shape[0]):
         assert rel_l2(g["imfs"][k], o[0][k]) <= REL_L2
+
+
+def test_unbounded_imf_loop(se, oracle):
+    """The reference's IMF loop (emd.cpp:160-169) is unbounded when max_imfs == 0; on a near-constant
+    signal with ulp-level wiggles every residue keeps extrema and it never terminates. With a cap the
+    engine matches the oracle bit-for-bit; without one it fails with a capacity error (after growing
+    its IMF store) instead of hanging."""
+    x = 1.0 + np.spacing(1.0) * np.random.default_rng(0).integers(0, 3, 500)
+    d = se.decompose_full(x, "emd", max_imfs=40, trace_cap=100000)
+    o = oracle.emd(x, imfs=40, trace_cap=100000)
+    assert d["imfs"].shape[0] == o[0].shape[0] == 40
+    assert np.array_equal(d["imfs"], o[0]) and np.array_equal(d["residue"], o[1])
+    assert d["sift_counts"].tolist() == o[2].tolist()
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(o[3]))
+    with pytest.raises(Exception, match="IMF capacity"):
+        se.decompose(x)
+    with pytest.raises(Exception, match="IMF capacity"):
+        se.decompose(x, "eemd", nr=3)
+
+
+def test_c5_realization_793(se, oracle):
+    """C5 realization 793 with the device noise stream ran away when beta came from a parallel
+    (non-sequential) std; with the reference's sequential std it ends at K=16 like its neighbours."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2106_15319_b200 import _native as N
+    from paper_2106_15319_b200 import workloads as W
+    s = se.concatenate(W.sine_variates(), 64)
+    assert se.signal_std(s) == oracle.signal_std(s)
+    ctx = se.context()
+    sd = torch.from_numpy(s).cuda()
+    sums = torch.zeros((32, s.size), dtype=torch.float64, device="cuda")
+    k = C.c_size_t()
+    ctx.check(ctx.lib.semd_eemd_partial_device(ctx.ptr, C.c_void_p(sd.data_ptr()), s.size,
+                                               C.byref(N.SiftCfg(0.2, 300, 0)), C.byref(N.EnsCfg(0.2, 1000, 0, 0)),
+                                               793, 794, C.c_void_p(sums.data_ptr()), 32, C.byref(k)))
+    assert k.value == 16
+    w = se.white_noise(s.size, oracle.derive_seed(0, 793))
+    o = oracle.emd(s + 0.2 * oracle.signal_std(s) * w)
+    assert o[0].shape[0] == 16
+    for i in range(16):
+        assert rel_l2(sums[i].cpu().numpy(), o[0][i]) <= REL_L2
 
 
 def test_cpp_mirror_runs(se):
