@@ -5,13 +5,14 @@
 //   SD partials sum(mean^2), sum(cur^2)  (emd.cpp:145-146)
 //   extrema of `new` + tile-local ordered lists for the next sift (emd.cpp:10-35)
 //
-// The envelopes are read from the segment table k_solve writes for every
-// mirrored knot v: {x_v, y_v, m_v, 1/(x_{v+1}-x_v)}. A thread owns kSpt
-// consecutive samples: one bounded binary search finds its first segment in
-// the tile's knot range (toff), the reference's march advances it, and the
-// arithmetic of the kSpt samples and two envelopes is branch-free and
-// independent (ILP). No shared-memory staging: the table rows a tile needs
-// are contiguous and L1/L2-resident, so many small CTAs per SM hide latency.
+// Work unit: a warp owns a strip of kStripTiles consecutive tiles of one slot.
+// Slot constants (buffers, table, knot offsets of the 17 tile boundaries) are
+// set up once per strip, lane-parallel; the new values at the tile boundary
+// are carried in registers. Each tile's inputs -- its samples and the two
+// envelopes' segment-table rows {x, y, m, 1/h} written by k_solve -- are
+// contiguous in HBM and arrive by bulk (TMA-engine) copies issued by one lane,
+// double-buffered per warp behind an mbarrier, so tile i+1 streams in while
+// tile i is computed.
 //
 // Arithmetic contract: -fmad=false; spline_eval_fast is the reference
 // expression bit-for-bit (div_rn = correctly rounded division, semd_device.cuh).
@@ -26,6 +27,10 @@
 namespace semd {
 namespace dev {
 
+// ------------------------------------------------------- global recomputation
+// (rare paths: the two values before a strip in INIT mode, plateau runs that
+// leave the lane's window)
+
 struct EvalCtx {
     int mode, L, init_kind;
     const double* src;
@@ -35,7 +40,26 @@ struct EvalCtx {
     TabView tv[2];
 };
 
-// new value at sample t from global data (reference formula; halos and plateau slow path)
+__device__ EvalCtx make_ctx(const Arena& A, int slot, int mode) {
+    const Slot& sl = A.slots[slot];
+    EvalCtx J;
+    J.mode = mode;
+    J.L = A.L;
+    J.init_kind = sl.init_kind;
+    J.a = sl.init_a;
+    J.b = sl.init_b;
+    J.beta = sl.beta;
+    J.src = A.bufs + buf_off(A, slot, (mode == EM_SIFT && sl.cb >= 0) ? sl.cb : sl.xb);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        J.tv[s].tab = A.ktab + tab_off(A, s, slot);
+        J.tv[s].idx = A.kidx + knot_off(A, sl.par, s, slot);
+        J.tv[s].n = (int)sl.n[s];
+    }
+    return J;
+}
+
+// new value at sample t from global data (reference formula)
 __device__ double new_value_global(const EvalCtx& J, int t) {
     if (J.mode == EM_INIT) return J.init_kind == 1 ? J.a[t] + J.beta * J.b[t] : J.a[t];
     if (J.mode == EM_DETECT) return J.src[t];
@@ -45,91 +69,50 @@ __device__ double new_value_global(const EvalCtx& J, int t) {
     return J.src[t] - mean;
 }
 
-constexpr int kTabRows = kEvalTile / 2 + 4;  // table rows a tile can touch per side
-
-__device__ __forceinline__ double4 ld_row(const double4* p) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    return make_double4(a.x, a.y, b.x, b.y);
+__device__ __noinline__ double init_value(const Arena& A, int slot, int t) {
+    return new_value_global(make_ctx(A, slot, EM_INIT), t);
 }
 
-// last table row q in [lo, hi] with x_q < t (x_lo < t holds for the tile's range)
-__device__ __forceinline__ int tab_search(const double4* tab, int lo, int hi, double t) {
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(&tab[mid].x) < t) lo = mid;
-        else hi = mid - 1;
+// Extrema flags of one lane's detection sample t given the window values t0-2..t0+3
+// (find_extrema, emd.cpp:16-33): the maximal run of samples exactly equal to v.
+struct Win6 {
+    double w[kSpt + 2];
+};
+__device__ __noinline__ unsigned plateau_flags(const Arena& A, int slot, int mode, int t, Win6 win, int t0, double v,
+                                               int& ismin) {
+    const EvalCtx J = make_ctx(A, slot, mode);
+    auto val = [&](int u) -> double {
+        const int li = u - (t0 - 2);
+        if (li >= 0 && li < kSpt + 2 && u < J.L) return win.w[li];
+        return new_value_global(J, u);
+    };
+    const int L = J.L;
+    int rs = t, re = t;
+    while (rs > 0 && val(rs - 1) == v) --rs;
+    while (re < L - 1 && val(re + 1) == v) ++re;
+    ismin = 0;
+    if (rs > 0 && re < L - 1 && t == (rs + re) / 2) {
+        const double lv = val(rs - 1), rv = val(re + 1);
+        ismin = v < lv && v < rv;
+        return v > lv && v > rv;
     }
-    return lo;
+    return 0;
 }
 
-// Envelope value at t whose segment is known to lie in rows [lo, hi] of the table.
-__device__ __forceinline__ double env_in(const double4* tab, int lo, int hi, double tt) {
-    const int q = tab_search(tab, lo, hi, tt);
-    const double4 r0 = ld_row(tab + q), r1 = ld_row(tab + q + 1);
-    const double h = r1.x - r0.x;
-    return spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
-}
+// ------------------------------------------------------------- staging
 
-constexpr int kWarpRows = kEvalTile / 2 + 6;  // table rows one warp tile can touch per side
-constexpr int kWarpSamp = kEvalTile + 8;      // staged samples [base-2, base+T+2)
+constexpr int kWarpRows = kEvalTile / 2 + 6;  // table rows one tile can touch per side
+constexpr int kWarpSamp = kEvalTile + 8;      // staged samples [base-2, base+T)
 
-// One warp's staging buffer for one tile.
 struct alignas(16) WarpStage {
     double4 rows[2][kWarpRows];
     double samp[kWarpSamp];
-    int qmap[2][32];          // per-lane first segment (bucket map, SIFT mode)
+    int2 qmap[32];            // per-lane first segment of each side (bucket map, SIFT mode)
     unsigned long long bar;   // mbarrier: the tile's bulk copies have landed
-};
-
-// What a warp needs to know about a tile before issuing its copies.
-struct WarpMeta {
-    int valid, slot, j, mode, src_b, par, fresh;  // fresh: first tile of a strip (no carried values)
-    int vlo[2], vmax[2];
 };
 
 constexpr int kStripTiles = 16;  // consecutive tiles one warp walks, carrying boundary values
 
-// Tile number `seq` of this warp's sequence (strips q0, q0+stride, ...; 16 tiles each).
-__device__ __forceinline__ WarpMeta fetch_meta(const Arena& A, unsigned q0, unsigned stride, unsigned seq,
-                                               unsigned nstrips_total) {
-    WarpMeta m;
-    const unsigned strips = ((unsigned)A.tiles + kStripTiles - 1) / kStripTiles;
-    const unsigned k = seq / kStripTiles, within = seq % kStripTiles;
-    const unsigned item = q0 + k * stride;
-    m.valid = 0;
-    if (item >= nstrips_total) return m;
-    const unsigned strip = item % strips;
-    const int j = (int)(strip * kStripTiles + within);
-    if (j >= A.tiles) {  // short last strip: skip to the next strip of this warp
-        m.valid = 2;
-        return m;
-    }
-    m.valid = 1;
-    m.slot = A.eval_list[item / strips];
-    m.j = j;
-    m.fresh = within == 0;
-    const Slot& sl = A.slots[m.slot];
-    const int state = sl.state;
-    m.mode = state == ST_INIT ? EM_INIT : (state == ST_DETECT ? EM_DETECT : EM_SIFT);
-    m.src_b = (m.mode == EM_SIFT && sl.cb >= 0) ? sl.cb : sl.xb;
-    m.par = sl.par;
-    if (m.mode == EM_SIFT) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const ToffView to = toff_view(A, m.par, s, m.slot);
-            // tile j's extrema are those of window [base-1, base+T-1); samples [base-2, base+T)
-            // need segments in [toff[j], toff[j+1]+1] (plus the right row of the last one)
-            m.vlo[s] = (int)to[j];
-            m.vmax[s] = (int)to[j + 1] + 1;
-        }
-    }
-    return m;
-}
-
-// Bulk (TMA-engine) copies: one lane per warp issues a tile's contiguous
-// segments -- the samples and the two envelopes' table rows -- signalling the
-// stage's mbarrier with the byte count (cp.async.bulk ... complete_tx).
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(unsigned long long* bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
@@ -156,26 +139,64 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parit
         : "memory");
 }
 
-// Issue the tile's copies (lane 0). Every call completes one phase of the stage's barrier.
-__device__ __forceinline__ void issue_stage(const Arena& A, const WarpMeta& m, WarpStage& st) {
+// Per-strip constants of one warp.
+struct Strip {
+    int slot, j0, nt, mode;
+    const double* src;     // the samples this pass reads (SIFT, DETECT)
+    double* dst;           // where new values go (INIT: X, SIFT: the candidate; DETECT: none)
+    const double4* tab0;   // side-0 segment table (side 1 at + tab_side)
+    size_t stg;            // stage_off(side 0) + j0 * kTileKnots
+    int to[2];             // lane l <= nt: knot offset (toff) of tile j0 + l, per side (SIFT)
+};
+
+__device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsigned strips) {
+    const int lane = threadIdx.x & 31;
+    Strip S;
+    const unsigned sx = item % strips;
+    S.slot = A.eval_list[item / strips];
+    S.j0 = (int)sx * kStripTiles;
+    S.nt = min(kStripTiles, A.tiles - S.j0);
+    const Slot& sl = A.slots[S.slot];
+    const int state = sl.state;
+    S.mode = state == ST_INIT ? EM_INIT : (state == ST_DETECT ? EM_DETECT : EM_SIFT);
+    const int cb = sl.cb, xb = sl.xb;
+    S.src = A.bufs + buf_off(A, S.slot, (S.mode == EM_SIFT && cb >= 0) ? cb : xb);
+    S.dst = S.mode == EM_INIT ? A.bufs + buf_off(A, S.slot, xb)
+                              : (S.mode == EM_SIFT ? A.bufs + buf_off(A, S.slot, sl.db) : nullptr);
+    S.tab0 = A.ktab + tab_off(A, 0, S.slot);
+    S.stg = stage_off(A, 0, S.slot) + (size_t)S.j0 * kTileKnots;
+    S.to[0] = S.to[1] = 0;
+    if (S.mode == EM_SIFT) {
+        const int j = S.j0 + min(lane, S.nt);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) S.to[s] = (int)toff_view(A, sl.par, s, S.slot)[j];
+    }
+    return S;
+}
+
+// Issue tile i's copies (lane 0 arms the barrier; every call completes one phase).
+// Tile j's extrema are those of window [base-1, base+T-1); samples [base-2, base+T)
+// need table rows [toff[j], toff[j+1]+2].
+__device__ __forceinline__ void issue_tile(const Arena& A, const Strip& S, int i, WarpStage& st) {
+    int lo[2], hi[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        lo[s] = __shfl_sync(0xffffffffu, S.to[s], i);
+        hi[s] = __shfl_sync(0xffffffffu, S.to[s], i + 1);
+    }
     if ((threadIdx.x & 31) != 0) return;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
-    if (m.valid == 1 && m.mode != EM_INIT) {
-        const double* src = A.bufs + buf_off(A, m.slot, m.src_b);
-        const int base = m.j * kEvalTile;
-        const int e0 = base > 0 ? base - 2 : 0;  // samples [base-2, base+T) (16-byte aligned; Lp = whole tiles)
+    if (S.mode != EM_INIT) {
+        const int base = (S.j0 + i) * kEvalTile;
+        const int e0 = base > 0 ? base - 2 : 0;  // 16-byte aligned; Lp = whole tiles
         const unsigned sb = (unsigned)(base + kEvalTile - e0) * 8u;
-        unsigned rb[2] = {0u, 0u};
-        if (m.mode == EM_SIFT) {
-#pragma unroll
-            for (int s = 0; s < 2; ++s) rb[s] = (unsigned)(m.vmax[s] + 2 - m.vlo[s]) * 32u;
-        }
-        bar_arrive_tx(&st.bar, sb + rb[0] + rb[1]);
-        bulk_g2s(&st.samp[e0 - (base - 2)], src + e0, sb, &st.bar);
-        if (m.mode == EM_SIFT) {
-#pragma unroll
-            for (int s = 0; s < 2; ++s)
-                bulk_g2s(st.rows[s], A.ktab + tab_off(A, s, m.slot) + m.vlo[s], rb[s], &st.bar);
+        const unsigned r0 = S.mode == EM_SIFT ? (unsigned)(hi[0] + 3 - lo[0]) * 32u : 0u;
+        const unsigned r1 = S.mode == EM_SIFT ? (unsigned)(hi[1] + 3 - lo[1]) * 32u : 0u;
+        bar_arrive_tx(&st.bar, sb + r0 + r1);
+        bulk_g2s(&st.samp[e0 - (base - 2)], S.src + e0, sb, &st.bar);
+        if (S.mode == EM_SIFT) {
+            bulk_g2s(st.rows[0], S.tab0 + lo[0], r0, &st.bar);
+            bulk_g2s(st.rows[1], S.tab0 + (size_t)A.G * (A.cap + 8) + lo[1], r1, &st.bar);
         }
     } else {
         bar_arrive_tx(&st.bar, 0u);
@@ -192,63 +213,29 @@ __device__ __forceinline__ int smem_search(const double4* R, int hi, double t) {
     return lo;
 }
 
-// Extrema flags of one lane's detection window t0-1..t0+2 given v[-2..3] (find_extrema, emd.cpp:16-33).
-struct Win6 {
-    double w[kSpt + 2];
-};
-__device__ __noinline__ unsigned plateau_flags(const EvalCtx& J, int t, Win6 win, int t0, double v, int& ismin) {
-    // the maximal run of samples exactly equal to v; win holds values t0-2 .. t0+3
-    auto val = [&](int u) -> double {
-        const int li = u - (t0 - 2);
-        if (li >= 0 && li < kSpt + 2 && u < J.L) return win.w[li];
-        return new_value_global(J, u);
-    };
-    const int L = J.L;
-    int rs = t, re = t;
-    while (rs > 0 && val(rs - 1) == v) --rs;
-    while (re < L - 1 && val(re + 1) == v) ++re;
-    ismin = 0;
-    if (rs > 0 && re < L - 1 && t == (rs + re) / 2) {
-        const double lv = val(rs - 1), rv = val(re + 1);
-        ismin = v < lv && v < rv;
-        return v > lv && v > rv;
-    }
-    return 0;
-}
-
-// One warp evaluates one 128-sample tile (kSpt = 4 consecutive samples per lane)
-// from its staged rows/samples; c2/c1 carry the new values at base-2/base-1.
-__device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, WarpStage& st, double& c2, double& c1) {
+// ---------------------------------------------------------------- one tile
+// kSpt = 4 consecutive samples per lane; c2/c1 carry the new values at base-2/base-1.
+__device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i, WarpStage& st, double& c2,
+                                          double& c1, double& snum, double& sden) {
     const int lane = threadIdx.x & 31;
-    const int slot = m.slot, j = m.j, mode = m.mode;
-    const Slot& sl = A.slots[slot];
+    const int mode = S.mode;
     const int L = A.L;
-    EvalCtx J;
-    J.mode = mode;
-    J.L = L;
-    J.init_kind = sl.init_kind;
-    J.a = sl.init_a;
-    J.b = sl.init_b;
-    J.beta = sl.beta;
-    J.src = A.bufs + buf_off(A, slot, m.src_b);
-    double* dst = mode == EM_INIT ? A.bufs + buf_off(A, slot, sl.xb)
-                                  : (mode == EM_SIFT ? A.bufs + buf_off(A, slot, sl.db) : nullptr);
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        J.tv[s].tab = A.ktab + tab_off(A, s, slot);
-        J.tv[s].idx = A.kidx + knot_off(A, m.par, s, slot);
-        J.tv[s].n = (int)sl.n[s];
-    }
+    const int j = S.j0 + i;
     const int base = j * kEvalTile;
     const int t0 = base + lane * kSpt;
-    const bool inside = t0 + kSpt <= L;
-    if (m.fresh && base > 0) {  // strip start: the new values at base-2, base-1 (staged rows cover them)
+    int qmax[2] = {0, 0};
+    if (mode == EM_SIFT) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+            qmax[s] = __shfl_sync(0xffffffffu, S.to[s], i + 1) + 1 - __shfl_sync(0xffffffffu, S.to[s], i);
+    }
+    if (i == 0 && base > 0) {  // strip start: the new values at base-2, base-1 (staged rows cover them)
         double cc[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int t = base - 2 + u;
             if (mode == EM_INIT) {
-                cc[u] = new_value_global(J, t);
+                cc[u] = init_value(A, S.slot, t);
             } else if (mode == EM_DETECT) {
                 cc[u] = st.samp[u];
             } else {
@@ -257,7 +244,7 @@ __device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, WarpStage& st,
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
                     const double4* R = st.rows[s];
-                    const int qq = smem_search(R, m.vmax[s] - m.vlo[s], tt);
+                    const int qq = smem_search(R, qmax[s], tt);
                     const double4 r0 = R[qq], r1 = R[qq + 1];
                     const double h = r1.x - r0.x;
                     e[s] = spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
@@ -268,12 +255,17 @@ __device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, WarpStage& st,
         c2 = cc[0];
         c1 = cc[1];
     }
-    double cv[kSpt], nv[kSpt];
+    double cv[kSpt];
     if (mode == EM_INIT) {
+        const Slot& sl = A.slots[S.slot];
+        const double* a = sl.init_a;
+        const double* b = sl.init_b;
+        const double beta = sl.beta;
+        const int kind = sl.init_kind;
 #pragma unroll
         for (int k = 0; k < kSpt; ++k) {
             const int t = t0 + k;
-            cv[k] = t < L ? (J.init_kind == 1 ? J.a[t] + J.beta * J.b[t] : J.a[t]) : 0.0;
+            cv[k] = t < L ? (kind == 1 ? a[t] + beta * b[t] : a[t]) : 0.0;
         }
     } else {
         const double* sp = st.samp + 2 + lane * kSpt;
@@ -285,74 +277,80 @@ __device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, WarpStage& st,
         }
     }
 
-    double num = 0.0, den = 0.0;
+    double nv[kSpt];
     if (mode == EM_SIFT) {
         // seg(t) = last staged row q <= qmax with x_q < t (the reference's march, emd.cpp:79).
         // Knot positions are distinct integers, so at most one row boundary lies between
         // consecutive samples: the warp finds each lane's first segment with a bucket map
-        // (row r -> first lane whose t0 exceeds x_r; prefix max over lanes), and the lane's
-        // kSpt segments follow from kSpt-1 independent compares -- no data-dependent branches.
-        double env[2][kSpt];
+        // (row r -> first lane whose t0 exceeds x_r; prefix max over lanes, both sides packed
+        // in 16-bit halves), and the lane's kSpt segments follow from kSpt-1 independent
+        // compares -- no data-dependent branches.
+        st.qmap[lane] = make_int2(0, 0);
+        __syncwarp();
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const double4* R = st.rows[s];
-            const int qmax = m.vmax[s] - m.vlo[s];
-            int* qm = st.qmap[s];
-            qm[lane] = 0;
-            __syncwarp();
 #pragma unroll
-            for (int i = 0; i < (kWarpRows + 31) / 32; ++i) {
-                const int r = 1 + lane + 32 * i;
-                if (r <= qmax) {
+            for (int q = 0; q < (kWarpRows + 31) / 32; ++q) {
+                const int r = 1 + lane + 32 * q;
+                if (r <= qmax[s]) {
                     const int d = (int)R[r].x - base;  // x integral; bucket = first lane with t0 > x
-                    const int b = d < 0 ? 0 : (d >> 2) + 1;
-                    if (b < 32) atomicMax(&qm[b], r);
+                    const int bk = d < 0 ? 0 : (d >> 2) + 1;
+                    if (bk < 32) atomicMax(s == 0 ? &st.qmap[bk].x : &st.qmap[bk].y, r);
                 }
             }
-            __syncwarp();
-            int q0 = qm[lane];
+        }
+        __syncwarp();
+        const int2 qq = st.qmap[lane];
+        unsigned qp = (unsigned)qq.x | ((unsigned)qq.y << 16);
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, q0, o);
-                if (lane >= o) q0 = max(q0, y);
-            }
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, qp, o);
+            if (lane >= o) qp = __vmaxu2(qp, y);
+        }
+        double env0[kSpt];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const double4* R = st.rows[s];
+            const int q0 = s == 0 ? (int)(qp & 0xFFFF) : (int)(qp >> 16);
             double xa[kSpt - 1];
 #pragma unroll
-            for (int i = 1; i < kSpt; ++i) xa[i - 1] = q0 + i <= qmax ? R[q0 + i].x : 1e300;
+            for (int u = 1; u < kSpt; ++u) xa[u - 1] = q0 + u <= qmax[s] ? R[q0 + u].x : 1e300;
 #pragma unroll
             for (int k = 0; k < kSpt; ++k) {
                 const double tt = (double)(t0 + k);
                 int q = q0;
 #pragma unroll
-                for (int i = 1; i <= k; ++i) q += xa[i - 1] < tt;
+                for (int u = 1; u <= k; ++u) q += xa[u - 1] < tt;
                 const double4 r0 = R[q], r1 = R[q + 1];
                 const double h = r1.x - r0.x;
-                env[s][k] = spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < kSpt; ++k) {
-            const double mean = 0.5 * (env[0][k] + env[1][k]);  // emd.cpp:144-147
-            if (t0 + k < L) {
-                num += mean * mean;
-                den += cv[k] * cv[k];
-                nv[k] = cv[k] - mean;
-            } else {
-                nv[k] = 0.0;
+                const double e = spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
+                if (s == 0) {
+                    env0[k] = e;
+                } else {
+                    const double mean = 0.5 * (env0[k] + e);  // emd.cpp:144-147
+                    if (t0 + k < L) {
+                        snum += mean * mean;
+                        sden += cv[k] * cv[k];
+                        nv[k] = cv[k] - mean;
+                    } else {
+                        nv[k] = 0.0;
+                    }
+                }
             }
         }
     } else {
 #pragma unroll
         for (int k = 0; k < kSpt; ++k) nv[k] = cv[k];
     }
-    if (dst) {
-        if (inside) {
+    if (S.dst) {
+        if (t0 + kSpt <= L) {
 #pragma unroll
             for (int k = 0; k < kSpt; k += 2)
-                __stcs(reinterpret_cast<double2*>(dst + t0 + k), make_double2(nv[k], nv[k + 1]));
+                __stcs(reinterpret_cast<double2*>(S.dst + t0 + k), make_double2(nv[k], nv[k + 1]));
         } else {
             for (int k = 0; k < kSpt; ++k)
-                if (t0 + k < L) dst[t0 + k] = nv[k];
+                if (t0 + k < L) S.dst[t0 + k] = nv[k];
         }
     }
     // detection window t0-1 .. t0+2 needs values t0-2 .. t0+3
@@ -382,7 +380,7 @@ __device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, WarpStage& st,
             Win6 win;
 #pragma unroll
             for (int z = 0; z < kSpt + 2; ++z) win.w[z] = w[z];
-            if (plateau_flags(J, t, win, t0, v, mn)) fmax |= 1u << k;
+            if (plateau_flags(A, S.slot, mode, t, win, t0, v, mn)) fmax |= 1u << k;
             if (mn) fmin |= 1u << k;
         }
     }
@@ -397,85 +395,69 @@ __device__ void eval_warp_tile(const Arena& A, const WarpMeta& m, WarpStage& st,
     }
     const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
     const unsigned excl = incl - packed;
-    unsigned omax = excl & 0xFFFF, omin = excl >> 16;
     if (fmax | fmin) {
-        int* si0 = A.sidx + stage_off(A, 0, slot) + (size_t)j * kTileKnots;
-        int* si1 = A.sidx + stage_off(A, 1, slot) + (size_t)j * kTileKnots;
-        double* sv0 = A.sval + stage_off(A, 0, slot) + (size_t)j * kTileKnots;
-        double* sv1 = A.sval + stage_off(A, 1, slot) + (size_t)j * kTileKnots;
+        const size_t side1 = (size_t)A.G * A.tiles * kTileKnots;
+        const size_t o = S.stg + (size_t)i * kTileKnots;
+        unsigned omax = excl & 0xFFFF, omin = excl >> 16;
 #pragma unroll
         for (int k = 0; k < kSpt; ++k) {
             if (fmax & (1u << k)) {
-                si0[omax] = t0 - 1 + k;
-                sv0[omax] = w[k + 1];
+                A.sidx[o + omax] = t0 - 1 + k;
+                A.sval[o + omax] = w[k + 1];
                 ++omax;
             }
             if (fmin & (1u << k)) {
-                si1[omin] = t0 - 1 + k;
-                sv1[omin] = w[k + 1];
+                A.sidx[side1 + o + omin] = t0 - 1 + k;
+                A.sval[side1 + o + omin] = w[k + 1];
                 ++omin;
             }
         }
     }
-    if (mode == EM_SIFT) {
-        num = warp_sum(num);
-        den = warp_sum(den);
-    }
     if (lane == 0) {
-        A.scnt[scnt_off(A, 0, slot) + j] = total & 0xFFFF;
-        A.scnt[scnt_off(A, 1, slot) + j] = total >> 16;
-        if (mode == EM_SIFT) {
-            A.tnum[tsd_off(A, slot) + j] = num;
-            A.tden[tsd_off(A, slot) + j] = den;
-        }
+        const size_t c = scnt_off(A, 0, S.slot) + j;
+        A.scnt[c] = total & 0xFFFF;
+        A.scnt[c + (size_t)A.G * tiles4(A)] = total >> 16;
     }
 }
 
-// Warp-level software pipeline over the warp's strips: tile i is computed while
-// the copies of tile i+1 are in flight and the metadata of tile i+2 is loading.
+// Warp-level software pipeline: tile i is computed while the bulk copies of tile
+// i+1 are in flight. SD partials are summed per lane over the strip and reduced
+// once per strip (tnum/tden are indexed by strip).
 __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     extern __shared__ __align__(16) unsigned char eval_smem[];
+    const int lane = threadIdx.x & 31;
     WarpStage* stage = reinterpret_cast<WarpStage*>(eval_smem) + 2 * (threadIdx.x >> 5);
     const unsigned strips = ((unsigned)A.tiles + kStripTiles - 1) / kStripTiles;
     const unsigned nstrips = (unsigned)A.ctrl->n_eval * strips;
     const unsigned wpb = kEvalThreads / 32;
-    const unsigned stride = gridDim.x * wpb;
-    const unsigned q0 = blockIdx.x * wpb + (threadIdx.x >> 5);
-    // tile `seq` of this warp's sequence; a short last strip jumps to the next strip
-    auto meta = [&](unsigned& sq) {
-        WarpMeta m = fetch_meta(A, q0, stride, sq, nstrips);
-        while (m.valid == 2) {
-            sq = (sq / kStripTiles + 1) * kStripTiles;
-            m = fetch_meta(A, q0, stride, sq, nstrips);
-        }
-        return m;
-    };
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         bar_init(&stage[0].bar);
         bar_init(&stage[1].bar);
     }
     __syncwarp();
     unsigned phase = 0;  // bit b: parity of stage b's next completion
-    unsigned seq0 = 0;
-    WarpMeta cur = meta(seq0);
-    issue_stage(A, cur, stage[0]);
-    unsigned seq1 = seq0 + 1;
-    WarpMeta nxt = meta(seq1);
-    double c2 = 0.0, c1 = 0.0;
-    for (unsigned i = 0; cur.valid; ++i) {
-        issue_stage(A, nxt, stage[(i + 1) & 1]);
-        unsigned seq2 = seq1 + 1;
-        const WarpMeta after = meta(seq2);
-        const unsigned b = i & 1;
-        bar_wait(&stage[b].bar, (phase >> b) & 1u);
-        phase ^= 1u << b;
-        eval_warp_tile(A, cur, stage[b], c2, c1);
-        __syncwarp();  // stage b is refilled next iteration
-        cur = nxt;
-        nxt = after;
-        seq1 = seq2;
+    int b = 0;           // stage of the next tile
+    for (unsigned item = blockIdx.x * wpb + (threadIdx.x >> 5); item < nstrips; item += gridDim.x * wpb) {
+        const Strip S = strip_setup(A, item, strips);
+        issue_tile(A, S, 0, stage[b]);
+        double c2 = 0.0, c1 = 0.0, snum = 0.0, sden = 0.0;
+        for (int i = 0; i < S.nt; ++i) {
+            if (i + 1 < S.nt) issue_tile(A, S, i + 1, stage[b ^ 1]);
+            bar_wait(&stage[b].bar, (phase >> b) & 1u);
+            phase ^= 1u << b;
+            eval_tile(A, S, i, stage[b], c2, c1, snum, sden);
+            __syncwarp();  // stage b is refilled next
+            b ^= 1;
+        }
+        if (S.mode == EM_SIFT) {
+            snum = warp_sum(snum);
+            sden = warp_sum(sden);
+            if (lane == 0) {
+                A.tnum[tsd_off(A, S.slot) + S.j0 / kStripTiles] = snum;
+                A.tden[tsd_off(A, S.slot) + S.j0 / kStripTiles] = sden;
+            }
+        }
     }
-    // the last issue was for an invalid tile (arrive only): no copies are in flight
 }
 
 size_t eval_smem_bytes() { return sizeof(WarpStage) * 2 * (kEvalThreads / 32); }

@@ -291,21 +291,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
             A.ctot[chunk_off(A, side, s) + c] = tot;
         }
         if (side == 0 && S.state == ST_SIFT) {  // SD sums (emd.cpp:145-146), fixed reduction order
-            const double* tn = A.tnum + tsd_off(A, s);
-            const double* td = A.tden + tsd_off(A, s);
+            // k_eval leaves one partial per 16-tile strip; this chunk owns strips [jb/16, ceil(je/16))
+            static_assert(kScanChunk == 16 * kScanThreads, "one strip per scan thread");
+            const int sx = jb / 16 + tid;
             double a = 0.0, b = 0.0;
-#pragma unroll
-            for (int q = 0; q < kScanPer / 2; ++q) {
-                if (j0 + 2 * q < je) {
-                    const double2 x = *reinterpret_cast<const double2*>(tn + j0 + 2 * q);
-                    const double2 y = *reinterpret_cast<const double2*>(td + j0 + 2 * q);
-                    a += x.x;
-                    b += y.x;
-                    if (j0 + 2 * q + 1 < je) {
-                        a += x.y;
-                        b += y.y;
-                    }
-                }
+            if (sx < (je + 15) / 16) {
+                a = A.tnum[tsd_off(A, s) + sx];
+                b = A.tden[tsd_off(A, s) + sx];
             }
             a = warp_sum(a);
             b = warp_sum(b);
