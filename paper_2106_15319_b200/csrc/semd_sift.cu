@@ -846,18 +846,18 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
     const int nf = C->n_final;
     const int tiles = (A.L + kFinalTile - 1) / kFinalTile;
     const unsigned nitems = nf > 0 ? (unsigned)tiles : 0u;
-    constexpr int PER = kFinalTile / 256;
+    static_assert(kFinalTile == 4 * 256, "4 consecutive samples per thread");
+    const size_t L = (size_t)A.L;
     while (true) {
         if (threadIdx.x == 0) s_ticket = atomicAdd(&C->ticket[3], 1u);
         __syncthreads();
         const unsigned q = s_ticket;
         __syncthreads();
         if (q >= nitems) break;
-        const size_t t0 = (size_t)q * kFinalTile;
-        double acc[PER];
+        const size_t tb = (size_t)q * kFinalTile + 4 * threadIdx.x;  // this thread's 4 samples
+        const bool full = tb + 4 <= L;  // slot rows are whole tiles: 32-byte aligned vector access
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
         double* accrow = nullptr;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) acc[i] = 0.0;
         for (int c0 = 0; c0 < nf; c0 += kFinalChunk) {
             const int cn = min(kFinalChunk, nf - c0);
             __syncthreads();
@@ -874,44 +874,68 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
                 tab[li] = f;
             }
             __syncthreads();
-            for (int li = 0; li < cn; ++li) {
-                const FinalSlot f = tab[li];
-                if (f.row && f.row != accrow) {
-                    if (accrow) {
+            if (tb >= L) continue;
+            // groups of 4 slots: all loads in flight first, then the adds in slot order
+            for (int g = 0; g < cn; g += 4) {
+                double xv[4][4], iv[4][4];
 #pragma unroll
-                        for (int i = 0; i < PER; ++i) {
-                            const size_t t = t0 + threadIdx.x + 256 * i;
-                            if (t < (size_t)A.L) accrow[t] = acc[i];
+                for (int u = 0; u < 4; ++u) {
+                    if (g + u >= cn) break;
+                    const FinalSlot& f = tab[g + u];
+                    if (full) {
+                        const double2 a0 = __ldcs(reinterpret_cast<const double2*>(f.x + tb));
+                        const double2 a1 = __ldcs(reinterpret_cast<const double2*>(f.x + tb) + 1);
+                        const double2 b0 = __ldcs(reinterpret_cast<const double2*>(f.imf + tb));
+                        const double2 b1 = __ldcs(reinterpret_cast<const double2*>(f.imf + tb) + 1);
+                        xv[u][0] = a0.x; xv[u][1] = a0.y; xv[u][2] = a1.x; xv[u][3] = a1.y;
+                        iv[u][0] = b0.x; iv[u][1] = b0.y; iv[u][2] = b1.x; iv[u][3] = b1.y;
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            xv[u][e] = tb + e < L ? f.x[tb + e] : 0.0;
+                            iv[u][e] = tb + e < L ? f.imf[tb + e] : 0.0;
                         }
                     }
-                    accrow = f.row;
+                }
 #pragma unroll
-                    for (int i = 0; i < PER; ++i) {
-                        const size_t t = t0 + threadIdx.x + 256 * i;
-                        acc[i] = t < (size_t)A.L ? accrow[t] : 0.0;
+                for (int u = 0; u < 4; ++u) {
+                    if (g + u >= cn) break;
+                    const FinalSlot& f = tab[g + u];
+                    double rv[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) rv[e] = xv[u][e] - iv[u][e];  // emd.cpp:167
+                    if (full) {
+                        reinterpret_cast<double2*>(f.res + tb)[0] = make_double2(rv[0], rv[1]);
+                        reinterpret_cast<double2*>(f.res + tb)[1] = make_double2(rv[2], rv[3]);
+                    } else {
+                        for (int e = 0; e < 4; ++e)
+                            if (tb + e < L) f.res[tb + e] = rv[e];
+                    }
+                    if (f.imf_out || f.res_out) {
+                        for (int e = 0; e < 4; ++e) {
+                            if (tb + e >= L) break;
+                            if (f.imf_out) f.imf_out[tb + e] = iv[u][e];
+                            if (f.res_out) f.res_out[tb + e] = rv[e];
+                        }
+                    }
+                    if (f.row) {
+                        if (f.row != accrow) {
+                            if (accrow)
+                                for (int e = 0; e < 4; ++e)
+                                    if (tb + e < L) accrow[tb + e] = acc[e];
+                            accrow = f.row;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) acc[e] = tb + e < L ? accrow[tb + e] : 0.0;
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[e] = acc[e] + iv[u][e];  // emd.cpp:249-251, slot order
                     }
                 }
-#pragma unroll
-                for (int i = 0; i < PER; ++i) {
-                    const size_t t = t0 + threadIdx.x + 256 * i;
-                    if (t >= (size_t)A.L) continue;
-                    const double x = f.x[t];
-                    const double imf = f.imf[t];
-                    const double res = x - imf;
-                    f.res[t] = res;
-                    if (f.imf_out) f.imf_out[t] = imf;
-                    if (f.res_out) f.res_out[t] = res;
-                    if (f.row) acc[i] = acc[i] + imf;
-                }
             }
         }
-        if (accrow) {
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const size_t t = t0 + threadIdx.x + 256 * i;
-                if (t < (size_t)A.L) accrow[t] = acc[i];
-            }
-        }
+        if (accrow)
+            for (int e = 0; e < 4; ++e)
+                if (tb + e < L) accrow[tb + e] = acc[e];
     }
     if (threadIdx.x == 0) {
         __threadfence();
