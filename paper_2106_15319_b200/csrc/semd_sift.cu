@@ -449,8 +449,8 @@ __device__ __forceinline__ void fwd_step(const SolveCtx& c, int i, double& d, do
 struct SolveShared {
     unsigned ticket;
     int item, b, last, any;
-    int dirty[kSolveChains + 1];
-    int moved[kSolveChains + 1];
+    int dirty[kSolveMaxChains];
+    int moved[kSolveMaxChains];
 };
 
 __device__ void solve_small(const KnotView& kv, double4* tab, double* sm) {
@@ -528,31 +528,32 @@ __device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) 
     tab[0] = make_double4(x0, y0, 0.0, 1.0 / (xn - x0));
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
+__global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena A) {
     extern __shared__ double sm[];
     __shared__ SolveShared sh;
     Ctrl* C = A.ctrl;
     const int tid = threadIdx.x;
     const int nblocks = C->solve_blocks;
     const int nitems = C->n_solve;
-    while (true) {
-        if (tid == 0) {
-            sh.ticket = atomicAdd(&C->ticket[2], 1u);
-            if (sh.ticket < (unsigned)nblocks) {
-                int lo = 0, hi = nitems - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if ((unsigned)A.solve_off[mid] <= sh.ticket) lo = mid;
-                    else hi = mid - 1;
-                }
-                sh.item = lo;
-                sh.b = (int)sh.ticket - A.solve_off[lo];
-            }
+    // static round-robin blocks; the (slot, side) item of a block is the last i with
+    // solve_off[i] <= block. The next block's item is searched by an idle helper thread
+    // during this block's forward sweep.
+    auto find_item = [&](int blk, int lo) {
+        int hi = nitems - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (A.solve_off[mid] <= blk) lo = mid;
+            else hi = mid - 1;
         }
-        __syncthreads();
-        if (sh.ticket >= (unsigned)nblocks) break;
-        const int code = A.solve_item[sh.item];
-        const int slot = code >> 1, side = code & 1, b = sh.b;
+        return lo;
+    };
+    if (tid == 0 && (int)blockIdx.x < nblocks) sh.item = find_item(blockIdx.x, 0);
+    __syncthreads();
+    for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+        const int item = sh.item;
+        const int code = A.solve_item[item];
+        const int slot = code >> 1, side = code & 1, b = blk - A.solve_off[item];
+        __syncthreads();  // sh.item consumed
         const Slot& S = A.slots[slot];
         KnotView kv;
         kv.idx = A.kidx + knot_off(A, S.par, side, slot);
@@ -562,19 +563,22 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
         kv.mom = nullptr;
         double4* tab = A.ktab + tab_off(A, side, slot);
         const int N = kv.n + 4;
+        const int next = blk + (int)gridDim.x;
         if (N - 2 <= kSolveSeqMax) {
-            solve_small(kv, tab, sm);
+            if (tid == kSolveThreads - 1 && next < nblocks) sh.item = find_item(next, item);
+            solve_small(kv, tab, sm);  // ends with __syncthreads
             continue;
         }
-        const int HW = kSolveHalo, B = kSolveBlock, CH = kSolveChunk, NT = kSolveChains, W0 = kSolveWarm;
+        const int HW = kSolveHalo, B = kSolveBlock, CH = kSolveChunk, W0 = kSolveWarm;
         const int r0 = 1 + b * B;
         const int r1 = min(r0 + B, N - 1);
         const int r1e = min(r1 + HW, N - 1);
-        const int wa = max(0, r0 - HW - 1);
-        const int wb = min(N - 1, r1 + HW);
+        const int ra = max(1, r0 - HW);              // first chain row (front halo)
+        const int wa = max(0, ra - W0 - 1);          // staged window: every chain warms up W0 rows
+        const int wb = r1e;
         const int wn = wb - wa + 1;
         double* H = sm;          // [wn]   H[v] = X[v+1]-X[v]
-        double* RHS = H + kSolveWin;
+        double* RHS = H + kSolveWin;     // rhs; after the forward sweep: RN(1/diag)
         double* DP = RHS + kSolveWin;
         double* RP = DP + kSolveWin;
         double* M = RP + kSolveWin;
@@ -613,28 +617,22 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
         }
         __syncthreads();
         SolveCtx cx{H, RHS, wa};
-        // chain c < NT owns rows [cs, ce) of [r0, r1); chain NT owns the back halo [r1, r1e)
+        // Chains tile rows [ra, rb) = [r0-HW, r1+HW) (clipped to the system) in CH-row pieces:
+        // the front-halo chains (rows < r0) only carry the forward state up to r0-1, the
+        // back-halo chains (rows >= r1) only the back-substitution down to r1.
+        const int rb = r1e;
+        const int nch = (rb - ra + CH - 1) / CH;
         const int c = tid;
-        int cs = 0, ce = 0;
-        if (c < NT) {
-            cs = min(r0 + c * CH, r1);
-            ce = min(cs + CH, r1);
-        } else if (c == NT) {
-            cs = r1;
-            ce = r1e;
-        }
-        const bool mine = c <= NT && cs < ce;
+        const int cs = ra + c * CH, ce = min(cs + CH, rb);
+        const bool mine = c < nch;
         double* rec = A.sb + (((size_t)side * A.G + slot) * A.max_blocks + b) * 6;
-        // --- phase A: forward from a guessed state kSolveWarm rows early (chain 0: kSolveHalo)
+        // --- phase A: forward from a guessed state kSolveWarm rows early (exact from row 1)
+        if (tid == kSolveThreads - 1 && next < nblocks) sh.item = find_item(next, item);  // idle helper
         if (mine) {
-            const int ws = max(1, cs - (c == 0 ? HW : W0));
+            const int ws = max(1, cs - W0);
             double d, r;
             fwd_first(cx, ws, d, r);  // exact when ws == 1, otherwise a guess
             for (int i = ws + 1; i < cs; ++i) fwd_step(cx, i, d, r);
-            if (c == 0 && r0 > 1) {
-                rec[0] = d;  // warm-up state at row r0-1 (cross-block check)
-                rec[1] = r;
-            }
             if (ws < cs) fwd_step(cx, cs, d, r);
             DP[cs - wa] = d;
             RP[cs - wa] = r;
@@ -644,12 +642,12 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
                 RP[i - wa] = r;
             }
         }
-        if (tid <= NT) sh.moved[tid] = 1;
+        if (tid < kSolveMaxChains) sh.moved[tid] = 1;
         __syncthreads();
         // --- phase B: replay chain heads from the predecessor's end state until bitwise agreement
-        for (int round = 0; round <= NT; ++round) {
+        for (int round = 0; round < nch; ++round) {
             if (tid == 0) sh.any = 0;
-            if (tid <= NT) sh.dirty[tid] = 0;
+            if (tid < kSolveMaxChains) sh.dirty[tid] = 0;
             __syncthreads();
             if (mine && c >= 1 && sh.moved[c - 1]) {
                 double d = DP[cs - 1 - wa], r = RP[cs - 1 - wa];
@@ -670,34 +668,36 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
             }
             __syncthreads();
             const int any = sh.any;
-            if (tid <= NT) sh.moved[tid] = sh.dirty[tid];
+            if (tid < kSolveMaxChains) sh.moved[tid] = sh.dirty[tid];
             __syncthreads();
             if (!any) break;
         }
-        // --- phase C: back substitution (emd.cpp:70-73), speculative above each chunk
+        for (int q = tid + r0 - wa; q < rb - wa; q += blockDim.x) RHS[q] = 1.0 / DP[q];  // RN(1/diag)
+        __syncthreads();
+        // --- phase C: back substitution (emd.cpp:70-73), speculative above each chunk;
+        // chains below r0 take no part
         auto upper = [&](int i) { return H[i - wa]; };  // X[i+1]-X[i]
-        if (mine) {
-            const int top = c == NT ? ce : min(ce + W0, r1e);
+        const bool back = mine && ce > r0;
+        if (back) {
+            const int top = min(ce + W0, rb);
             double m = 0.0;  // exact when top == N-1, otherwise a guess
             for (int i = top - 1; i >= cs; --i) {
-                const double dp = DP[i - wa];
-                m = div_rn(RP[i - wa] - upper(i) * m, dp, 1.0 / dp);
+                m = div_rn(RP[i - wa] - upper(i) * m, DP[i - wa], RHS[i - wa]);
                 if (i < ce) M[i - wa] = m;
             }
         }
-        if (tid <= NT) sh.moved[tid] = 1;
+        if (tid < kSolveMaxChains) sh.moved[tid] = 1;
         __syncthreads();
         // --- phase D: replay chain tails from the successor's first value
-        for (int round = 0; round <= NT; ++round) {
+        for (int round = 0; round < nch; ++round) {
             if (tid == 0) sh.any = 0;
-            if (tid <= NT) sh.dirty[tid] = 0;
+            if (tid < kSolveMaxChains) sh.dirty[tid] = 0;
             __syncthreads();
-            if (mine && c < NT && ce < N - 1 && sh.moved[c + 1]) {
+            if (back && c + 1 < nch && sh.moved[c + 1]) {
                 double m = M[ce - wa];
                 bool conv = false;
                 for (int i = ce - 1; i >= cs; --i) {
-                    const double dp = DP[i - wa];
-                    m = div_rn(RP[i - wa] - upper(i) * m, dp, 1.0 / dp);
+                    m = div_rn(RP[i - wa] - upper(i) * m, DP[i - wa], RHS[i - wa]);
                     if (m == M[i - wa]) {
                         conv = true;
                         break;
@@ -711,17 +711,17 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
             }
             __syncthreads();
             const int any = sh.any;
-            if (tid <= NT) sh.moved[tid] = sh.dirty[tid];
+            if (tid < kSolveMaxChains) sh.moved[tid] = sh.dirty[tid];
             __syncthreads();
             if (!any) break;
         }
-        // --- outputs + cross-block records: [0,1] warm-up state at r0-1, [2,3]
-        // this block's state at r1-1, [4] m at r0, [5] the m at r1 it used
+        // --- outputs + cross-block records: [0,1] forward state at r0-1 (from the front halo),
+        // [2,3] this block's state at r1-1, [4] m at r0, [5] the m at r1 it used
         // segment table rows {x, y, m, 1/h} (vknot re-reads the staged knot from L2)
         for (int i = r0 + tid; i < r1; i += blockDim.x) {
             double x, y;
             vknot(kv, i, x, y);
-            tab[i] = make_double4(x, y, M[i - wa], 1.0 / H[i - wa]);  // x, y re-read (L2-resident)
+            tab[i] = make_double4(x, y, M[i - wa], 1.0 / H[i - wa]);
         }
         if (tid == 0) {
             if (r0 == 1) {
@@ -733,6 +733,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
                 double x, y;
                 vknot(kv, N - 1, x, y);
                 tab[N - 1] = make_double4(x, y, 0.0, 0.0);
+            }
+            if (r0 > 1) {
+                rec[0] = DP[r0 - 1 - wa];
+                rec[1] = RP[r0 - 1 - wa];
             }
             rec[2] = DP[r1 - 1 - wa];
             rec[3] = RP[r1 - 1 - wa];
@@ -748,46 +752,97 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(Arena A) {
     __syncthreads();
     if (sh.last) {
         __threadfence();
+        // Cross-block check of every multi-block envelope: block bb's warm-up state at r0-1
+        // must equal block bb-1's state there, and the m at r0 it produced must equal the m
+        // block bb-1 assumed. Items with few blocks are checked by one thread each; items
+        // with many blocks (queued in shared memory) by the whole CTA.
+        __shared__ int s_big[64];
+        __shared__ int s_nbig, s_bad;
+        if (tid == 0) s_nbig = 0;
+        __syncthreads();
+        auto boundary_bad = [&](const double* base, int bb) {
+            const double* p = base + (size_t)(bb - 1) * 6;
+            const double* q = base + (size_t)bb * 6;
+            const bool fwd = __ldcg(q) != __ldcg(p + 2) || __ldcg(q + 1) != __ldcg(p + 3);
+            const bool bwd = __ldcg(p + 5) != __ldcg(q + 4);
+            return fwd ? 1 : (bwd ? 2 : 0);
+        };
+        auto log_hazard = [&](int slot, int side, int bb, int nb, int kind) {
+            const int pos = atomicAdd(&C->hz_count, 1);
+            if (A.hzlog && pos < A.hzlog_cap) {
+                const Slot& S = A.slots[slot];
+                int* r = A.hzlog + (size_t)pos * 8;
+                r[0] = S.m;
+                r[1] = S.k;
+                r[2] = S.iter;
+                r[3] = side;
+                r[4] = (int)S.n[side];
+                r[5] = bb;
+                r[6] = nb;
+                r[7] = kind;  // 1 forward state, 2 back-substitution
+            }
+        };
+        auto repair = [&](int slot, int side, int bad) {  // the whole envelope again, sequentially and exactly
+            atomicAdd(&A.slots[slot].hazards, bad);
+            atomicAdd(&C->hazards, bad);
+            const Slot& S = A.slots[slot];
+            KnotView kv;
+            kv.idx = A.kidx + knot_off(A, S.par, side, slot);
+            kv.val = A.kval + knot_off(A, S.par, side, slot);
+            kv.n = (int)S.n[side];
+            kv.e2 = 2.0 * (double)(A.L - 1);
+            kv.mom = nullptr;
+            solve_sequential(kv, A.ktab + tab_off(A, side, slot));
+        };
         for (int it = tid; it < nitems; it += blockDim.x) {
+            const int nb = A.solve_off[it + 1] - A.solve_off[it];
+            if (nb <= 1) continue;
+            if (nb > 32) {
+                const int k = atomicAdd(&s_nbig, 1);
+                if (k < 64) {
+                    s_big[k] = it;
+                    continue;
+                }
+            }
             const int code = A.solve_item[it];
             const int slot = code >> 1, side = code & 1;
-            const int nb = A.solve_off[it + 1] - A.solve_off[it];
-            if ((int)A.slots[slot].n[side] + 2 <= kSolveSeqMax) continue;
             const double* base = A.sb + ((size_t)side * A.G + slot) * A.max_blocks * 6;
             int bad = 0;
             for (int bb = 1; bb < nb; ++bb) {
-                const double* p = base + (size_t)(bb - 1) * 6;
-                const double* q = base + (size_t)bb * 6;
-                if (__ldcg(q) != __ldcg(p + 2) || __ldcg(q + 1) != __ldcg(p + 3) || __ldcg(p + 5) != __ldcg(q + 4)) {
+                const int kind = boundary_bad(base, bb);
+                if (kind) {
                     ++bad;
-                    const int pos = atomicAdd(&C->hz_count, 1);
-                    if (A.hzlog && pos < A.hzlog_cap) {
-                        const Slot& S = A.slots[slot];
-                        int* r = A.hzlog + (size_t)pos * 8;
-                        r[0] = S.m;
-                        r[1] = S.k;
-                        r[2] = S.iter;
-                        r[3] = side;
-                        r[4] = (int)S.n[side];
-                        r[5] = bb;
-                        r[6] = nb;
-                        r[7] = (__ldcg(q) != __ldcg(p + 2) || __ldcg(q + 1) != __ldcg(p + 3)) ? 1 : 2;  // 1 fwd, 2 back
-                    }
+                    log_hazard(slot, side, bb, nb, kind);
                 }
             }
-            if (A.debug & 1) bad += nb > 1;
-            if (bad) {  // repair: the whole envelope again, sequentially and exactly
-                atomicAdd(&A.slots[slot].hazards, bad);
-                atomicAdd(&C->hazards, bad);
-                const Slot& S = A.slots[slot];
-                KnotView kv;
-                kv.idx = A.kidx + knot_off(A, S.par, side, slot);
-                kv.val = A.kval + knot_off(A, S.par, side, slot);
-                kv.n = (int)S.n[side];
-                kv.e2 = 2.0 * (double)(A.L - 1);
-                kv.mom = nullptr;
-                solve_sequential(kv, A.ktab + tab_off(A, side, slot));
+            if (A.debug & 1) ++bad;
+            if (bad) repair(slot, side, bad);
+        }
+        __syncthreads();
+        const int nbig = min(s_nbig, 64);
+        for (int k = 0; k < nbig; ++k) {
+            const int it = s_big[k];
+            const int nb = A.solve_off[it + 1] - A.solve_off[it];
+            const int code = A.solve_item[it];
+            const int slot = code >> 1, side = code & 1;
+            const double* base = A.sb + ((size_t)side * A.G + slot) * A.max_blocks * 6;
+            if (tid == 0) s_bad = 0;
+            __syncthreads();
+            int bad = 0;
+            for (int bb = 1 + tid; bb < nb; bb += blockDim.x) {
+                const int kind = boundary_bad(base, bb);
+                if (kind) {
+                    ++bad;
+                    log_hazard(slot, side, bb, nb, kind);
+                }
             }
+            if (bad) atomicAdd(&s_bad, bad);
+            __syncthreads();
+            if (tid == 0) {
+                const int tb = s_bad + ((A.debug & 1) ? 1 : 0);
+                if (tb) repair(slot, side, tb);
+            }
+            __syncthreads();
         }
         if (tid == 0) {
             C->ticket[2] = 0;
@@ -977,7 +1032,7 @@ unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC
 void count_launches(int n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
 
 void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begin, cudaEvent_t eval_end) {
-    k_solve<<<2 * sms, kSolveThreads, solve_smem_bytes(), st>>>(A);
+    k_solve<<<kSolveCtasPerSm * sms, kSolveThreads, solve_smem_bytes(), st>>>(A);
     if (eval_begin) cudaEventRecord(eval_begin, st);
     launch_eval(A, sms, st);
     if (eval_end) cudaEventRecord(eval_end, st);

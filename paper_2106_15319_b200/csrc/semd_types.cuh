@@ -32,13 +32,15 @@ constexpr int kKnotCapTile = kEvalTile / 2 + 4; // knots of one side touching a 
 constexpr int kTileKnots = kEvalTile / 2;       // stage capacity per tile and side
 
 constexpr int kSolveChains = 64;                         // speculative chains per block
-constexpr int kSolveChunk = 32;                          // rows per chain
-constexpr int kSolveWarm = 16;                           // per-chain warm-up rows
+constexpr int kSolveChunk = 16;                          // rows per chain
+constexpr int kSolveWarm = 32;                           // per-chain warm-up rows
 constexpr int kSolveBlock = kSolveChains * kSolveChunk;  // rows per CTA
-constexpr int kSolveHalo = 64;                           // cross-block warm-up rows
-constexpr int kSolveThreads = kSolveChains + 64;         // + the back-halo chain + load helpers
+constexpr int kSolveHalo = 64;                           // cross-block warm-up rows (front and back halo chains)
+constexpr int kSolveThreads = 128;                       // >= kSolveMaxChains (the rest help staging)
+constexpr int kSolveCtasPerSm = 4;
+constexpr int kSolveMaxChains = (kSolveBlock + 2 * kSolveHalo) / kSolveChunk;  // chains tiling a block + halos
 constexpr int kSolveSeqMax = 96;                         // rows solved by one exact thread
-constexpr int kSolveWin = kSolveBlock + 2 * kSolveHalo + 4;  // knot window per block
+constexpr int kSolveWin = kSolveBlock + 2 * kSolveHalo + kSolveWarm + 4;  // staged knot window per block
 
 constexpr int kFinalTile = 1024;
 
