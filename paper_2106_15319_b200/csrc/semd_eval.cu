@@ -429,7 +429,6 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     WarpStage* stage = reinterpret_cast<WarpStage*>(eval_smem) + 2 * (threadIdx.x >> 5);
     const unsigned strips = ((unsigned)A.tiles + kStripTiles - 1) / kStripTiles;
     const unsigned nstrips = (unsigned)A.ctrl->n_eval * strips;
-    const unsigned wpb = kEvalThreads / 32;
     if (lane == 0) {
         bar_init(&stage[0].bar);
         bar_init(&stage[1].bar);
@@ -437,7 +436,15 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     __syncwarp();
     unsigned phase = 0;  // bit b: parity of stage b's next completion
     int b = 0;           // stage of the next tile
-    for (unsigned item = blockIdx.x * wpb + (threadIdx.x >> 5); item < nstrips; item += gridDim.x * wpb) {
+    // dynamic strip tickets (C->ticket[0], reset by k_scan): a CTA that starts late -- e.g.
+    // next to the noise generator on the side stream -- just takes fewer strips. The next
+    // ticket is fetched one strip ahead.
+    unsigned* tk = &A.ctrl->ticket[0];
+    unsigned item = 0, next = 0;
+    if (lane == 0) item = atomicAdd(tk, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    while (item < nstrips) {
+        if (lane == 0) next = atomicAdd(tk, 1u);
         const Strip S = strip_setup(A, item, strips);
         issue_tile(A, S, 0, stage[b]);
         double c2 = 0.0, c1 = 0.0, snum = 0.0, sden = 0.0;
@@ -457,6 +464,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
                 A.tden[tsd_off(A, S.slot) + S.j0 / kStripTiles] = sden;
             }
         }
+        item = __shfl_sync(0xffffffffu, next, 0);
     }
 }
 

@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
     if (s_last) {
         __threadfence();
         decide_after_eval(A);
-        if (tid == 0) C->done[4] = 0;
+        if (tid == 0) {
+            C->done[4] = 0;
+            C->ticket[0] = 0;  // k_eval's strip tickets
+        }
     }
 }
 
@@ -535,9 +538,9 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
     const int tid = threadIdx.x;
     const int nblocks = C->solve_blocks;
     const int nitems = C->n_solve;
-    // static round-robin blocks; the (slot, side) item of a block is the last i with
-    // solve_off[i] <= block. The next block's item is searched by an idle helper thread
-    // during this block's forward sweep.
+    // dynamic block tickets (C->ticket[2]); the (slot, side) item of a block is the last i
+    // with solve_off[i] <= block. The next ticket and its item are fetched by an idle helper
+    // thread during this block's forward sweep.
     auto find_item = [&](int blk, int lo) {
         int hi = nitems - 1;
         while (lo < hi) {
@@ -547,13 +550,23 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         }
         return lo;
     };
-    if (tid == 0 && (int)blockIdx.x < nblocks) sh.item = find_item(blockIdx.x, 0);
+    if (tid == 0) {
+        sh.b = (int)atomicAdd(&C->ticket[2], 1u);
+        if (sh.b < nblocks) sh.item = find_item(sh.b, 0);
+    }
     __syncthreads();
-    for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    while (true) {
+        const int blk = sh.b;
+        if (blk >= nblocks) break;
         const int item = sh.item;
         const int code = A.solve_item[item];
         const int slot = code >> 1, side = code & 1, b = blk - A.solve_off[item];
-        __syncthreads();  // sh.item consumed
+        __syncthreads();  // sh.b / sh.item consumed
+        auto prefetch = [&]() {  // one thread: the next block and its item
+            const int nb2 = (int)atomicAdd(&C->ticket[2], 1u);
+            sh.b = nb2;
+            if (nb2 < nblocks) sh.item = find_item(nb2, item);
+        };
         const Slot& S = A.slots[slot];
         KnotView kv;
         kv.idx = A.kidx + knot_off(A, S.par, side, slot);
@@ -563,9 +576,8 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         kv.mom = nullptr;
         double4* tab = A.ktab + tab_off(A, side, slot);
         const int N = kv.n + 4;
-        const int next = blk + (int)gridDim.x;
         if (N - 2 <= kSolveSeqMax) {
-            if (tid == kSolveThreads - 1 && next < nblocks) sh.item = find_item(next, item);
+            if (tid == kSolveThreads - 1) prefetch();
             solve_small(kv, tab, sm);  // ends with __syncthreads
             continue;
         }
@@ -627,7 +639,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         const bool mine = c < nch;
         double* rec = A.sb + (((size_t)side * A.G + slot) * A.max_blocks + b) * 6;
         // --- phase A: forward from a guessed state kSolveWarm rows early (exact from row 1)
-        if (tid == kSolveThreads - 1 && next < nblocks) sh.item = find_item(next, item);  // idle helper
+        if (tid == kSolveThreads - 1) prefetch();  // idle helper
         if (mine) {
             const int ws = max(1, cs - W0);
             double d, r;
