@@ -484,8 +484,20 @@ struct semd_ctx {
         const int jobs = std::max(0, m_end - m_begin);
         const int G = auto_slots(n, jobs);
         int kcap = default_kcap(n, cfg.max_imfs);
-        const double beta = device_std(d_x, n, ens.nstd);  // emd.cpp:233
         const long long Ls = (n + 1) / 2 * 2;
+        // the first wave's noise (side stream) overlaps the sequential std on the main stream
+        bool first_noise_ready = false;
+        if (!noise_override && jobs > 0) {
+            noise.alloc((size_t)2 * G * Ls * 8);
+            semd::dev::launch_rng_ensemble(ens.base_seed, m_begin, std::min(G, jobs),
+                                           reinterpret_cast<uint64_t*>(noise.as<double>()), Ls, n, rng_stream);
+            semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(noise.as<double>()),
+                                         (long long)std::min(G, jobs) * Ls, 1.0, rng_stream);
+            ck(cudaGetLastError(), "rng");
+            ck(cudaEventRecord(noise_ready[0], rng_stream), "rng event");
+            first_noise_ready = true;
+        }
+        const double beta = device_std(d_x, n, ens.nstd);  // emd.cpp:233
         for (int attempt = 0;; ++attempt) {
             configure(n, G, kcap, tr ? trace_cap_for(tr) : 0);
             A.sd_threshold = cfg.sd_threshold;
@@ -507,7 +519,8 @@ struct semd_ctx {
                 ck(cudaEventRecord(noise_ready[b], rng_stream), "rng event");
             };
             try {
-                if (!noise_override) make_noise(m_begin, 0);
+                if (!noise_override && !first_noise_ready) make_noise(m_begin, 0);
+                first_noise_ready = false;  // a capacity retry regenerates it
                 int wi = 0;
                 for (int w0 = m_begin; w0 < m_end; w0 += G, ++wi) {
                     const int g = std::min(G, m_end - w0);
