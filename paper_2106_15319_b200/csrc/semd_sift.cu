@@ -352,38 +352,51 @@ __device__ void emit_trace(const Arena& A, const Slot& S, uint64_t h) {
     }
 }
 
-// One warp per (compact slot, side, tile) item, grid-stride (no tickets).
+// One warp per (compact slot, side, strip of 16 tiles) item, grid-stride: lanes load
+// the strip's tile counts and offsets in one coalesced access, then the warp
+// copies each tile's extrema (16 tiles x <= 64 knots).
 constexpr int kCompactThreads = 128;
+constexpr int kCompactStrip = 16;
 __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
     __shared__ int s_last;
     Ctrl* C = A.ctrl;
     const int lane = threadIdx.x & 31;
     const int wpb = kCompactThreads / 32;
-    const unsigned nitems = (unsigned)C->n_compact * 2u * (unsigned)A.tiles;
+    const int strips = (A.tiles + kCompactStrip - 1) / kCompactStrip;
+    const unsigned per_slot = 2u * (unsigned)strips;
+    const unsigned nitems = (unsigned)C->n_compact * per_slot;
     const bool tracing = A.trace != nullptr;
     for (unsigned it = blockIdx.x * wpb + (threadIdx.x >> 5); it < nitems; it += gridDim.x * wpb) {
-        const unsigned per_slot = 2u * (unsigned)A.tiles;
         const int s = A.compact_list[it / per_slot];
         const unsigned r = it % per_slot;
-        const int side = (int)(r / (unsigned)A.tiles);
-        const int j = (int)(r % (unsigned)A.tiles);
+        const int side = (int)(r / (unsigned)strips);
+        const int sx = (int)(r % (unsigned)strips);
+        const int j0 = sx * kCompactStrip;
+        const int nt = min(kCompactStrip, A.tiles - j0);
         const int cpar = A.slots[s].cpar;
-        const unsigned cnt = A.scnt[scnt_off(A, side, s) + j];
-        const unsigned off = toff_view(A, cpar, side, s)[j];
-        const int* si = A.sidx + stage_off(A, side, s) + (size_t)j * kTileKnots;
-        const double* sv = A.sval + stage_off(A, side, s) + (size_t)j * kTileKnots;
-        int* gi = A.kidx + knot_off(A, cpar, side, s) + off;
-        double* gv = A.kval + knot_off(A, cpar, side, s) + off;
+        unsigned cnt = 0, off = 0;
+        if (lane < nt) {
+            cnt = A.scnt[scnt_off(A, side, s) + j0 + lane];
+            off = toff_view(A, cpar, side, s)[j0 + lane];
+        }
+        const int* si = A.sidx + stage_off(A, side, s) + (size_t)j0 * kTileKnots;
+        const double* sv = A.sval + stage_off(A, side, s) + (size_t)j0 * kTileKnots;
+        int* gi = A.kidx + knot_off(A, cpar, side, s);
+        double* gv = A.kval + knot_off(A, cpar, side, s);
         uint64_t h = 0;
-        for (unsigned i = lane; i < cnt; i += 32) {
-            const int t = si[i];
-            gi[i] = t;
-            gv[i] = sv[i];
-            if (tracing) h += knot_hash(side, off + i, (unsigned)t);
+        for (int u = 0; u < nt; ++u) {
+            const unsigned cu = __shfl_sync(0xffffffffu, cnt, u);
+            const unsigned ou = __shfl_sync(0xffffffffu, off, u);
+            for (unsigned i = lane; i < cu; i += 32) {
+                const int t = si[u * kTileKnots + i];
+                gi[ou + i] = t;
+                gv[ou + i] = sv[u * kTileKnots + i];
+                if (tracing) h += knot_hash(side, ou + i, (unsigned)t);
+            }
         }
         if (tracing) {
             h = warp_sum(h);
-            if (lane == 0) A.thash[((size_t)side * A.G + s) * A.tiles + j] = h;
+            if (lane == 0) A.thash[((size_t)side * A.G + s) * A.tiles + sx] = h;
         }
     }
     __syncthreads();
@@ -400,7 +413,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
                 const int s = A.compact_list[li];
                 const Slot& S = A.slots[s];
                 uint64_t h = 0;
-                for (int j = lane; j < A.tiles; j += 32)
+                const int strips = (A.tiles + kCompactStrip - 1) / kCompactStrip;
+                for (int j = lane; j < strips; j += 32)
                     h += __ldcg(A.thash + (size_t)s * A.tiles + j) + __ldcg(A.thash + ((size_t)A.G + s) * A.tiles + j);
                 h = warp_sum(h);
                 if (lane == 0 && S.trace_iter >= 0) emit_trace(A, S, h);
