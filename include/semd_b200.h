@@ -168,6 +168,26 @@ int semd_serial_decompose_device(semd_ctx* ctx, int algo, const double* d_x, siz
                                  const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* d_tensor,
                                  size_t k_cap, size_t* modes_out);
 
+/* ---- CEEMDAN across GPUs: stages over a realization shard (emd.cpp:264-344) ----------
+ * Rank r owns realizations [m_begin, m_end) (seeds from the global index). Driver loop:
+ *   begin; stage(partial); all-reduce(partial) -> total; finish_stage(total, nr, 0, ...);
+ *   while (max_imfs == 0 || K < max_imfs) {
+ *     residue_extrema(&t); if (t < 3) break;                       (emd.cpp:311)
+ *     stage(partial); all-reduce; finish_stage(total, nr, 1, mode, &ok); if (!ok) break;
+ *   }
+ *   residue(out).
+ * stage() writes the UNSCALED sum over the shard of this stage's first modes (n doubles);
+ * finish_stage scales the global total by 1/nr, stops on an all-zero mode (ok = 0;
+ * emd.cpp:332-337) or subtracts it from the residue. With one shard [0, nr) this is
+ * bit-identical to semd_decompose(SEMD_ALGO_CEEMDAN). One active shard per context. */
+int semd_ceemdan_shard_begin(semd_ctx* ctx, const double* d_x, size_t n, const semd_sift_cfg* cfg,
+                             const semd_ens_cfg* ens, int32_t m_begin, int32_t m_end);
+int semd_ceemdan_shard_residue_extrema(semd_ctx* ctx, size_t* total);
+int semd_ceemdan_shard_stage(semd_ctx* ctx, double* d_partial);
+int semd_ceemdan_shard_finish_stage(semd_ctx* ctx, const double* d_total, int32_t nr, int32_t check_zero,
+                                    double* d_mode_out, int32_t* accepted);
+int semd_ceemdan_shard_residue(semd_ctx* ctx, double* d_res_out);
+
 #ifdef __cplusplus
 }
 #endif

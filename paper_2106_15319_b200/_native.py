@@ -92,6 +92,13 @@ SIGNATURES = {
     "semd_serial_decompose_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
                                                C.POINTER(SiftCfg), C.POINTER(EnsCfg), C.c_void_p, C.c_size_t,
                                                _szp]),
+    "semd_ceemdan_shard_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(SiftCfg), C.POINTER(EnsCfg),
+                                           C.c_int32, C.c_int32]),
+    "semd_ceemdan_shard_residue_extrema": (C.c_int, [C.c_void_p, _szp]),
+    "semd_ceemdan_shard_stage": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "semd_ceemdan_shard_finish_stage": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                                  C.POINTER(C.c_int32)]),
+    "semd_ceemdan_shard_residue": (C.c_int, [C.c_void_p, C.c_void_p]),
 }
 # test-only hook (not part of the reference API)
 EXTRA = {"semd_set_noise_override": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t]),

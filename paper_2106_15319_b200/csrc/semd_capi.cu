@@ -560,153 +560,207 @@ struct semd_ctx {
         }
     }
 
-    // emd.cpp:264-344. Returns K; IMFs in `out_imfs` (device, kcap rows), residue in out_res.
-    int ceemdan_device(const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens,
-                       double* out_imfs, int k_cap, double* out_res, semd_trace* tr, int* k_needed) {
+    // ---- CEEMDAN (emd.cpp:264-344) as stages over a realization shard [m0, m1) ----------
+    // begin -> stage 0 -> finish -> { residue_extrema >= 3 ? stage K -> finish : stop }.
+    // A stage leaves the UNSCALED sum of the shard's first modes (realization order) in
+    // sums row K; finish takes the all-shard total (this row on one GPU, an all-reduced
+    // copy across GPUs), scales it by 1/nr, applies the all-zero stop (emd.cpp:332-337) and
+    // updates the residue. Every rank holds the same residue, so beta_i, the stop tests and
+    // the modes are identical on all ranks.
+    struct CeemdanShard {
+        bool active = false;
+        const double* x = nullptr;
+        long long n = 0, Ls = 0;
+        semd_sift_cfg cfg{};
+        semd_ens_cfg ens{};
+        int m0 = 0, m1 = 0, G = 1, kcap = 0, K = 0, waves = 0;
+        double beta0 = 0.0;
+        std::vector<char> alive;
+    } cs;
+    double* cs_noise() { return noise.as<double>(); }         // shard noise residues (Ls stride)
+    double* cs_E() { return scratch.as<double>(); }           // E_i(w^(m)) of the shard (n stride)
+    double* cs_residue() { return scratch2.as<double>(); }
+    int* cs_flag() { return reinterpret_cast<int*>(scratch2.as<double>() + cs.n); }
+
+    void ceemdan_begin(const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens, int m0,
+                       int m1, semd_trace* tr) {
         if (n < 4) raise(SEMD_INVALID_INPUT, "ceemdan: signal too short (need at least 4 samples)");
-        const int nr = ens.nr;
-        const int G = auto_slots(n, nr);
-        int kcap = default_kcap(n, cfg.max_imfs);
-        configure(n, G, kcap, tr ? trace_cap_for(tr) : 0);
+        if (m0 < 0 || m1 < m0 || m1 > ens.nr) raise(SEMD_INVALID_INPUT, "invalid realization range");
+        cs = CeemdanShard{};
+        cs.x = d_x;
+        cs.n = n;
+        cs.Ls = (n + 1) / 2 * 2;
+        cs.cfg = cfg;
+        cs.ens = ens;
+        cs.m0 = m0;
+        cs.m1 = m1;
+        const int cnt = m1 - m0;
+        cs.G = auto_slots(n, std::max(1, cnt));
+        cs.kcap = default_kcap(n, cfg.max_imfs);
+        configure(n, cs.G, cs.kcap, tr ? trace_cap_for(tr) : 0);
         A.sd_threshold = cfg.sd_threshold;
         A.max_sift_iters = cfg.max_sift_iters;
         h_trace.clear();
         trace_total = 0;
-        const long long Ls = (n + 1) / 2 * 2;
-        noise.alloc((size_t)nr * Ls * 8);    // noise residues (per realization)
-        scratch.alloc((size_t)nr * n * 8);   // E_i(w^(m))
-        scratch2.alloc((size_t)n * 8 * 2);   // residue + nonzero flag
-        double* noise_res = noise.as<double>();
-        double* E = scratch.as<double>();
-        double* residue = scratch2.as<double>();
-        int* nonzero = reinterpret_cast<int*>(residue + n);
+        noise.alloc((size_t)std::max(1, cnt) * cs.Ls * 8);
+        scratch.alloc((size_t)std::max(1, cnt) * n * 8);
+        scratch2.alloc((size_t)n * 8 * 2);
         if (noise_override) {
-            for (int m = 0; m < nr; ++m)
-                ck(cudaMemcpyAsync(noise_res + (size_t)m * Ls, noise_override + (size_t)m * n, n * 8,
+            for (int i = 0; i < cnt; ++i)
+                ck(cudaMemcpyAsync(cs_noise() + (size_t)i * cs.Ls, noise_override + (size_t)(m0 + i) * n, n * 8,
                                    cudaMemcpyDeviceToDevice, stream),
                    "noise override");
         } else {
-            for (int m0 = 0; m0 < nr; m0 += 1024) {
-                const int g = std::min(1024, nr - m0);
+            for (int i0 = 0; i0 < cnt; i0 += 1024) {
+                const int g = std::min(1024, cnt - i0);
                 std::vector<uint64_t> seeds(g);
-                for (int i = 0; i < g; ++i) seeds[i] = derive_seed(ens.base_seed, (uint64_t)(m0 + i));
-                gen_noise(seeds, n, Ls, noise_res + (size_t)m0 * Ls);
+                for (int i = 0; i < g; ++i) seeds[i] = derive_seed(ens.base_seed, (uint64_t)(m0 + i0 + i));
+                gen_noise(seeds, n, cs.Ls, cs_noise() + (size_t)i0 * cs.Ls);
             }
         }
-        std::vector<char> alive(nr, 1);
-        semd::dev::launch_copy(d_x, residue, n, stream);
-        fill_sums(kcap, 0.0);
-        const double inv = 1.0 / (double)nr;
-        int K = 0;
-        int waves = 0;
-        auto run_tasks = [&](std::vector<JobSpec>& all, std::vector<Slot>* results) {
-            results->resize(all.size());
-            for (size_t w0 = 0; w0 < all.size(); w0 += G) {
-                const size_t g = std::min<size_t>(G, all.size() - w0);
-                std::vector<JobSpec> js(all.begin() + w0, all.begin() + w0 + g);
-                set_jobs(js);
-                run(max_steps_for(cfg));
-                ++waves;
-                for (size_t i = 0; i < g; ++i) (*results)[w0 + i] = h_slots[i];
-            }
-        };
-        auto stage_mean = [&](int row, bool check_zero) -> bool {
-            double* mode = A.sums + (size_t)row * n;
-            ck(cudaMemsetAsync(nonzero, 0, 4, stream), "flag");
-            semd::dev::launch_stage_scale(mode, n, inv, nonzero, stream);
-            int nz = 0;
-            ck(cudaMemcpyAsync(&nz, nonzero, 4, cudaMemcpyDeviceToHost, stream), "flag");
-            ck(cudaStreamSynchronize(stream), "stage");
-            if (check_zero && !nz) return false;
-            semd::dev::launch_sub(residue, mode, n, stream);
-            return true;
-        };
-        {  // mode 1 (emd.cpp:292-307)
-            const double beta0 = device_std(d_x, n, ens.nstd);
-            std::vector<JobSpec> js(nr);
-            for (int m = 0; m < nr; ++m) {
-                JobSpec& J = js[m];
-                J.m = m;
+        cs.alive.assign(cnt, 1);
+        semd::dev::launch_copy(d_x, cs_residue(), n, stream);
+        fill_sums(cs.kcap, 0.0);
+        cs.beta0 = device_std(d_x, n, ens.nstd);  // emd.cpp:293
+        cs.active = true;
+    }
+
+    void cs_run_tasks(std::vector<JobSpec>& all, std::vector<Slot>* results) {
+        results->resize(all.size());
+        for (size_t w0 = 0; w0 < all.size(); w0 += cs.G) {
+            const size_t g = std::min<size_t>(cs.G, all.size() - w0);
+            std::vector<JobSpec> js(all.begin() + w0, all.begin() + w0 + g);
+            set_jobs(js);
+            run(max_steps_for(cs.cfg));
+            ++cs.waves;
+            for (size_t i = 0; i < g; ++i) (*results)[w0 + i] = h_slots[i];
+        }
+    }
+
+    // find_extrema(residue).total() (emd.cpp:311)
+    long long ceemdan_residue_extrema() {
+        if (!cs.active) raise(SEMD_INVALID_INPUT, "ceemdan: no active shard (call begin)");
+        JobSpec J;
+        J.m = -1;
+        J.task = 3;
+        J.k = cs.K;
+        J.a = cs_residue();
+        J.detect_only = 1;
+        std::vector<JobSpec> js{J};
+        std::vector<Slot> res;
+        cs_run_tasks(js, &res);
+        return (long long)res[0].n[0] + (long long)res[0].n[1];
+    }
+
+    // the shard's unscaled first-mode sum of stage K into sums row K
+    void ceemdan_stage() {
+        if (!cs.active) raise(SEMD_INVALID_INPUT, "ceemdan: no active shard (call begin)");
+        if (cs.K >= cs.kcap) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", cs.kcap);
+        const int cnt = cs.m1 - cs.m0;
+        const long long n = cs.n;
+        if (cs.K == 0) {  // mode 1 (emd.cpp:292-307): first modes of x + beta0 w^(m)
+            std::vector<JobSpec> js(cnt);
+            for (int i = 0; i < cnt; ++i) {
+                JobSpec& J = js[i];
+                J.m = cs.m0 + i;
                 J.task = 2;
                 J.k = 0;
                 J.kmax = 1;
                 J.init_kind = 1;
-                J.beta = beta0;
-                J.a = d_x;
-                J.b = noise_res + (size_t)m * Ls;
+                J.beta = cs.beta0;
+                J.a = cs.x;
+                J.b = cs_noise() + (size_t)i * cs.Ls;
             }
             std::vector<Slot> res;
-            run_tasks(js, &res);
-            stage_mean(0, false);
-            K = 1;
+            cs_run_tasks(js, &res);
+            return;
         }
-        while (cfg.max_imfs == 0 || K < cfg.max_imfs) {  // emd.cpp:310
-            if (K >= kcap) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", kcap);
-            {  // stage check: find_extrema(residue).total() < 3 (emd.cpp:311)
+        const double beta_i = device_std(cs_residue(), n, cs.ens.nstd);  // emd.cpp:312
+        {  // E_i(w^(m)) for the living noise residues (emd.cpp:316-325)
+            std::vector<JobSpec> js;
+            std::vector<int> idx;
+            for (int i = 0; i < cnt; ++i) {
+                if (!cs.alive[i]) continue;
                 JobSpec J;
-                J.m = -1;
-                J.task = 3;
-                J.k = K;
-                J.a = residue;
-                J.detect_only = 1;
-                std::vector<JobSpec> js{J};
-                std::vector<Slot> res;
-                run_tasks(js, &res);
-                if (res[0].n[0] + res[0].n[1] < 3) break;
+                J.m = cs.m0 + i;
+                J.task = 1;
+                J.k = cs.K;
+                J.kmax = cs.K + 1;
+                J.write_imf = 0;
+                J.a = cs_noise() + (size_t)i * cs.Ls;
+                J.imf_out = cs_E() + (size_t)i * n;
+                J.res_out = cs_noise() + (size_t)i * cs.Ls;
+                js.push_back(J);
+                idx.push_back(i);
             }
-            const double beta_i = device_std(residue, n, ens.nstd);  // emd.cpp:312
-            {  // E_i(w^(m)) for the living noise residues (emd.cpp:316-325)
-                std::vector<JobSpec> js;
-                std::vector<int> ms;
-                for (int m = 0; m < nr; ++m) {
-                    if (!alive[m]) continue;
-                    JobSpec J;
-                    J.m = m;
-                    J.task = 1;
-                    J.k = K;
-                    J.kmax = K + 1;
-                    J.write_imf = 0;
-                    J.a = noise_res + (size_t)m * Ls;
-                    J.imf_out = E + (size_t)m * n;
-                    J.res_out = noise_res + (size_t)m * Ls;
-                    js.push_back(J);
-                    ms.push_back(m);
-                }
-                std::vector<Slot> res;
-                run_tasks(js, &res);
-                for (size_t i = 0; i < ms.size(); ++i) {
-                    if (res[i].ended_insufficient) {
-                        alive[ms[i]] = 0;
-                        ck(cudaMemsetAsync(E + (size_t)ms[i] * n, 0, n * 8, stream), "E zero");
-                    }
+            std::vector<Slot> res;
+            cs_run_tasks(js, &res);
+            for (size_t q = 0; q < idx.size(); ++q) {
+                if (res[q].ended_insufficient) {
+                    cs.alive[idx[q]] = 0;
+                    ck(cudaMemsetAsync(cs_E() + (size_t)idx[q] * n, 0, n * 8, stream), "E zero");
                 }
             }
-            {  // first modes of r_i + beta_i E_i (emd.cpp:326-329)
-                std::vector<JobSpec> js(nr);
-                for (int m = 0; m < nr; ++m) {
-                    JobSpec& J = js[m];
-                    J.m = m;
-                    J.task = 2;
-                    J.k = K;
-                    J.kmax = K + 1;
-                    J.init_kind = 1;
-                    J.beta = beta_i;
-                    J.a = residue;
-                    J.b = E + (size_t)m * n;
-                }
-                std::vector<Slot> res;
-                run_tasks(js, &res);
-            }
-            if (!stage_mean(K, true)) break;  // all-zero mode (emd.cpp:332-337)
-            ++K;
         }
-        stats.waves += waves;
-        stats.slots = G;
+        {  // first modes of r_i + beta_i E_i (emd.cpp:326-329)
+            std::vector<JobSpec> js(cnt);
+            for (int i = 0; i < cnt; ++i) {
+                JobSpec& J = js[i];
+                J.m = cs.m0 + i;
+                J.task = 2;
+                J.k = cs.K;
+                J.kmax = cs.K + 1;
+                J.init_kind = 1;
+                J.beta = beta_i;
+                J.a = cs_residue();
+                J.b = cs_E() + (size_t)i * n;
+            }
+            std::vector<Slot> res;
+            cs_run_tasks(js, &res);
+        }
+    }
+
+    // mode_K = total / nr; false (and no update) when check_zero and the mode is all zero.
+    bool ceemdan_finish(const double* d_total, int nr, bool check_zero, double* d_mode_out) {
+        if (!cs.active) raise(SEMD_INVALID_INPUT, "ceemdan: no active shard (call begin)");
+        if (nr < 1) raise(SEMD_INVALID_INPUT, "ensemble: nr must be at least 1");
+        const long long n = cs.n;
+        double* mode = A.sums + (size_t)cs.K * n;
+        if (d_total && d_total != mode)
+            ck(cudaMemcpyAsync(mode, d_total, n * 8, cudaMemcpyDeviceToDevice, stream), "stage total");
+        ck(cudaMemsetAsync(cs_flag(), 0, 4, stream), "flag");
+        semd::dev::launch_stage_scale(mode, n, 1.0 / (double)nr, cs_flag(), stream);
+        int nz = 0;
+        ck(cudaMemcpyAsync(&nz, cs_flag(), 4, cudaMemcpyDeviceToHost, stream), "flag");
+        ck(cudaStreamSynchronize(stream), "stage");
+        if (check_zero && !nz) return false;  // emd.cpp:332-337
+        semd::dev::launch_sub(cs_residue(), mode, n, stream);
+        if (d_mode_out) ck(cudaMemcpyAsync(d_mode_out, mode, n * 8, cudaMemcpyDeviceToDevice, stream), "mode");
+        ++cs.K;
+        return true;
+    }
+
+    // emd.cpp:264-344 on one GPU. Returns K; IMFs in `out_imfs` (device, k_cap rows), residue in out_res.
+    int ceemdan_device(const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens,
+                       double* out_imfs, int k_cap, double* out_res, semd_trace* tr, int* k_needed) {
+        ceemdan_begin(d_x, n, cfg, ens, 0, ens.nr, tr);
+        ceemdan_stage();
+        ceemdan_finish(nullptr, ens.nr, false, nullptr);
+        while (cfg.max_imfs == 0 || cs.K < cfg.max_imfs) {  // emd.cpp:310
+            if (cs.K >= cs.kcap) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", cs.kcap);
+            if (ceemdan_residue_extrema() < 3) break;
+            ceemdan_stage();
+            if (!ceemdan_finish(nullptr, ens.nr, true, nullptr)) break;
+        }
+        const int K = cs.K;
+        stats.waves += cs.waves;
+        stats.slots = cs.G;
         *k_needed = K;
+        cs.active = false;
         if (K > k_cap) return K;
         if (out_imfs && K)
             ck(cudaMemcpyAsync(out_imfs, A.sums, (size_t)K * n * 8, cudaMemcpyDeviceToDevice, stream), "imfs");
-        if (out_res) ck(cudaMemcpyAsync(out_res, residue, n * 8, cudaMemcpyDeviceToDevice, stream), "residue");
+        if (out_res) ck(cudaMemcpyAsync(out_res, cs_residue(), n * 8, cudaMemcpyDeviceToDevice, stream), "residue");
         ck(cudaStreamSynchronize(stream), "ceemdan");
         return K;
     }
@@ -909,6 +963,56 @@ int semd_set_noise_override(semd_ctx* ctx, const double* noise, size_t nr, size_
         ctx->in_y.alloc(nr * n * 8);
         ck(cudaMemcpy(ctx->in_y.p, noise, nr * n * 8, cudaMemcpyHostToDevice), "noise override");
         ctx->noise_override = ctx->in_y.as<double>();
+    });
+}
+
+// ---- CEEMDAN stages over a realization shard (multi-GPU drivers) ----------------------
+int semd_ceemdan_shard_begin(semd_ctx* ctx, const double* d_x, size_t n, const semd_sift_cfg* cfg_,
+                             const semd_ens_cfg* ens_, int32_t m_begin, int32_t m_end) {
+    return guard([&] {
+        need_ctx(ctx);
+        const semd_sift_cfg cfg = sift_or_default(cfg_);
+        const semd_ens_cfg ens = ens_or_default(ens_);
+        if (ens.nr < 1) raise(SEMD_INVALID_INPUT, "ensemble: nr must be at least 1");
+        if (ens.nstd < 0.0) raise(SEMD_INVALID_INPUT, "ensemble: nstd must be non-negative");
+        ctx->reset_stats(1);
+        ctx->ceemdan_begin(d_x, (long long)n, cfg, ens, m_begin, m_end, nullptr);
+    });
+}
+int semd_ceemdan_shard_residue_extrema(semd_ctx* ctx, size_t* total) {
+    return guard([&] {
+        need_ctx(ctx);
+        const long long t = ctx->ceemdan_residue_extrema();
+        if (total) *total = (size_t)t;
+    });
+}
+int semd_ceemdan_shard_stage(semd_ctx* ctx, double* d_partial) {
+    return guard([&] {
+        need_ctx(ctx);
+        ctx->ceemdan_stage();
+        if (d_partial)
+            ck(cudaMemcpyAsync(d_partial, ctx->A.sums + (size_t)ctx->cs.K * ctx->cs.n, ctx->cs.n * 8,
+                               cudaMemcpyDeviceToDevice, ctx->stream),
+               "partial");
+        ck(cudaStreamSynchronize(ctx->stream), "stage");
+    });
+}
+int semd_ceemdan_shard_finish_stage(semd_ctx* ctx, const double* d_total, int32_t nr, int32_t check_zero,
+                                    double* d_mode_out, int32_t* accepted) {
+    return guard([&] {
+        need_ctx(ctx);
+        const bool ok = ctx->ceemdan_finish(d_total, nr, check_zero != 0, d_mode_out);
+        if (accepted) *accepted = ok ? 1 : 0;
+        ck(cudaStreamSynchronize(ctx->stream), "finish");
+    });
+}
+int semd_ceemdan_shard_residue(semd_ctx* ctx, double* d_res_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!ctx->cs.active) raise(SEMD_INVALID_INPUT, "ceemdan: no active shard (call begin)");
+        ck(cudaMemcpyAsync(d_res_out, ctx->cs_residue(), ctx->cs.n * 8, cudaMemcpyDeviceToDevice, ctx->stream),
+           "residue");
+        ck(cudaStreamSynchronize(ctx->stream), "residue");
     });
 }
 

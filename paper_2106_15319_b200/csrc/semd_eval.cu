@@ -295,7 +295,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
                 const int r = 1 + lane + 32 * q;
                 if (r <= qmax[s]) {
                     const int d = (int)R[r].x - base;  // x integral; bucket = first lane with t0 > x
-                    const int bk = d < 0 ? 0 : (d >> 2) + 1;
+                    const int bk = d < 0 ? 0 : d / kSpt + 1;
                     if (bk < 32) atomicMax(s == 0 ? &st.qmap[bk].x : &st.qmap[bk].y, r);
                 }
             }

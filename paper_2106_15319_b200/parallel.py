@@ -1,5 +1,10 @@
 """Realization sharding across GPUs.
 
+CEEMDAN (emd.cpp:264-344) shards the same way but exchanges once per stage:
+each rank sums the first modes of its realizations, one all-reduce(sum) of L
+doubles forms the global stage sum, and every rank applies the identical
+mode / residue update and stop tests (sharded_ceemdan).
+
 EEMD realizations are independent units: rank r of W owns the contiguous
 range shard_range(nr, r, W) and runs them on its own GPU (seeds derive from
 the GLOBAL realization index, emd.cpp:238, so the work of realization m is
@@ -33,6 +38,24 @@ def sharded_ensemble(nr: int, rank: int, world: int,
     K = allreduce_max(k_local)
     total = allreduce_sum(sums, K)
     return finish(total, K)
+
+
+def sharded_ceemdan(nr: int, rank: int, world: int, engine, allreduce_sum: Callable[[object], object],
+                    max_imfs: int = 0):
+    """Generic CEEMDAN stage driver (emd.cpp:290-341) over an engine exposing
+    begin(m_begin, m_end), stage() -> unscaled shard sum, finish(total, check_zero) -> accepted,
+    residue_extrema() -> int and result() -> (modes, residue)."""
+    mb, me = shard_range(nr, rank, world)
+    engine.begin(mb, me)
+    engine.finish(allreduce_sum(engine.stage()), False)  # mode 1
+    k = 1
+    while max_imfs == 0 or k < max_imfs:
+        if engine.residue_extrema() < 3:  # emd.cpp:311
+            break
+        if not engine.finish(allreduce_sum(engine.stage()), True):  # all-zero mode, emd.cpp:332-337
+            break
+        k += 1
+    return engine.result()
 
 
 # ------------------------------------------------------------- torch / GPU driver
@@ -86,6 +109,87 @@ def eemd_distributed(x_dev, n: int, cfg: dict, ens: dict, rank: int, world: int,
 
     imfs, residue = sharded_ensemble(nr, rank, world, partial, amax, asum, finish)
     return imfs, residue, state.get("stats", {})
+
+
+class GpuCeemdanShard:
+    """sharded_ceemdan engine over the C ABI (semd_ceemdan_shard_*) on one GPU."""
+
+    def __init__(self, ctx, x_dev, n: int, cfg: dict, ens: dict):
+        import ctypes as C
+
+        from . import _native as N
+        self.C, self.c, self.x, self.n = C, ctx, x_dev, n
+        self.scfg = N.SiftCfg(cfg.get("sd_threshold", 0.2), cfg.get("max_sift_iters", 300), cfg.get("max_imfs", 0))
+        self.ecfg = N.EnsCfg(ens.get("nstd", 0.2), ens.get("nr", 100), 0, ens.get("base_seed", 0))
+        self.modes = []
+
+    def begin(self, mb, me):
+        C, c = self.C, self.c
+        c.check(c.lib.semd_ceemdan_shard_begin(c.ptr, C.c_void_p(self.x.data_ptr()), self.n, C.byref(self.scfg),
+                                               C.byref(self.ecfg), mb, me))
+
+    def stage(self):
+        import torch
+        part = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
+        self.c.check(self.c.lib.semd_ceemdan_shard_stage(self.c.ptr, self.C.c_void_p(part.data_ptr())))
+        return part
+
+    def finish(self, total, check_zero):
+        import torch
+        C, c = self.C, self.c
+        mode = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
+        ok = C.c_int32()
+        c.check(c.lib.semd_ceemdan_shard_finish_stage(c.ptr, C.c_void_p(total.data_ptr()), self.ecfg.nr,
+                                                      int(check_zero), C.c_void_p(mode.data_ptr()), C.byref(ok)))
+        if ok.value:
+            self.modes.append(mode)
+        return bool(ok.value)
+
+    def residue_extrema(self):
+        t = self.C.c_size_t()
+        self.c.check(self.c.lib.semd_ceemdan_shard_residue_extrema(self.c.ptr, self.C.byref(t)))
+        return int(t.value)
+
+    def result(self):
+        import torch
+        res = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
+        self.c.check(self.c.lib.semd_ceemdan_shard_residue(self.c.ptr, self.C.c_void_p(res.data_ptr())))
+        imfs = torch.stack(self.modes) if self.modes else torch.empty((0, self.n), dtype=torch.float64,
+                                                                        device=self.x.device)
+        return imfs, res
+
+
+def ceemdan_distributed(x_dev, n: int, cfg: dict, ens: dict, rank: int, world: int, ctx=None, group=None):
+    """CEEMDAN with realizations sharded over the ranks' GPUs and one NCCL all-reduce per stage;
+    returns (imfs (K, n), residue) torch tensors (identical on every rank)."""
+    import torch.distributed as dist
+
+    from .api import context
+    c = ctx or context(x_dev.device.index or 0)
+    if float(ens.get("nstd", 0.2)) == 0.0:  # degenerate ensemble is plain EMD (emd.cpp:267), same on every rank
+        import ctypes as C
+
+        import torch
+
+        from . import _native as N
+        k_cap = 64
+        imfs = torch.empty((k_cap, n), dtype=torch.float64, device=x_dev.device)
+        res = torch.empty(n, dtype=torch.float64, device=x_dev.device)
+        k = C.c_size_t()
+        c.check(c.lib.semd_decompose_device(c.ptr, 0, C.c_void_p(x_dev.data_ptr()), n,
+                                            C.byref(N.SiftCfg(cfg.get("sd_threshold", 0.2),
+                                                              cfg.get("max_sift_iters", 300), cfg.get("max_imfs", 0))),
+                                            None, C.c_void_p(imfs.data_ptr()), k_cap, C.byref(k),
+                                            C.c_void_p(res.data_ptr())))
+        return imfs[:k.value], res
+    eng = GpuCeemdanShard(c, x_dev, n, cfg, ens)
+
+    def asum(part):
+        if world > 1:
+            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+        return part
+
+    return sharded_ceemdan(int(ens.get("nr", 100)), rank, world, eng, asum, int(cfg.get("max_imfs", 0)))
 
 
 # ------------------------------------------------------------- numpy reference driver (tests)

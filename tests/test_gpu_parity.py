@@ -430,3 +430,25 @@ def test_cpp_mirror_runs(se):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.startswith("OK")
+
+
+def test_ceemdan_stage_api_matches_monolithic(se, oracle):
+    """The per-stage CEEMDAN API (multi-GPU driver, world 1) is the monolithic CEEMDAN bit-for-bit,
+    and with the oracle's noise injected both are the oracle's CEEMDAN bit-for-bit."""
+    import torch
+
+    from paper_2106_15319_b200.parallel import ceemdan_distributed
+    x = pickup_serialized(se, 50)[:3000].copy()
+    nr = 24
+    ctx = se.context()
+    w = np.stack([oracle.white_noise(x.size, oracle.derive_seed(0, m)) for m in range(nr)])
+    ctx.set_noise_override(w)
+    try:
+        mono = se.decompose(x, "ceemdan", nr=nr)
+        xd = torch.from_numpy(x).cuda()
+        imfs, res = ceemdan_distributed(xd, x.size, {}, {"nr": nr}, 0, 1, ctx=ctx)
+    finally:
+        ctx.set_noise_override(None)
+    o = oracle.decompose(x, 2, nr=nr)
+    assert np.array_equal(imfs.cpu().numpy(), mono["imfs"]) and np.array_equal(res.cpu().numpy(), mono["residue"])
+    assert np.array_equal(mono["imfs"], o[0]) and np.array_equal(mono["residue"], o[1])

@@ -80,3 +80,116 @@ def test_sharded_eemd_world2(oracle, nr):
         assert rel <= 1e-12  # shard-order sums differ from the sequential order only by rounding
         assert np.max(np.abs(x - imfs.sum(0) - r)) <= 1e-12
     assert np.array_equal(res[0][1], res[1][1])  # every rank holds the identical result
+
+
+# ------------------------------------------------------------------ CEEMDAN stage sharding
+
+class OracleCeemdanShard:
+    """sharded_ceemdan engine restated with the oracle's primitives (emd.cpp:264-344): the CPU
+    stand-in for GpuCeemdanShard (same begin/stage/finish/residue_extrema/result contract)."""
+
+    def __init__(self, o, x, nr, nstd=0.2, seed=0, sd=0.2, iters=300):
+        self.o, self.x, self.nr, self.nstd, self.seed, self.sd, self.iters = o, x, nr, nstd, seed, sd, iters
+
+    def _first_mode(self, s):
+        from oracle.ffi import OracleError
+        try:
+            return self.o.extract_imf(s, sd=self.sd, iters=self.iters)[0]
+        except OracleError:  # InsufficientExtrema -> zeros (emd.cpp:280-286)
+            return np.zeros(self.x.size)
+
+    def begin(self, mb, me):
+        o, n = self.o, self.x.size
+        self.ms = list(range(mb, me))
+        self.noise = {m: o.white_noise(n, o.derive_seed(self.seed, m)) for m in self.ms}
+        self.alive = {m: True for m in self.ms}
+        self.residue = self.x.copy()
+        self.modes = []
+        self.beta0 = self.nstd * o.signal_std(self.x)
+
+    def stage(self):
+        from oracle.ffi import OracleError
+        part = np.zeros(self.x.size)
+        if not self.modes:
+            for m in self.ms:
+                part = part + self._first_mode(self.x + self.beta0 * self.noise[m])
+            return part
+        beta = self.nstd * self.o.signal_std(self.residue)
+        for m in self.ms:
+            ei = np.zeros(self.x.size)
+            if self.alive[m]:
+                try:
+                    ei = self.o.extract_imf(self.noise[m], sd=self.sd, iters=self.iters)[0]
+                    self.noise[m] = self.noise[m] - ei
+                except OracleError:
+                    self.alive[m] = False
+            part = part + self._first_mode(self.residue + beta * ei)
+        return part
+
+    def finish(self, total, check_zero):
+        mode = total * (1.0 / float(self.nr))
+        if check_zero and not np.any(mode != 0.0):
+            return False
+        self.residue = self.residue - mode
+        self.modes.append(mode)
+        return True
+
+    def residue_extrema(self):
+        mi, _, ni, _ = self.o.find_extrema(self.residue)
+        return len(mi) + len(ni)
+
+    def result(self):
+        return np.array(self.modes), self.residue
+
+
+def _ceemdan_signal():
+    t = np.arange(700) / 700.0
+    return np.sin(2 * np.pi * 23 * t) + 0.6 * np.sin(2 * np.pi * 5 * t) + 0.3 * np.cos(2 * np.pi * 61 * t)
+
+
+def test_sharded_ceemdan_world1_equals_oracle(oracle):
+    from paper_2106_15319_b200.parallel import sharded_ceemdan
+    x, nr = _ceemdan_signal(), 6
+    imfs, res = sharded_ceemdan(nr, 0, 1, OracleCeemdanShard(oracle, x, nr), lambda p: p)
+    o = oracle.decompose(x, 2, nr=nr)
+    assert imfs.shape == o[0].shape
+    assert np.array_equal(imfs, o[0]) and np.array_equal(res, o[1])
+
+
+def _ceemdan_worker(rank, world, port, x, nr, out_q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle.ffi import Oracle
+    from paper_2106_15319_b200.parallel import sharded_ceemdan
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def asum(part):
+        t = torch.from_numpy(np.ascontiguousarray(part))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.numpy()
+
+    imfs, res = sharded_ceemdan(nr, rank, world, OracleCeemdanShard(Oracle(), x, nr), asum)
+    out_q.put((rank, imfs, res))
+    dist.destroy_process_group()
+
+
+def test_sharded_ceemdan_gloo_world2(oracle):
+    x, nr, world = _ceemdan_signal(), 6, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ceemdan_worker, args=(r, world, port, x, nr, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict((r, (i, s)) for r, i, s in (q.get(timeout=300) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+    o = oracle.decompose(x, 2, nr=nr)
+    for r in range(world):
+        imfs, res = got[r]
+        assert np.array_equal(imfs, got[0][0]) and np.array_equal(res, got[0][1])  # every rank identical
+        assert imfs.shape == o[0].shape
+        assert np.max(np.abs(imfs - o[0])) <= 1e-11 * np.max(np.abs(x))  # stage sums in a different tree
