@@ -107,13 +107,13 @@ def run_ours(args, rank, world, local):
 
     import paper_2106_15319_b200 as se
     from paper_2106_15319_b200 import _native as N
-    from paper_2106_15319_b200.parallel import eemd_distributed, shard_range
+    from paper_2106_15319_b200.parallel import ceemdan_distributed, eemd_distributed, shard_range
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg, x = workload(args.config)
-    if cfg["algo"] != "eemd":
-        raise SystemExit("bench measures the serial-EEMD configs (c2, c4, c5)")
+    if cfg["algo"] not in ("eemd", "ceemdan"):
+        raise SystemExit("bench measures the serial-EEMD / serial-CEEMDAN configs (c2, c3, c4, c5)")
     M, Nch = x.shape
     D = cfg["D"]
     ctx = se.context(local)
@@ -136,8 +136,7 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize(dev)
 
     def step():
-        imfs, res, st = eemd_distributed(s_dev, L, scfg, ens, rank, world, ctx=ctx, k_cap=64)
-        return imfs, res, st
+        return decompose_sharded(cfg, s_dev, L, scfg, ens, rank, world, ctx)
 
     # warm-up
     for _ in range(args.warmup):
@@ -207,6 +206,16 @@ def run_ours(args, rank, world, local):
     return out
 
 
+def decompose_sharded(cfg, s_dev, L, scfg, ens, rank, world, ctx):
+    """One whole decomposition with this rank's realization shard: EEMD (one all-reduce at the end)
+    or CEEMDAN (one all-reduce per stage). Returns (imfs, residue, this rank's engine stats)."""
+    from paper_2106_15319_b200.parallel import ceemdan_distributed, eemd_distributed
+    if cfg["algo"] == "ceemdan":
+        imfs, res = ceemdan_distributed(s_dev, L, scfg, ens, rank, world, ctx=ctx)
+        return imfs, res, ctx.stats()
+    return eemd_distributed(s_dev, L, scfg, ens, rank, world, ctx=ctx, k_cap=64)
+
+
 def _concat_device(lib, ctx, src, dst, M, Nch, D):
     """semd_serial_decompose's first stage on device buffers: transition weights + concatenate kernels."""
     return lib.semd_concatenate_device(ctx.ptr, C.c_void_p(src.data_ptr()), M, Nch, D, C.c_void_p(dst.data_ptr()))
@@ -233,7 +242,7 @@ def run_e2e(args, rank, world, local, ctx, x, cfg, scfg, ens, dev):
         h2d += host_in.numel() * 8
         s_dev = torch.empty(L, dtype=torch.float64, device=dev)
         ctx.check(_concat_device(lib, ctx, d_in, s_dev, M, Nch, D))
-        imfs, res, st = eemd_distributed(s_dev, L, scfg, ens, rank, world, ctx=ctx, k_cap=64)
+        imfs, res, st = decompose_sharded(cfg, s_dev, L, scfg, ens, rank, world, ctx)
         sifted += st.get("sifted_samples", 0)
         if rank == 0:
             modes = torch.cat([imfs, res[None, :]], 0).contiguous()
@@ -254,7 +263,8 @@ def run_e2e(args, rank, world, local, ctx, x, cfg, scfg, ens, dev):
         wall, sifted = float(w[0]), float(t[1])
     return {"value": sifted / wall, "unit": "sifted samples/s", "h2d_bytes_per_step": h2d // steps,
             "d2h_bytes_per_step": d2h // steps, "steps": steps,
-            "path": "pinned host (M,N) -> H2D -> concatenate -> sharded EEMD (+NCCL) -> deconcatenate -> D2H (M,N,K+1)"}
+            "path": f"pinned host (M,N) -> H2D -> concatenate -> sharded {cfg['algo'].upper()} (+NCCL) -> "
+                    "deconcatenate -> D2H (M,N,K+1)"}
 
 
 # ------------------------------------------------------------------ CPU baselines
@@ -277,7 +287,9 @@ def cpu_sample(x, cfg, threads, count=None, scale=1):
     s = impl.concatenate(xc, M, Nch, D)
     count = count or threads
     t0 = time.perf_counter()
-    if kind == "reference":
+    if cfg["algo"] == "ceemdan":  # the reference ceemdan() is sequential: one full decomposition, one thread
+        impl.decompose(s, 2, iters=cfg["max_sift_iters"], imfs=cfg["max_imfs"], nstd=0.2, nr=cfg["nr"])
+    elif kind == "reference":
         impl.emd_realizations(s, 0, count, threads, iters=cfg["max_sift_iters"], imfs=cfg["max_imfs"], nstd=0.2)
     else:
         from concurrent.futures import ThreadPoolExecutor
@@ -288,7 +300,12 @@ def cpu_sample(x, cfg, threads, count=None, scale=1):
 
 
 def sifted_for(s, cfg, m_end, ctx):
-    """Sifted samples of realizations [0, m_end) from the parity-checked GPU engine."""
+    """Sifted samples of realizations [0, m_end) (CEEMDAN: the whole decomposition) from the
+    parity-checked GPU engine."""
+    if cfg["algo"] == "ceemdan":
+        import paper_2106_15319_b200 as se
+        se.decompose(s, "ceemdan", max_sift_iters=cfg["max_sift_iters"], max_imfs=cfg["max_imfs"], nr=cfg["nr"])
+        return ctx.stats()["sifted_samples"]
     import paper_2106_15319_b200 as se
     from paper_2106_15319_b200 import _native as N
     lib = ctx.lib
@@ -310,6 +327,11 @@ def cpu_threads():
 
 def cpu_baseline(args, x, cfg, ctx):
     T = cpu_threads()
+    if cfg["algo"] == "ceemdan":
+        wall, kind, s = cpu_sample(x, cfg, 1)
+        sifted = sifted_for(s, cfg, cfg["nr"], ctx)
+        return {"value": sifted / wall, "unit": "sifted samples/s", "cores": 1, "kind": kind,
+                "sample": f"the whole decomposition by the reference ceemdan() (sequential), wall {wall:.1f} s"}
     wall, kind, s = cpu_sample(x, cfg, T)
     sifted = sifted_for(s, cfg, T, ctx)
     return {"value": sifted / wall, "unit": "sifted samples/s", "cores": T, "kind": kind,
@@ -335,6 +357,8 @@ def run_reference(args, rank, world):
         total_wall += w
     sifted = sifted_for(s, cfg, T, ctx) * args.steps
     value = sifted / total_wall
+    if cfg["algo"] == "ceemdan":
+        T = 1  # the reference ceemdan() is sequential
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "sifted samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_wall / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -350,7 +374,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c5", choices=["c2", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
