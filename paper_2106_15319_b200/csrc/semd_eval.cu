@@ -215,6 +215,9 @@ __device__ __forceinline__ int smem_search(const double4* R, int hi, double t) {
 
 // ---------------------------------------------------------------- one tile
 // kSpt = 4 consecutive samples per lane; c2/c1 carry the new values at base-2/base-1.
+// Interior: the whole tile and its detection windows lie inside [1, L-2] (every tile but the
+// first and the last of a slot) -- no per-sample bound checks.
+template <bool Interior>
 __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i, WarpStage& st, double& c2,
                                           double& c1, double& snum, double& sden) {
     const int lane = threadIdx.x & 31;
@@ -272,8 +275,8 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
 #pragma unroll
         for (int k = 0; k < kSpt; k += 2) {
             const double2 v = *reinterpret_cast<const double2*>(sp + k);
-            cv[k] = t0 + k < L ? v.x : 0.0;
-            cv[k + 1] = t0 + k + 1 < L ? v.y : 0.0;
+            cv[k] = Interior || t0 + k < L ? v.x : 0.0;
+            cv[k + 1] = Interior || t0 + k + 1 < L ? v.y : 0.0;
         }
     }
 
@@ -329,7 +332,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
                     env0[k] = e;
                 } else {
                     const double mean = 0.5 * (env0[k] + e);  // emd.cpp:144-147
-                    if (t0 + k < L) {
+                    if (Interior || t0 + k < L) {
                         snum += mean * mean;
                         sden += cv[k] * cv[k];
                         nv[k] = cv[k] - mean;
@@ -344,7 +347,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         for (int k = 0; k < kSpt; ++k) nv[k] = cv[k];
     }
     if (S.dst) {
-        if (t0 + kSpt <= L) {
+        if (Interior || t0 + kSpt <= L) {
 #pragma unroll
             for (int k = 0; k < kSpt; k += 2)
                 __stcs(reinterpret_cast<double2*>(S.dst + t0 + k), make_double2(nv[k], nv[k + 1]));
@@ -370,7 +373,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
 #pragma unroll
     for (int k = 0; k < kSpt; ++k) {
         const int t = t0 - 1 + k;
-        if (t < 1 || t > L - 2) continue;
+        if (!Interior && (t < 1 || t > L - 2)) continue;
         const double l = w[k], v = w[k + 1], r = w[k + 2];
         if (v != l && v != r) {
             if (v > l && v > r) fmax |= 1u << k;
@@ -452,7 +455,11 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
             if (i + 1 < S.nt) issue_tile(A, S, i + 1, stage[b ^ 1]);
             bar_wait(&stage[b].bar, (phase >> b) & 1u);
             phase ^= 1u << b;
-            eval_tile(A, S, i, stage[b], c2, c1, snum, sden);
+            const int base = (S.j0 + i) * kEvalTile;
+            if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
+                eval_tile<true>(A, S, i, stage[b], c2, c1, snum, sden);
+            else
+                eval_tile<false>(A, S, i, stage[b], c2, c1, snum, sden);
             __syncwarp();  // stage b is refilled next
             b ^= 1;
         }
