@@ -103,6 +103,7 @@ SIGNATURES = {
 # test-only hook (not part of the reference API)
 EXTRA = {"semd_set_noise_override": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t]),
          "semd_set_debug": (C.c_int, [C.c_void_p, C.c_int]),
+         "semd_solve_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
          "semd_hazard_log": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
          "semd_mt19937_64_device_test": (C.c_int, [C.c_void_p, C.c_uint64, C.c_size_t, C.POINTER(C.c_uint64)])}
 

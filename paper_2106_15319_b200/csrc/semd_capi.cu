@@ -120,7 +120,7 @@ struct semd_ctx {
     // engine arena
     Arena A{};
     int cfg_L = -1, cfg_G = -1, cfg_kcap = -1, cfg_trace = -1;
-    DBuf bufs, kidx, kval, toff, tbase, ctot, cnum, cden, ktab, sidx, sval, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog;
+    DBuf bufs, kidx, kval, toff, tbase, ctot, cnum, cden, ktab, sidx, sval, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog, prof;
     int* status_host = nullptr;
     int* status_host_dev = nullptr;
     std::vector<Slot> h_slots;
@@ -221,6 +221,8 @@ struct semd_ctx {
         A.hzlog = hzlog.as<int>();
         A.hzlog_cap = kHzCap;
         A.debug = debug_flags;
+        prof.alloc(16 * 8);
+        A.prof = prof.as<unsigned long long>();
         ck(cudaMemsetAsync(toff.p, 0, toff.bytes, stream), "memset toff");
         ck(cudaMemsetAsync(tbase.p, 0, tbase.bytes, stream), "memset tbase");
         ck(cudaMemsetAsync(sb.p, 0, sb.bytes, stream), "memset sb");
@@ -1022,6 +1024,16 @@ int semd_set_debug(semd_ctx* ctx, int flags) {
         need_ctx(ctx);
         ctx->debug_flags = flags;
         ctx->A.debug = flags;
+    });
+}
+
+// Test hook: k_solve per-phase cycle counters (debug bit 1), 16 u64; reset after reading.
+int semd_solve_profile(semd_ctx* ctx, uint64_t* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!ctx->prof.p) raise(SEMD_INVALID_INPUT, "no engine configured");
+        ck(cudaMemcpy(out, ctx->prof.p, 16 * 8, cudaMemcpyDeviceToHost), "prof");
+        ck(cudaMemset(ctx->prof.p, 0, 16 * 8), "prof");
     });
 }
 

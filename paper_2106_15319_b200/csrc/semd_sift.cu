@@ -443,6 +443,11 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
 // Shared layout per block, indexed by knot/row v - wa:
 //   H[v] = X[v+1]-X[v], RHS[i], DP[i], RP[i], M[i]  (X and Y only staged)
 
+// Shared arrays of the chunked solve are indexed through spad(): one pad double per
+// kSolveChunk rows, so the chains (kSolveChunk rows apart) of a warp hit distinct banks.
+__device__ __forceinline__ int spad(int q) { return q + (q >> 4); }
+static_assert(kSolveChunk == 16, "spad() pads one double per 16 rows");
+
 struct SolveCtx {
     const double* H;
     const double* RHS;
@@ -450,17 +455,17 @@ struct SolveCtx {
 };
 
 __device__ __forceinline__ void fwd_first(const SolveCtx& c, int i, double& d, double& r) {
-    const double h0 = c.H[i - 1 - c.wa], h1 = c.H[i - c.wa];
+    const double h0 = c.H[spad(i - 1 - c.wa)], h1 = c.H[spad(i - c.wa)];
     d = 2.0 * (h0 + h1);  // emd.cpp:60
-    r = c.RHS[i - c.wa];
+    r = c.RHS[spad(i - c.wa)];
 }
 
 // emd.cpp:64-69: w = h0 / diag[i-1]; diag[i] -= w*upper[i-1]; rhs[i] -= w*rhs[i-1]
 __device__ __forceinline__ void fwd_step(const SolveCtx& c, int i, double& d, double& r) {
-    const double h0 = c.H[i - 1 - c.wa], h1 = c.H[i - c.wa];
+    const double h0 = c.H[spad(i - 1 - c.wa)], h1 = c.H[spad(i - c.wa)];
     const double w = h0 / d;
     d = 2.0 * (h0 + h1) - w * h0;
-    r = c.RHS[i - c.wa] - w * r;
+    r = c.RHS[spad(i - c.wa)] - w * r;
 }
 
 struct SolveShared {
@@ -545,7 +550,18 @@ __device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) 
     tab[0] = make_double4(x0, y0, 0.0, 1.0 / (xn - x0));
 }
 
+#define SOLVE_PROF(k)                                                              \
+    do {                                                                           \
+        if (prof_on && tid == 0) {                                                 \
+            const long long now = clock64();                                       \
+            atomicAdd(&A.prof[k], (unsigned long long)(now - prof_t));             \
+            prof_t = now;                                                          \
+        }                                                                          \
+    } while (0)
+
 __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena A) {
+    const bool prof_on = (A.debug & 2) && A.prof;
+    long long prof_t = clock64();
     extern __shared__ double sm[];
     __shared__ SolveShared sh;
     Ctrl* C = A.ctrl;
@@ -603,11 +619,12 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         const int wa = max(0, ra - W0 - 1);          // staged window: every chain warms up W0 rows
         const int wb = r1e;
         const int wn = wb - wa + 1;
-        double* H = sm;          // [wn]   H[v] = X[v+1]-X[v]
-        double* RHS = H + kSolveWin;     // rhs; after the forward sweep: RN(1/diag)
-        double* DP = RHS + kSolveWin;
-        double* RP = DP + kSolveWin;
-        double* M = RP + kSolveWin;
+        double* H = sm;          // [wn]   H[spad(v)] = X[v+1]-X[v]
+        double* RHS = H + kSolvePadWin;     // rhs; after the forward sweep: RN(1/diag)
+        double* DP = RHS + kSolvePadWin;
+        double* RP = DP + kSolvePadWin;
+        double* M = RP + kSolvePadWin;
+        SOLVE_PROF(0);  // item fetch + setup
         // stage X into DP and Y into M (temporarily), then H, 1/H (into RP), RHS
         for (int q0 = 0; q0 < wn; q0 += 8 * kSolveThreads) {  // 8 independent loads in flight per thread
             int iv[8];
@@ -625,23 +642,30 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             for (int u = 0; u < 8; ++u) {
                 const int q = q0 + u * kSolveThreads + tid;
                 if (q < wn) {
-                    DP[q] = vknot_x(kv.n, wa + q, iv[u], kv.e2);
-                    M[q] = yv[u];
+                    DP[spad(q)] = vknot_x(kv.n, wa + q, iv[u], kv.e2);
+                    M[spad(q)] = yv[u];
                 }
             }
         }
         __syncthreads();
         for (int q = tid; q < wn - 1; q += blockDim.x) {
-            const double h = DP[q + 1] - DP[q];
-            H[q] = h;
-            RP[q] = 1.0 / h;
+            const double h = DP[spad(q + 1)] - DP[spad(q)];
+            H[spad(q)] = h;
+            RP[spad(q)] = 1.0 / h;
         }
         __syncthreads();
         for (int q = tid + 1; q < wn - 1; q += blockDim.x) {  // emd.cpp:62 with exactly rounded divisions
-            const double h0 = H[q - 1], h1 = H[q];
-            RHS[q] = 6.0 * (div_rn(M[q + 1] - M[q], h1, RP[q]) - div_rn(M[q] - M[q - 1], h0, RP[q - 1]));
+            const double h0 = H[spad(q - 1)], h1 = H[spad(q)];
+            RHS[spad(q)] = 6.0 * (div_rn(M[spad(q + 1)] - M[spad(q)], h1, RP[spad(q)]) - div_rn(M[spad(q)] - M[spad(q - 1)], h0, RP[spad(q - 1)]));
+            const int i = wa + q;  // this block's segment-table rows {x, y, -, 1/h}; m follows the solve
+            if (i >= r0 && i < r1) tab[i] = make_double4(DP[spad(q)], M[spad(q)], 0.0, RP[spad(q)]);
+        }
+        if (tid == 0) {
+            if (r0 == 1) tab[0] = make_double4(DP[spad(0 - wa)], M[spad(0 - wa)], 0.0, RP[spad(0 - wa)]);
+            if (r1 == N - 1) tab[N - 1] = make_double4(DP[spad(N - 1 - wa)], M[spad(N - 1 - wa)], 0.0, 0.0);
         }
         __syncthreads();
+        SOLVE_PROF(1);  // staging + H + RHS
         SolveCtx cx{H, RHS, wa};
         // Chains tile rows [ra, rb) = [r0-HW, r1+HW) (clipped to the system) in CH-row pieces:
         // the front-halo chains (rows < r0) only carry the forward state up to r0-1, the
@@ -660,32 +684,34 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             fwd_first(cx, ws, d, r);  // exact when ws == 1, otherwise a guess
             for (int i = ws + 1; i < cs; ++i) fwd_step(cx, i, d, r);
             if (ws < cs) fwd_step(cx, cs, d, r);
-            DP[cs - wa] = d;
-            RP[cs - wa] = r;
+            DP[spad(cs - wa)] = d;
+            RP[spad(cs - wa)] = r;
             for (int i = cs + 1; i < ce; ++i) {
                 fwd_step(cx, i, d, r);
-                DP[i - wa] = d;
-                RP[i - wa] = r;
+                DP[spad(i - wa)] = d;
+                RP[spad(i - wa)] = r;
             }
         }
         if (tid < kSolveMaxChains) sh.moved[tid] = 1;
         __syncthreads();
+        SOLVE_PROF(2);  // phase A
         // --- phase B: replay chain heads from the predecessor's end state until bitwise agreement
         for (int round = 0; round < nch; ++round) {
+            if (prof_on && tid == 0) atomicAdd(&A.prof[8], 1ull);
             if (tid == 0) sh.any = 0;
             if (tid < kSolveMaxChains) sh.dirty[tid] = 0;
             __syncthreads();
             if (mine && c >= 1 && sh.moved[c - 1]) {
-                double d = DP[cs - 1 - wa], r = RP[cs - 1 - wa];
+                double d = DP[spad(cs - 1 - wa)], r = RP[spad(cs - 1 - wa)];
                 bool conv = false;
                 for (int i = cs; i < ce; ++i) {
                     fwd_step(cx, i, d, r);
-                    if (d == DP[i - wa] && r == RP[i - wa]) {
+                    if (d == DP[spad(i - wa)] && r == RP[spad(i - wa)]) {
                         conv = true;
                         break;
                     }
-                    DP[i - wa] = d;
-                    RP[i - wa] = r;
+                    DP[spad(i - wa)] = d;
+                    RP[spad(i - wa)] = r;
                 }
                 if (!conv) {
                     sh.dirty[c] = 1;
@@ -698,37 +724,40 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             __syncthreads();
             if (!any) break;
         }
-        for (int q = tid + r0 - wa; q < rb - wa; q += blockDim.x) RHS[q] = 1.0 / DP[q];  // RN(1/diag)
+        SOLVE_PROF(3);  // phase B
+        for (int q = tid + r0 - wa; q < rb - wa; q += blockDim.x) RHS[spad(q)] = 1.0 / DP[spad(q)];  // RN(1/diag)
         __syncthreads();
         // --- phase C: back substitution (emd.cpp:70-73), speculative above each chunk;
         // chains below r0 take no part
-        auto upper = [&](int i) { return H[i - wa]; };  // X[i+1]-X[i]
+        auto upper = [&](int i) { return H[spad(i - wa)]; };  // X[i+1]-X[i]
         const bool back = mine && ce > r0;
         if (back) {
             const int top = min(ce + W0, rb);
             double m = 0.0;  // exact when top == N-1, otherwise a guess
             for (int i = top - 1; i >= cs; --i) {
-                m = div_rn(RP[i - wa] - upper(i) * m, DP[i - wa], RHS[i - wa]);
-                if (i < ce) M[i - wa] = m;
+                m = div_rn(RP[spad(i - wa)] - upper(i) * m, DP[spad(i - wa)], RHS[spad(i - wa)]);
+                if (i < ce) M[spad(i - wa)] = m;
             }
         }
         if (tid < kSolveMaxChains) sh.moved[tid] = 1;
         __syncthreads();
+        SOLVE_PROF(4);  // 1/diag + phase C
         // --- phase D: replay chain tails from the successor's first value
         for (int round = 0; round < nch; ++round) {
+            if (prof_on && tid == 0) atomicAdd(&A.prof[9], 1ull);
             if (tid == 0) sh.any = 0;
             if (tid < kSolveMaxChains) sh.dirty[tid] = 0;
             __syncthreads();
             if (back && c + 1 < nch && sh.moved[c + 1]) {
-                double m = M[ce - wa];
+                double m = M[spad(ce - wa)];
                 bool conv = false;
                 for (int i = ce - 1; i >= cs; --i) {
-                    m = div_rn(RP[i - wa] - upper(i) * m, DP[i - wa], RHS[i - wa]);
-                    if (m == M[i - wa]) {
+                    m = div_rn(RP[spad(i - wa)] - upper(i) * m, DP[spad(i - wa)], RHS[spad(i - wa)]);
+                    if (m == M[spad(i - wa)]) {
                         conv = true;
                         break;
                     }
-                    M[i - wa] = m;
+                    M[spad(i - wa)] = m;
                 }
                 if (!conv) {
                     sh.dirty[c] = 1;
@@ -741,35 +770,24 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             __syncthreads();
             if (!any) break;
         }
+        SOLVE_PROF(5);  // phase D
         // --- outputs + cross-block records: [0,1] forward state at r0-1 (from the front halo),
         // [2,3] this block's state at r1-1, [4] m at r0, [5] the m at r1 it used
-        // segment table rows {x, y, m, 1/h} (vknot re-reads the staged knot from L2)
-        for (int i = r0 + tid; i < r1; i += blockDim.x) {
-            double x, y;
-            vknot(kv, i, x, y);
-            tab[i] = make_double4(x, y, M[i - wa], 1.0 / H[i - wa]);
-        }
+        // the m column of this block's segment-table rows (x, y, 1/h were written with the rhs)
+        for (int i = r0 + tid; i < r1; i += blockDim.x) reinterpret_cast<double*>(tab + i)[2] = M[spad(i - wa)];
         if (tid == 0) {
-            if (r0 == 1) {
-                double x, y;
-                vknot(kv, 0, x, y);
-                tab[0] = make_double4(x, y, 0.0, 1.0 / H[0 - wa]);
-            }
-            if (r1 == N - 1) {
-                double x, y;
-                vknot(kv, N - 1, x, y);
-                tab[N - 1] = make_double4(x, y, 0.0, 0.0);
-            }
             if (r0 > 1) {
-                rec[0] = DP[r0 - 1 - wa];
-                rec[1] = RP[r0 - 1 - wa];
+                rec[0] = DP[spad(r0 - 1 - wa)];
+                rec[1] = RP[spad(r0 - 1 - wa)];
             }
-            rec[2] = DP[r1 - 1 - wa];
-            rec[3] = RP[r1 - 1 - wa];
-            rec[4] = M[r0 - wa];
-            rec[5] = r1 < N - 1 ? M[r1 - wa] : 0.0;
+            rec[2] = DP[spad(r1 - 1 - wa)];
+            rec[3] = RP[spad(r1 - 1 - wa)];
+            rec[4] = M[spad(r0 - wa)];
+            rec[5] = r1 < N - 1 ? M[spad(r1 - wa)] : 0.0;
         }
         __syncthreads();
+        SOLVE_PROF(6);  // outputs
+        if (prof_on && tid == 0) atomicAdd(&A.prof[10], 1ull);
     }
     if (tid == 0) {
         __threadfence();
@@ -1042,7 +1060,7 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
 // --------------------------------------------------------------- launchers
 
 size_t solve_smem_bytes() {
-    const size_t chunked = (size_t)5 * kSolveWin * sizeof(double);
+    const size_t chunked = (size_t)5 * kSolvePadWin * sizeof(double);
     const size_t seq = (size_t)4 * (kSolveSeqMax + 4) * sizeof(double);
     return chunked > seq ? chunked : seq;
 }

@@ -41,6 +41,7 @@ constexpr int kSolveCtasPerSm = 4;
 constexpr int kSolveMaxChains = (kSolveBlock + 2 * kSolveHalo) / kSolveChunk;  // chains tiling a block + halos
 constexpr int kSolveSeqMax = 96;                         // rows solved by one exact thread
 constexpr int kSolveWin = kSolveBlock + 2 * kSolveHalo + kSolveWarm + 4;  // staged knot window per block
+constexpr int kSolvePadWin = kSolveWin + kSolveWin / 16 + 2;               // + one pad double per 16 rows
 
 constexpr int kFinalTile = 1024;
 
@@ -156,6 +157,8 @@ struct Arena {
     int* hzlog;       // [hzlog_cap][8] solve-hazard records {m, k, iter, side, n, block, blocks, 0}
     int hzlog_cap;
     int debug;        // test hook bit 0: treat every solve block boundary as a hazard (exercise the repair)
+                      // bit 1: accumulate k_solve per-phase clock cycles into prof[]
+    unsigned long long* prof;  // [16]
     int* status_host; // mapped pinned: [0] active slots after this step, [1] step counter
 };
 
