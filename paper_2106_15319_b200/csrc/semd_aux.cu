@@ -175,6 +175,11 @@ __global__ void __launch_bounds__(64) k_signal_std(const double* x, long long n,
     if (threadIdx.x == 0) *out = scale * sqrt(acc / (double)n);
 }
 
+// out[i] = src[idx[i]] (find_extrema's values: the samples at the extrema)
+__global__ void k_gather(const int* idx, unsigned n, const double* src, double* out) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
+}
+
 // eemd finish (emd.cpp:252-260): imfs *= 1/nr ; residue = x - sum_k imf_k (k order).
 __global__ void k_ensemble_finish(double* sums, int K, long long L, const double* x, double* residue, double inv) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < L; t += (long long)gridDim.x * blockDim.x) {
@@ -363,6 +368,12 @@ void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t s
 }
 void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st) {
     k_signal_std<<<1, 64, 0, st>>>(x, n, out, scale);
+    count_launches(1);
+}
+static int grid_for(long long n);
+void launch_gather(const int* idx, unsigned n, const double* src, double* out, cudaStream_t st) {
+    if (!n) return;
+    k_gather<<<grid_for(n), 256, 0, st>>>(idx, n, src, out);
     count_launches(1);
 }
 static int grid_for(long long n) {

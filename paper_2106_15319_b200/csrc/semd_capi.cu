@@ -120,7 +120,7 @@ struct semd_ctx {
     // engine arena
     Arena A{};
     int cfg_L = -1, cfg_G = -1, cfg_kcap = -1, cfg_trace = -1;
-    DBuf bufs, kidx, kval, toff, tbase, ctot, cnum, cden, ktab, sidx, sval, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog, prof;
+    DBuf bufs, kidx, toff, tbase, ctot, cnum, cden, ktab, sidx, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog, prof;
     int* status_host = nullptr;
     int* status_host_dev = nullptr;
     std::vector<Slot> h_slots;
@@ -157,7 +157,6 @@ struct semd_ctx {
         const long long Lp = (long long)tiles * semd::dev::kEvalTile;  // whole tiles: bulk copies stay inside
         bufs.alloc((size_t)G * 3 * Lp * 8);
         kidx.alloc(((size_t)4 * G * cap + 16) * 4);
-        kval.alloc(((size_t)4 * G * cap + 16) * 8);
         const size_t t4 = ((size_t)tiles + 3) & ~(size_t)3, t4p = ((size_t)tiles + 4) & ~(size_t)3;
         const int chunks = (tiles + semd::dev::kScanChunk - 1) / semd::dev::kScanChunk;
         toff.alloc((size_t)4 * G * t4p * 4);
@@ -167,7 +166,6 @@ struct semd_ctx {
         cden.alloc((size_t)G * chunks * 8);
         ktab.alloc(((size_t)2 * G * (cap + 8) + 16) * 32);
         sidx.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 4);
-        sval.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 8);
         scnt.alloc((size_t)2 * G * t4 * 4);
         tnum.alloc((size_t)G * t4 * 8);
         tden.alloc((size_t)G * t4 * 8);
@@ -188,7 +186,6 @@ struct semd_ctx {
         A.kcap = kcap;
         A.bufs = bufs.as<double>();
         A.kidx = kidx.as<int>();
-        A.kval = kval.as<double>();
         A.toff = toff.as<unsigned>();
         A.tbase = tbase.as<unsigned>();
         A.ctot = ctot.as<unsigned>();
@@ -197,7 +194,6 @@ struct semd_ctx {
         A.chunks = chunks;
         A.ktab = ktab.as<double4>();
         A.sidx = sidx.as<int>();
-        A.sval = sval.as<double>();
         A.scnt = scnt.as<unsigned>();
         A.tnum = tnum.as<double>();
         A.tden = tden.as<double>();
@@ -402,6 +398,15 @@ struct semd_ctx {
     }
 
     double* buf(int slot, int b) { return A.bufs + semd::dev::buf_off(A, slot, b); }
+
+    // host out[i] = src[idx[i]] (extremum values: the samples at the extrema), gathered on the device
+    void gather_values(const int* d_idx, unsigned n, const double* d_src, double* out) {
+        scratch2.alloc((size_t)n * 8 + 8);
+        semd::dev::launch_gather(d_idx, n, d_src, scratch2.as<double>(), stream);
+        ck(cudaGetLastError(), "gather");
+        ck(cudaMemcpyAsync(out, scratch2.p, (size_t)n * 8, cudaMemcpyDeviceToHost, stream), "values");
+        ck(cudaStreamSynchronize(stream), "values");
+    }
 
     void fill_sums(int rows, double value) {
         // +0.0 for ensembles (the reference's Signal(n, 0.0)), -0.0 where the
@@ -1107,12 +1112,12 @@ int semd_find_extrema(semd_ctx* ctx, const double* x, size_t n, size_t* max_idx,
         if (nm) {
             ck(cudaMemcpy(idx.data(), A.kidx + semd::dev::knot_off(A, 1, 0, 0), nm * 4, cudaMemcpyDeviceToHost), "idx");
             for (unsigned i = 0; i < nm; ++i) max_idx[i] = (size_t)idx[i];
-            ck(cudaMemcpy(max_val, A.kval + semd::dev::knot_off(A, 1, 0, 0), nm * 8, cudaMemcpyDeviceToHost), "val");
+            ctx->gather_values(A.kidx + semd::dev::knot_off(A, 1, 0, 0), nm, d_x, max_val);
         }
         if (nn) {
             ck(cudaMemcpy(idx.data(), A.kidx + semd::dev::knot_off(A, 1, 1, 0), nn * 4, cudaMemcpyDeviceToHost), "idx");
             for (unsigned i = 0; i < nn; ++i) min_idx[i] = (size_t)idx[i];
-            ck(cudaMemcpy(min_val, A.kval + semd::dev::knot_off(A, 1, 1, 0), nn * 8, cudaMemcpyDeviceToHost), "val");
+            ctx->gather_values(A.kidx + semd::dev::knot_off(A, 1, 1, 0), nn, d_x, min_val);
         }
         *n_max = nm;
         *n_min = nn;

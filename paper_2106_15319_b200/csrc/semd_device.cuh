@@ -48,7 +48,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 // the extrema, n+2 and n+3 the (non-monotone) right mirrors.
 struct KnotView {
     const int* idx;
-    const double* val;
+    const double* src;  // the samples the extrema were found in: value of extremum r = src[idx[r]]
     const double* mom;
     int n;
     double e2;  // 2*(L-1)
@@ -71,7 +71,7 @@ __device__ __forceinline__ void vknot(const KnotView& kv, int v, double& X, doub
     const int r = vknot_rank(kv.n, v);
     const int i = kv.idx[r];
     X = vknot_x(kv.n, v, i, kv.e2);
-    Y = kv.val[r];
+    Y = kv.src[i];
 }
 
 // emd.cpp:80-85 verbatim (IEEE divisions): reference-order evaluation of one segment.

@@ -406,12 +406,10 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         for (int k = 0; k < kSpt; ++k) {
             if (fmax & (1u << k)) {
                 A.sidx[o + omax] = t0 - 1 + k;
-                A.sval[o + omax] = w[k + 1];
                 ++omax;
             }
             if (fmin & (1u << k)) {
                 A.sidx[side1 + o + omin] = t0 - 1 + k;
-                A.sval[side1 + o + omin] = w[k + 1];
                 ++omin;
             }
         }

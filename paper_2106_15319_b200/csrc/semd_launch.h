@@ -44,6 +44,7 @@ void launch_envelope_knots(const unsigned long long* idx, const double* val, lon
                            double* xs, double* ys, cudaStream_t st);
 void launch_fill(double* p, long long n, double v, cudaStream_t st);
 void launch_copy(const double* src, double* dst, long long n, cudaStream_t st);
+void launch_gather(const int* idx, unsigned n, const double* src, double* out, cudaStream_t st);
 void launch_axpy(const double* a, const double* b, double beta, double* out, long long n, cudaStream_t st);
 
 }  // namespace dev

@@ -380,9 +380,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
             off = toff_view(A, cpar, side, s)[j0 + lane];
         }
         const int* si = A.sidx + stage_off(A, side, s) + (size_t)j0 * kTileKnots;
-        const double* sv = A.sval + stage_off(A, side, s) + (size_t)j0 * kTileKnots;
         int* gi = A.kidx + knot_off(A, cpar, side, s);
-        double* gv = A.kval + knot_off(A, cpar, side, s);
         uint64_t h = 0;
         for (int u = 0; u < nt; ++u) {
             const unsigned cu = __shfl_sync(0xffffffffu, cnt, u);
@@ -390,7 +388,6 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
             for (unsigned i = lane; i < cu; i += 32) {
                 const int t = si[u * kTileKnots + i];
                 gi[ou + i] = t;
-                gv[ou + i] = sv[u * kTileKnots + i];
                 if (tracing) h += knot_hash(side, ou + i, (unsigned)t);
             }
         }
@@ -600,7 +597,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         const Slot& S = A.slots[slot];
         KnotView kv;
         kv.idx = A.kidx + knot_off(A, S.par, side, slot);
-        kv.val = A.kval + knot_off(A, S.par, side, slot);
+        kv.src = A.bufs + buf_off(A, slot, S.cb >= 0 ? S.cb : S.xb);
         kv.n = (int)S.n[side];
         kv.e2 = 2.0 * (double)(A.L - 1);
         kv.mom = nullptr;
@@ -626,21 +623,23 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         double* M = RP + kSolvePadWin;
         SOLVE_PROF(0);  // item fetch + setup
         // stage X into DP and Y into M (temporarily), then H, 1/H (into RP), RHS
-        for (int q0 = 0; q0 < wn; q0 += 8 * kSolveThreads) {  // 8 independent loads in flight per thread
-            int iv[8];
-            double yv[8];
+        {  // every row of the window in one batch: the index loads, then the value gathers
+            constexpr int U = (kSolveWin + kSolveThreads - 1) / kSolveThreads;
+            int iv[U];
+            double yv[U];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int q = q0 + u * kSolveThreads + tid;
-                if (q < wn) {
-                    const int r = vknot_rank(kv.n, wa + q);
-                    iv[u] = kv.idx[r];
-                    yv[u] = kv.val[r];
-                }
+            for (int u = 0; u < U; ++u) {
+                const int q = u * kSolveThreads + tid;
+                if (q < wn) iv[u] = kv.idx[vknot_rank(kv.n, wa + q)];
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int q = q0 + u * kSolveThreads + tid;
+            for (int u = 0; u < U; ++u) {
+                const int q = u * kSolveThreads + tid;
+                if (q < wn) yv[u] = kv.src[iv[u]];  // extremum value = the candidate sample
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = u * kSolveThreads + tid;
                 if (q < wn) {
                     DP[spad(q)] = vknot_x(kv.n, wa + q, iv[u], kv.e2);
                     M[spad(q)] = yv[u];
@@ -832,7 +831,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             const Slot& S = A.slots[slot];
             KnotView kv;
             kv.idx = A.kidx + knot_off(A, S.par, side, slot);
-            kv.val = A.kval + knot_off(A, S.par, side, slot);
+            kv.src = A.bufs + buf_off(A, slot, S.cb >= 0 ? S.cb : S.xb);
             kv.n = (int)S.n[side];
             kv.e2 = 2.0 * (double)(A.L - 1);
             kv.mom = nullptr;

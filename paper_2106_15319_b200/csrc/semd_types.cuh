@@ -8,10 +8,10 @@
 //
 // HBM layout per engine (L = serialized length, G = slots, T = eval tile):
 //   bufs    f64 [G][3][L]        rotating X (IMF input), C (candidate), R (next residue)
-//   sidx/sval  [2 side][G][tiles*T/2]     tile-local extrema found by k_eval (stage)
+//   sidx    i32 [2 side][G][tiles*T/2]    tile-local extrema found by k_eval (stage)
 //   scnt    u32 [2 side][G][tiles]        extrema per tile
 //   kidx    i32 [2 par][2 side][G][cap]   compacted extrema indices (cap = L/2+2)
-//   kval    f64 [2][2][G][cap]            extrema values
+//   (extremum values are not stored: value r = candidate[idx[r]], gathered by k_solve)
 //   toff    u32 [2][2][G][tiles+1]        per-tile knot offsets, local to a scan chunk
 //   tbase   u32 [2][2][G][chunks]         knot offset of each scan chunk (toff_at adds it)
 //   ctot/cnum/cden [2 side][G][chunks]    per-chunk extrema totals and SD partials
@@ -128,7 +128,6 @@ struct Arena {
     int trace_cap;
     double* bufs;
     int* kidx;
-    double* kval;
     unsigned* toff;
     unsigned* tbase;
     unsigned* ctot;
@@ -137,7 +136,6 @@ struct Arena {
     int chunks;  // scan chunks per (slot, side): ceil(tiles / kScanChunk)
     double4* ktab;
     int* sidx;
-    double* sval;
     unsigned* scnt;
     double* tnum;
     double* tden;
