@@ -283,6 +283,7 @@ struct semd_ctx {
         ck(cudaMemcpyAsync(A.slots, h_slots.data(), (size_t)G * sizeof(Slot), cudaMemcpyHostToDevice, stream),
            "upload slots");
         Ctrl c{};
+        c.ev_t0 = ~0ull;
         std::vector<int> el;
         for (int s = 0; s < (int)jobs.size() && s < G; ++s) el.push_back(s);
         c.n_eval = (int)el.size();
@@ -292,45 +293,36 @@ struct semd_ctx {
             ck(cudaMemcpyAsync(A.eval_list, el.data(), el.size() * 4, cudaMemcpyHostToDevice, stream), "lists");
         ck(cudaMemsetAsync(A.solve_off, 0, 4, stream), "lists");
         ck(cudaStreamSynchronize(stream), "sync");  // h_slots / el are reused by the caller
+        status_host[1] = 0;
         *(volatile int*)status_host = c.active;
     }
 
-    // per-step sift-kernel events (timing mode): a ring, harvested every R steps
-    std::vector<cudaEvent_t> tev;
-    void harvest(int from, int to) {  // accumulate eval durations of steps [from, to)
-        for (int s = from; s < to; ++s) {
-            float ms = 0.f;
-            const int i = (s % kTimedRing) * 2;
-            ck(cudaEventSynchronize(tev[i + 1]), "timing event");
-            ck(cudaEventElapsedTime(&ms, tev[i], tev[i + 1]), "timing");
-            stats.eval_ms += ms;
+    // Block until the device has completed `target` steps of this run (the last CTA of
+    // k_final publishes {active slots, completed steps} to mapped pinned memory). No
+    // per-step events: they would break the programmatic-dependent-launch chain.
+    void wait_steps(int target) {
+        volatile int* hs = status_host;
+        for (unsigned spin = 0; hs[1] < target; ++spin) {
+            if ((spin & 1023u) == 1023u) {
+                const cudaError_t e = cudaStreamQuery(stream);
+                if (e == cudaSuccess) {  // drained: the counter is final
+                    if (hs[1] < target) break;
+                } else if (e != cudaErrorNotReady) {
+                    ck(e, "engine step");
+                }
+            }
         }
     }
-    static constexpr int kTimedRing = 64;
 
     void run(int max_steps) {
-        const int LAG = 3, R = 16;
-        int step = 0, harvested = 0;
-        if (timing && tev.empty()) {
-            tev.resize(2 * kTimedRing);
-            for (auto& e : tev) ck(cudaEventCreate(&e), "event");
-        }
+        const int LAG = 3;
+        int step = 0;
         for (;; ++step) {
-            cudaEvent_t eb = nullptr, ee = nullptr;
-            if (timing) {
-                if (step - harvested >= kTimedRing - 1) {
-                    harvest(harvested, step - LAG);
-                    harvested = step - LAG;
-                }
-                eb = tev[(step % kTimedRing) * 2];
-                ee = tev[(step % kTimedRing) * 2 + 1];
-            }
-            semd::dev::launch_step(A, sms, stream, eb, ee);
+            semd::dev::launch_step(A, sms, stream);
             stats.eval_launches += 1;
             ck(cudaGetLastError(), "launch step");
-            ck(cudaEventRecord(ev[step % R], stream), "event record");
             if (step >= LAG) {
-                ck(cudaEventSynchronize(ev[(step - LAG) % R]), "step");
+                wait_steps(step - LAG + 1);
                 if (*(volatile int*)status_host == 0) break;
             }
             if (step > max_steps) {
@@ -350,7 +342,6 @@ struct semd_ctx {
             }
         }
         ck(cudaStreamSynchronize(stream), "engine run");
-        if (timing) harvest(harvested, step + 1);
         stats.steps += step + 1;
         ck(cudaMemcpy(h_slots.data(), A.slots, (size_t)A.G * sizeof(Slot), cudaMemcpyDeviceToHost), "download slots");
         Ctrl c{};
@@ -360,6 +351,7 @@ struct semd_ctx {
             stats.sift_iterations += (uint64_t)(S.sifted / std::max(1, A.L));
         }
         stats.solve_hazards += (uint64_t)c.hazards;
+        if (timing) stats.eval_ms += (double)c.ev_ns * 1e-6;
         if (c.hz_count > 0) {
             const int n = std::min(c.hz_count, kHzCap);
             const size_t old = h_hz.size();
@@ -377,6 +369,7 @@ struct semd_ctx {
         }
         // reset counters for the next run
         Ctrl z{};
+        z.ev_t0 = ~0ull;
         ck(cudaMemcpyAsync(A.ctrl, &z, sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
     }
     long long trace_total = 0;

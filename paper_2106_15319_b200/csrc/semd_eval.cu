@@ -424,8 +424,16 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
 // Warp-level software pipeline: tile i is computed while the bulk copies of tile
 // i+1 are in flight. SD partials are summed per lane over the strip and reduced
 // once per strip (tnum/tden are indexed by strip).
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char eval_smem[];
+    if (threadIdx.x == 0) atomicMin(&A.ctrl->ev_t0, globaltimer());
     const int lane = threadIdx.x & 31;
     WarpStage* stage = reinterpret_cast<WarpStage*>(eval_smem) + 2 * (threadIdx.x >> 5);
     const unsigned strips = ((unsigned)A.tiles + kStripTiles - 1) / kStripTiles;
@@ -471,6 +479,8 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
         }
         item = __shfl_sync(0xffffffffu, next, 0);
     }
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&A.ctrl->ev_t1, globaltimer());
 }
 
 size_t eval_smem_bytes() { return sizeof(WarpStage) * 2 * (kEvalThreads / 32); }
@@ -479,7 +489,17 @@ cudaError_t eval_setup() {
 }
 
 void launch_eval(const Arena& A, int sms, cudaStream_t st) {
-    k_eval<<<sms * 2, kEvalThreads, eval_smem_bytes(), st>>>(A);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(sms * 2));
+    cfg.blockDim = dim3((unsigned)kEvalThreads);
+    cfg.dynamicSmemBytes = eval_smem_bytes();
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_eval, A);
 }
 
 }  // namespace dev

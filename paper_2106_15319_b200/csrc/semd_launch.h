@@ -20,8 +20,9 @@ cudaError_t eval_setup();
 void launch_eval(const Arena& A, int sms, cudaStream_t st);
 size_t solve_smem_bytes();
 cudaError_t launch_setup();
-void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begin = nullptr,
-                 cudaEvent_t eval_end = nullptr);
+void launch_step(const Arena& A, int sms, cudaStream_t st);
+// programmatic dependent launch of the step kernels (default on; SEMD_PDL=0 disables)
+bool pdl_enabled();
 unsigned long long launch_count();  // kernels launched by this library (all contexts)
 void count_launches(int n);
 void launch_rng(const RngJob* jobs, int njobs, cudaStream_t st);

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "semd_device.cuh"
 #include "semd_launch.h"
@@ -235,6 +236,7 @@ __device__ void decide_after_eval(const Arena& A) {
 // (side 0) the chunk's SD partials. The last CTA scans the chunk totals into
 // tbase and applies extract_imf's control flow.
 __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
+    pdl_begin();
     constexpr int W = kScanThreads / 32;
     __shared__ unsigned s_w[W];
     __shared__ double s_red[2][W];
@@ -328,6 +330,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
         if (tid == 0) {
             C->done[4] = 0;
             C->ticket[0] = 0;  // k_eval's strip tickets
+            if (C->ev_t1 > C->ev_t0) C->ev_ns += C->ev_t1 - C->ev_t0;
+            C->ev_t0 = ~0ull;
+            C->ev_t1 = 0;
         }
     }
 }
@@ -358,6 +363,7 @@ __device__ void emit_trace(const Arena& A, const Slot& S, uint64_t h) {
 constexpr int kCompactThreads = 128;
 constexpr int kCompactStrip = 16;
 __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
+    pdl_begin();
     __shared__ int s_last;
     Ctrl* C = A.ctrl;
     const int lane = threadIdx.x & 31;
@@ -557,6 +563,7 @@ __device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) 
     } while (0)
 
 __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena A) {
+    pdl_begin();
     const bool prof_on = (A.debug & 2) && A.prof;
     long long prof_t = clock64();
     extern __shared__ double sm[];
@@ -932,11 +939,13 @@ __device__ void decide_after_final(const Arena& A) {
         C->step += 1;
         volatile int* hs = A.status_host;
         hs[0] = C->active;
+        __threadfence_system();  // the host reads the step counter, then `active`
         hs[1] = C->step;
     }
 }
 
 __global__ void __launch_bounds__(256) k_final(Arena A) {
+    pdl_begin();
     __shared__ unsigned s_ticket;
     __shared__ int s_last;
     __shared__ FinalSlot tab[kFinalChunk];
@@ -1074,14 +1083,35 @@ static unsigned long long g_launches = 0;
 unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 void count_launches(int n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
 
-void launch_step(const Arena& A, int sms, cudaStream_t st, cudaEvent_t eval_begin, cudaEvent_t eval_end) {
-    k_solve<<<kSolveCtasPerSm * sms, kSolveThreads, solve_smem_bytes(), st>>>(A);
-    if (eval_begin) cudaEventRecord(eval_begin, st);
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SEMD_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename Kernel>
+static void launch_pdl(Kernel kernel, int grid, int block, size_t smem, cudaStream_t st, const Arena& A) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, A);
+}
+
+void launch_step(const Arena& A, int sms, cudaStream_t st) {
+    launch_pdl(k_solve, kSolveCtasPerSm * sms, kSolveThreads, solve_smem_bytes(), st, A);
     launch_eval(A, sms, st);
-    if (eval_end) cudaEventRecord(eval_end, st);
-    k_scan<<<2 * A.G * A.chunks, kScanThreads, 0, st>>>(A);
-    k_compact<<<sms * 8, kCompactThreads, 0, st>>>(A);
-    k_final<<<2 * sms, 256, 0, st>>>(A);
+    launch_pdl(k_scan, 2 * A.G * A.chunks, kScanThreads, 0, st, A);
+    launch_pdl(k_compact, sms * 8, kCompactThreads, 0, st, A);
+    launch_pdl(k_final, 2 * sms, 256, 0, st, A);
     count_launches(5);
 }
 

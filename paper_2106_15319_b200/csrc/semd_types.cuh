@@ -118,7 +118,20 @@ struct Ctrl {
     int step;
     int hz_count;  // hazard log records produced
     int pad[5];
+    unsigned long long ev_t0;  // k_eval span of this step (globaltimer): min CTA start, max CTA end
+    unsigned long long ev_t1;
+    unsigned long long ev_ns;  // accumulated k_eval spans of this run (timing mode)
 };
+
+// Programmatic dependent launch: every step kernel starts with pdl_begin(): the grid
+// may be launched while its predecessor drains (launch latency and ramp overlap the
+// tail); griddepcontrol.wait then holds it until the predecessor completed and its
+// memory is visible. The trigger lets this grid's successor launch once all of this
+// grid's CTAs have started. Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 struct Arena {
     int L, G, tiles, cap, kcap;
