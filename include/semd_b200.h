@@ -168,6 +168,17 @@ int semd_serial_decompose_device(semd_ctx* ctx, int algo, const double* d_x, siz
                                  const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* d_tensor,
                                  size_t k_cap, size_t* modes_out);
 
+/* baseline.hpp / baseline.cpp:5-29 slicewise_decompose: each channel of the channel-contiguous
+ * M x N multi-signal decomposed independently; the ImfTensor (k*N + j)*M + i holds each channel's
+ * IMFs zero-padded to a common mode count, residue last. EMD and EEMD run all channels (x all
+ * realizations) as one batched engine pass. *modes_out = common mode count (SEMD_CAPACITY and
+ * the needed count when it exceeds k_cap). */
+int semd_slicewise_decompose(semd_ctx* ctx, int algo, const double* x, size_t M, size_t N, const semd_sift_cfg* cfg,
+                             const semd_ens_cfg* ens, double* tensor, size_t k_cap, size_t* modes_out);
+int semd_slicewise_decompose_device(semd_ctx* ctx, int algo, const double* d_x, size_t M, size_t N,
+                                    const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* d_tensor,
+                                    size_t k_cap, size_t* modes_out);
+
 /* ---- CEEMDAN across GPUs: stages over a realization shard (emd.cpp:264-344) ----------
  * Rank r owns realizations [m_begin, m_end) (seeds from the global index). Driver loop:
  *   begin; stage(partial); all-reduce(partial) -> total; finish_stage(total, nr, 0, ...);

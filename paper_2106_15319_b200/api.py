@@ -340,18 +340,27 @@ def serial_decompose(x, d: int, algo="emd", sd_threshold=0.2, max_sift_iters=300
     return serial_decompose_full(x, d, algo, sd_threshold, max_sift_iters, max_imfs, nstd, nr, seed)[0]
 
 
-def slicewise_decompose(x, algo="emd", sd_threshold=0.2, max_sift_iters=300, max_imfs=0, nstd=0.2, nr=100, seed=0):
-    """baseline.cpp:5-29: each channel decomposed independently, zero-padded to a common K."""
-    a = _f64(x, 2)
-    M, Nc = a.shape
+def slicewise_decompose(x, algo="emd", sd_threshold=0.2, max_sift_iters=300, max_imfs=0, nstd=0.2, nr=100, seed=0,
+                        device: int = 0):
+    """baseline.cpp:5-29: each channel of the (M, N) multi-signal decomposed independently; returns the
+    (M, N, K) tensor (IMFs zero-padded to a common count, residue last). EMD / EEMD run every channel
+    (x every realization) as one batched engine pass on the GPU."""
+    c = context(device)
+    cm, M, Nc = _channel_major(x)
     if M == 0 or Nc == 0:
         raise InvalidInput("slicewise_decompose: empty input")
-    per = [decompose(a[:, j], algo, sd_threshold, max_sift_iters, max_imfs, nstd, nr, seed) for j in range(Nc)]
-    common = max(1, max(p["imfs"].shape[0] + 1 for p in per))
-    t = np.zeros((M, Nc, common))
-    for j, p in enumerate(per):
-        k = p["imfs"].shape[0]
-        if k:
-            t[:, j, :k] = p["imfs"].T
-        t[:, j, common - 1] = p["residue"]
-    return t
+    a = _algo(algo)
+    cfg, ens = _cfgs(sd_threshold, max_sift_iters, max_imfs, nstd, nr, seed)
+    k_cap = (max_imfs + 1) if max_imfs else 33
+    while True:
+        t = np.zeros(max(k_cap * M * Nc, 1))
+        mo = C.c_size_t()
+        rc = c.lib.semd_slicewise_decompose(c.ptr, a, _dp(cm), M, Nc, C.byref(cfg), C.byref(ens), _dp(t), k_cap,
+                                            C.byref(mo))
+        if rc == N.SEMD_CAPACITY and mo.value > k_cap:
+            k_cap = int(mo.value)
+            continue
+        c.check(rc)
+        break
+    K1 = int(mo.value)
+    return t[:K1 * M * Nc].reshape(K1, Nc, M).transpose(2, 1, 0).copy()

@@ -175,6 +175,59 @@ __global__ void __launch_bounds__(64) k_signal_std(const double* x, long long n,
     if (threadIdx.x == 0) *out = scale * sqrt(acc / (double)n);
 }
 
+// signal_std of B signals of length n (row b contiguous), one thread per signal:
+// emd.cpp:209-217's two sequential passes verbatim; out[b] = scale * std(x_b).
+__global__ void k_signal_std_batch(const double* x, long long n, int B, double* out, double scale) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const double* v = x + (size_t)b * n;
+    if (n == 0) {
+        out[b] = 0.0;
+        return;
+    }
+    double mean = 0.0;
+    for (long long i = 0; i < n; ++i) mean += v[i];
+    mean /= (double)n;
+    double acc = 0.0;
+    for (long long i = 0; i < n; ++i) acc += (v[i] - mean) * (v[i] - mean);
+    out[b] = scale * sqrt(acc / (double)n);
+}
+
+// slicewise tensor (baseline.cpp:17-27, layout types.hpp:105-110): mode k of channel j at
+// (k*N + j)*M + i; IMF rows k < K_j from sums row j*kc + k (scaled by `scale`), the residue
+// at k = common-1, zeros in between.
+__global__ void k_slicewise_tensor(const double* sums, int kc, const int* kj, const double* res, long long M, int N,
+                                   int common, double scale, int scaled, double* out) {
+    const long long total = (long long)common * N * M;
+    for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < total;
+         o += (long long)gridDim.x * blockDim.x) {
+        const long long i = o % M;
+        const long long kjn = o / M;
+        const int j = (int)(kjn % N), k = (int)(kjn / N);
+        double v = 0.0;
+        if (k == common - 1) v = res[(size_t)j * M + i];
+        else if (k < kj[j]) {
+            v = sums[((size_t)j * kc + k) * M + i];
+            if (scaled) v *= scale;
+        }
+        out[o] = v;
+    }
+}
+
+// EEMD residue per channel: res = x - sum_k (sums_k * inv) over the channel's kc rows
+// (emd.cpp:252-260; rows beyond K_j are +0.0 and leave every value unchanged)
+__global__ void k_slicewise_finish(const double* x, const double* sums, int kc, long long M, int N, double inv,
+                                   double* res) {
+    const long long total = (long long)N * M;
+    for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < total;
+         o += (long long)gridDim.x * blockDim.x) {
+        const long long j = o / M, i = o % M;
+        double r = x[o];
+        for (int k = 0; k < kc; ++k) r -= sums[((size_t)j * kc + k) * M + i] * inv;
+        res[o] = r;
+    }
+}
+
 // out[i] = src[idx[i]] (find_extrema's values: the samples at the extrema)
 __global__ void k_gather(const int* idx, unsigned n, const double* src, double* out) {
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
@@ -371,6 +424,21 @@ void launch_signal_std(const double* x, long long n, double* out, double scale, 
     count_launches(1);
 }
 static int grid_for(long long n);
+void launch_signal_std_batch(const double* x, long long n, int B, double* out, double scale, cudaStream_t st) {
+    k_signal_std_batch<<<(B + 127) / 128, 128, 0, st>>>(x, n, B, out, scale);
+    count_launches(1);
+}
+void launch_slicewise_tensor(const double* sums, int kc, const int* kj, const double* res, long long M, int N,
+                             int common, double scale, int scaled, double* out, cudaStream_t st) {
+    k_slicewise_tensor<<<grid_for((long long)common * N * M), 256, 0, st>>>(sums, kc, kj, res, M, N, common, scale,
+                                                                           scaled, out);
+    count_launches(1);
+}
+void launch_slicewise_finish(const double* x, const double* sums, int kc, long long M, int N, double inv, double* res,
+                             cudaStream_t st) {
+    k_slicewise_finish<<<grid_for((long long)N * M), 256, 0, st>>>(x, sums, kc, M, N, inv, res);
+    count_launches(1);
+}
 void launch_gather(const int* idx, unsigned n, const double* src, double* out, cudaStream_t st) {
     if (!n) return;
     k_gather<<<grid_for(n), 256, 0, st>>>(idx, n, src, out);

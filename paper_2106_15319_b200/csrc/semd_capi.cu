@@ -149,6 +149,7 @@ struct semd_ctx {
     // ---- arena --------------------------------------------------------------
     void configure(long long L, int G, int kcap, int trace_cap) {
         if (L >= (1LL << 30)) raise(SEMD_INVALID_INPUT, "signal too long for the engine (%lld samples)", L);
+        A.kper = 0;  // batched drivers set it after configuring
         if (L == cfg_L && G == cfg_G && kcap == cfg_kcap && trace_cap == cfg_trace) return;
         const int tiles = (int)((L + semd::dev::kEvalTile - 1) / semd::dev::kEvalTile);
         const int cap = (int)((L / 2 + 2 + 3) / 4 * 4);  // 16-byte aligned knot rows (bulk TMA staging)
@@ -763,6 +764,121 @@ struct semd_ctx {
         if (out_res) ck(cudaMemcpyAsync(out_res, cs_residue(), n * 8, cudaMemcpyDeviceToDevice, stream), "residue");
         ck(cudaStreamSynchronize(stream), "ceemdan");
         return K;
+    }
+
+    // ---- slicewise_decompose (baseline.cpp:5-29) on N same-length channels ----------------
+    // EMD / EEMD: every channel (EEMD: channel x realization, channel-major) is a job of ONE
+    // batched engine run; job j owns IMF rows [j*kc, (j+1)*kc). CEEMDAN: channel by channel.
+    DBuf sl_imfs, sl_res, sl_kj, sl_beta;
+    void slicewise_device(int algo, const double* d_x, long long M, int N, const semd_sift_cfg& cfg,
+                          const semd_ens_cfg& ens, double* d_tensor, size_t cap_modes, size_t* modes_out) {
+        if (M == 0 || N == 0) raise(SEMD_INVALID_INPUT, "slicewise_decompose: empty input");
+        if (algo != SEMD_ALGO_EMD) {  // emd.cpp:223-226, :229-230, :266-267
+            if (ens.nr < 1) raise(SEMD_INVALID_INPUT, "ensemble: nr must be at least 1");
+            if (ens.nstd < 0.0) raise(SEMD_INVALID_INPUT, "ensemble: nstd must be non-negative");
+            if (ens.nstd == 0.0) algo = SEMD_ALGO_EMD;
+        }
+        if (M < 4)
+            raise(SEMD_INVALID_INPUT, algo == SEMD_ALGO_CEEMDAN ? "ceemdan: signal too short (need at least 4 samples)"
+                                                               : "emd: signal too short (need at least 4 samples)");
+        std::vector<int> kj(N, 0);
+        int kc = default_kcap(M, cfg.max_imfs);
+        sl_res.alloc((size_t)N * M * 8);
+        double* res = sl_res.as<double>();
+        const double* imf_rows = nullptr;  // [N][kc][M]
+        bool scaled = false;
+        if (algo == SEMD_ALGO_CEEMDAN) {
+            sl_imfs.alloc((size_t)N * kc * M * 8);
+            for (int j = 0; j < N; ++j) {
+                int need = 0;
+                const int K = ceemdan_device(d_x + (size_t)j * M, M, cfg, ens, sl_imfs.as<double>() + (size_t)j * kc * M,
+                                             kc, res + (size_t)j * M, nullptr, &need);
+                if (K > kc) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", kc);
+                kj[j] = K;
+            }
+            imf_rows = sl_imfs.as<double>();
+        } else {
+            const bool ens_mode = algo == SEMD_ALGO_EEMD;
+            const int nr = ens_mode ? ens.nr : 1;
+            const long long Ls = (M + 1) / 2 * 2;
+            std::vector<double> beta(N, 0.0);
+            if (ens_mode) {  // beta_j = nstd * std(x_j) (emd.cpp:233), exact sequential sums per channel
+                sl_beta.alloc((size_t)N * 8);
+                semd::dev::launch_signal_std_batch(d_x, M, N, sl_beta.as<double>(), ens.nstd, stream);
+                ck(cudaMemcpyAsync(beta.data(), sl_beta.p, (size_t)N * 8, cudaMemcpyDeviceToHost, stream), "betas");
+                noise.alloc((size_t)nr * Ls * 8);  // w_m, shared by every channel (emd.cpp:238)
+                for (int m0 = 0; m0 < nr; m0 += 1024) {
+                    const int g = std::min(1024, nr - m0);
+                    std::vector<uint64_t> seeds(g);
+                    for (int i = 0; i < g; ++i) seeds[i] = derive_seed(ens.base_seed, (uint64_t)(m0 + i));
+                    gen_noise(seeds, M, Ls, noise.as<double>() + (size_t)m0 * Ls);
+                }
+            }
+            const long long jobs = (long long)N * nr;
+            for (int attempt = 0;; ++attempt) {
+                const int G = auto_slots(M, (int)std::min<long long>(jobs, 1 << 20));
+                if ((long long)N * kc * M * 8 > (1LL << 40)) raise(SEMD_NO_MEMORY, "slicewise IMF store too large");
+                configure(M, G, N * kc, 0);
+                A.kper = kc;
+                A.sd_threshold = cfg.sd_threshold;
+                A.max_sift_iters = cfg.max_sift_iters;
+                fill_sums(N * kc, ens_mode ? 0.0 : -0.0);
+                if (!ens_mode)  // channels without IMFs keep x as residue; k_final overwrites the rest
+                    ck(cudaMemcpyAsync(res, d_x, (size_t)N * M * 8, cudaMemcpyDeviceToDevice, stream), "res");
+                std::fill(kj.begin(), kj.end(), 0);
+                try {
+                    for (long long w0 = 0; w0 < jobs; w0 += G) {
+                        const int g = (int)std::min<long long>(G, jobs - w0);
+                        std::vector<JobSpec> js(g);
+                        for (int i = 0; i < g; ++i) {
+                            const long long q = w0 + i;
+                            const int j = (int)(q / nr), m = (int)(q % nr);
+                            JobSpec& J = js[i];
+                            J.m = ens_mode ? m : j;
+                            J.task = 0;
+                            J.kmax = cfg.max_imfs;
+                            J.k0 = j * kc;
+                            J.a = d_x + (size_t)j * M;
+                            if (ens_mode) {
+                                J.init_kind = 1;
+                                J.beta = beta[j];
+                                J.b = noise.as<double>() + (size_t)m * Ls;
+                            } else {
+                                J.res_out = res + (size_t)j * M;
+                            }
+                        }
+                        set_jobs(js);
+                        run(max_steps_for(cfg));
+                        for (int i = 0; i < g; ++i) {
+                            const int j = (int)((w0 + i) / nr);
+                            kj[j] = std::max(kj[j], h_slots[i].k);
+                        }
+                    }
+                } catch (const Error& e) {
+                    A.kper = 0;
+                    if (e.code == SEMD_CAPACITY && attempt < 3 && cfg.max_imfs == 0) {
+                        kc *= 2;
+                        continue;
+                    }
+                    throw;
+                }
+                A.kper = 0;
+                break;
+            }
+            if (ens_mode) semd::dev::launch_slicewise_finish(d_x, A.sums, kc, M, N, 1.0 / (double)nr, res, stream);
+            imf_rows = A.sums;
+            scaled = ens_mode;
+        }
+        int common = 1;
+        for (int j = 0; j < N; ++j) common = std::max(common, kj[j] + 1);
+        *modes_out = (size_t)common;
+        if ((size_t)common > cap_modes) raise(SEMD_CAPACITY, "output holds %zu modes, decomposition has %d", cap_modes, common);
+        sl_kj.alloc((size_t)N * 4);
+        ck(cudaMemcpyAsync(sl_kj.p, kj.data(), (size_t)N * 4, cudaMemcpyHostToDevice, stream), "kj");
+        semd::dev::launch_slicewise_tensor(imf_rows, kc, sl_kj.as<int>(), res, M, N, common,
+                                           scaled ? 1.0 / (double)ens.nr : 1.0, scaled ? 1 : 0, d_tensor, stream);
+        ck(cudaGetLastError(), "slicewise");
+        ck(cudaStreamSynchronize(stream), "slicewise");
     }
 
     // Full decomposition with device buffers. Returns K via *k_out; SEMD_CAPACITY if K > k_cap.
@@ -1418,6 +1534,49 @@ int semd_serial_decompose_device(semd_ctx* ctx, int algo, const double* d_x, siz
         size_t mo = 0;
         try {
             serial_device(ctx, algo, d_x, M, N, D, cfg, ens, d_tensor, k_cap, &mo, nullptr);
+        } catch (...) {
+            if (modes_out) *modes_out = mo;
+            throw;
+        }
+        if (modes_out) *modes_out = mo;
+    });
+}
+
+int semd_slicewise_decompose(semd_ctx* ctx, int algo, const double* x, size_t M, size_t N, const semd_sift_cfg* cfg_,
+                             const semd_ens_cfg* ens_, double* tensor, size_t k_cap, size_t* modes_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (algo < 0 || algo > 2) raise(SEMD_INVALID_INPUT, "unknown algorithm");
+        if (M == 0 || N == 0) raise(SEMD_INVALID_INPUT, "slicewise_decompose: empty input");
+        const semd_sift_cfg cfg = sift_or_default(cfg_);
+        const semd_ens_cfg ens = ens_or_default(ens_);
+        const double* d_x = ctx->upload(ctx->in_x, x, M * N);
+        ctx->reset_stats(1);
+        DBuf t(std::max<size_t>(k_cap, 1) * M * N * 8);
+        size_t mo = 0;
+        try {
+            ctx->slicewise_device(algo, d_x, (long long)M, (int)N, cfg, ens, t.as<double>(), k_cap, &mo);
+        } catch (...) {
+            if (modes_out) *modes_out = mo;
+            throw;
+        }
+        if (modes_out) *modes_out = mo;
+        ctx->download(tensor, t.as<double>(), mo * M * N);
+    });
+}
+
+int semd_slicewise_decompose_device(semd_ctx* ctx, int algo, const double* d_x, size_t M, size_t N,
+                                    const semd_sift_cfg* cfg_, const semd_ens_cfg* ens_, double* d_tensor,
+                                    size_t k_cap, size_t* modes_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (algo < 0 || algo > 2) raise(SEMD_INVALID_INPUT, "unknown algorithm");
+        const semd_sift_cfg cfg = sift_or_default(cfg_);
+        const semd_ens_cfg ens = ens_or_default(ens_);
+        ctx->reset_stats(1);
+        size_t mo = 0;
+        try {
+            ctx->slicewise_device(algo, d_x, (long long)M, (int)N, cfg, ens, d_tensor, k_cap, &mo);
         } catch (...) {
             if (modes_out) *modes_out = mo;
             throw;

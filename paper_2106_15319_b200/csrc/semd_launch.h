@@ -46,6 +46,11 @@ void launch_envelope_knots(const unsigned long long* idx, const double* val, lon
 void launch_fill(double* p, long long n, double v, cudaStream_t st);
 void launch_copy(const double* src, double* dst, long long n, cudaStream_t st);
 void launch_gather(const int* idx, unsigned n, const double* src, double* out, cudaStream_t st);
+void launch_signal_std_batch(const double* x, long long n, int B, double* out, double scale, cudaStream_t st);
+void launch_slicewise_tensor(const double* sums, int kc, const int* kj, const double* res, long long M, int N,
+                             int common, double scale, int scaled, double* out, cudaStream_t st);
+void launch_slicewise_finish(const double* x, const double* sums, int kc, long long M, int N, double inv, double* res,
+                             cudaStream_t st);
 void launch_axpy(const double* a, const double* b, double beta, double* out, long long n, cudaStream_t st);
 
 }  // namespace dev

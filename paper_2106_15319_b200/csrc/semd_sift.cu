@@ -930,7 +930,7 @@ __device__ void decide_after_final(const Arena& A) {
         S.k += 1;
         S.iter = 0;
         if (S.kmax > 0 && S.k >= S.kmax) S.state = ST_DONE;
-        else if (S.write_imf && S.k0 + S.k > A.kcap) S.state = ST_DONE;  // overflowed (counted): host grows kcap
+        else if (S.write_imf && !imf_row_ok(A, S.k0, S.k - 1)) S.state = ST_DONE;  // overflowed (counted): host grows kcap
         else S.state = ST_DETECT;
     }
     __syncthreads();
@@ -977,7 +977,7 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
                 f.imf_out = S.imf_out;
                 f.res_out = S.res_out;
                 const int r = S.k0 + S.k;
-                f.row = (S.write_imf && r < A.kcap) ? A.sums + (size_t)r * A.L : nullptr;
+                f.row = (S.write_imf && imf_row_ok(A, S.k0, S.k)) ? A.sums + (size_t)r * A.L : nullptr;
                 tab[li] = f;
             }
             __syncthreads();
@@ -1054,7 +1054,7 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
         if (threadIdx.x == 0) {
             for (int li = 0; li < nf; ++li) {
                 const Slot& S = A.slots[A.final_list[li]];
-                if (S.write_imf && S.k0 + S.k >= A.kcap) atomicAdd(&C->k_overflow, 1);
+                if (S.write_imf && !imf_row_ok(A, S.k0, S.k)) atomicAdd(&C->k_overflow, 1);
             }
         }
         decide_after_final(A);

@@ -135,6 +135,7 @@ __device__ __forceinline__ void pdl_begin() {
 
 struct Arena {
     int L, G, tiles, cap, kcap;
+    int kper;      // > 0: IMF rows per job (batched jobs own rows [k0, k0 + kper)); 0: all kcap rows
     long long Lp;  // slot-buffer stride = tiles * kEvalTile (16-byte aligned; whole tiles readable)
     double sd_threshold;
     int max_sift_iters;
@@ -173,6 +174,10 @@ struct Arena {
     int* status_host; // mapped pinned: [0] active slots after this step, [1] step counter
 };
 
+// sums row k0 + k of a job is writable (its IMF fits the job's rows)
+__host__ __device__ inline bool imf_row_ok(const Arena& a, int k0, int k) {
+    return k0 + k < a.kcap && (a.kper == 0 || k < a.kper);
+}
 __host__ __device__ inline size_t buf_off(const Arena& a, int slot, int b) {
     return ((size_t)slot * 3 + (size_t)b) * (size_t)a.Lp;
 }

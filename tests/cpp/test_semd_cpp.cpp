@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <string>
 
+#include "semd/baseline.hpp"
 #include "semd/emd.hpp"
 #include "semd/serialize.hpp"
 
@@ -108,6 +109,18 @@ int main() {
                 err = std::max(err, std::abs(sum - z(i, j)));
             }
         CHECK(err <= 1e-8);
+        // baseline.cpp:5-29: per-channel decompositions, residue last (test_baseline idioms)
+        const ImfTensor sw = slicewise_decompose(z, Algorithm::Emd);
+        const Decomposition d1 = emd(z.channel(1));
+        CHECK(sw.modes() >= d1.imfs.size() + 1);
+        bool same = true;
+        for (std::size_t i = 0; i < 200; ++i) {
+            if (!d1.imfs.empty() && sw(i, 1, 0) != d1.imfs[0][i]) same = false;
+            if (sw(i, 1, sw.modes() - 1) != d1.residue[i]) same = false;
+        }
+        CHECK(same);
+        CHECK(throws_with<InvalidInput>([] { slicewise_decompose(MultiSignal(), Algorithm::Emd); },
+                                        "slicewise_decompose: empty input"));
     }
     std::printf("%s %d/%d\n", fails ? "FAILED" : "OK", checks - fails, checks);
     return fails ? 1 : 0;

@@ -310,12 +310,42 @@ def test_deconcatenate_and_serial(se, oracle):
     assert np.max(np.abs(te.sum(axis=2) - x6.T)) <= 1e-8 * np.max(np.abs(x6))
 
 
+def _slicewise_expected(per):
+    """baseline.cpp:17-27 assembly of per-channel decompositions -> (M, N, K) tensor."""
+    common = max(1, max(d[0].shape[0] + 1 for d in per))
+    M = per[0][1].size
+    t = np.zeros((M, len(per), common))
+    for j, (imfs, res) in enumerate(per):
+        if imfs.shape[0]:
+            t[:, j, :imfs.shape[0]] = imfs.T
+        t[:, j, common - 1] = res
+    return t
+
+
 def test_slicewise(se, oracle):
-    x = np.random.default_rng(11).standard_normal((120, 3))
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((300, 5)) + np.sin(np.arange(300) / 9.0)[:, None]
+    x[:, 4] = np.arange(300) * 0.1  # monotone channel: no IMFs, residue = x
     t = se.slicewise_decompose(x)
-    single = se.decompose(x[:, 1])
-    assert np.array_equal(t[:, 1, 0], single["imfs"][0])
+    per = [oracle.emd(x[:, j])[:2] for j in range(x.shape[1])]
+    assert np.array_equal(t, _slicewise_expected(per))  # batched EMD == reference per channel, bit-exact
     assert np.max(np.abs(t.sum(axis=2) - x)) <= 1e-10 * np.max(np.abs(x))
+    with pytest.raises(se.InvalidInput, match="slicewise_decompose: empty input"):
+        se.slicewise_decompose(np.zeros((0, 3)))
+
+
+def test_slicewise_ensembles(se):
+    """Batched slicewise EEMD (every channel x realization in one engine pass) and channel-by-channel
+    CEEMDAN equal the per-channel GPU decompositions bit-for-bit (same seeds, same sums order)."""
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((256, 4)) + np.cos(np.arange(256) / 7.0)[:, None]
+    for algo, nr in (("eemd", 6), ("ceemdan", 5)):
+        t = se.slicewise_decompose(x, algo, nr=nr)
+        per = []
+        for j in range(x.shape[1]):
+            d = se.decompose(x[:, j], algo, nr=nr)
+            per.append((d["imfs"], d["residue"]))
+        assert np.array_equal(t, _slicewise_expected(per)), algo
 
 
 # ------------------------------------------------------------------ full-size properties
