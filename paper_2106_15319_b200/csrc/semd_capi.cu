@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -231,13 +232,22 @@ struct semd_ctx {
         for (auto& s : h_slots) s.epoch = 1;
     }
 
+    // samples per lockstep step the slot count aims at (SEMD_STEP_SAMPLES overrides; tuning)
+    static long long step_samples() {
+        static const long long v = [] {
+            const char* e = std::getenv("SEMD_STEP_SAMPLES");
+            const long long x = e ? std::atoll(e) : 0;
+            return x > 0 ? x : (256LL << 20);  // C5: 15 realizations per wave (fewer steps, amortised fixed costs)
+        }();
+        return v;
+    }
     int auto_slots(long long L, int jobs) {
-        long long g = (64LL << 20) / std::max(1LL, L);
+        long long g = step_samples() / std::max(1LL, L);
         g = std::max(1LL, std::min<long long>(g, 1024));
         if (max_slots > 0) g = std::min<long long>(g, max_slots);
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
-        const long long per_slot = 72LL * L + 4096;
+        const long long per_slot = 96LL * L + 4096;  // slot buffers, knot lists, tables, stage, noise
         const long long mem_g = (long long)(0.5 * (double)free_b) / per_slot;
         g = std::max(1LL, std::min(g, mem_g));
         return (int)std::min<long long>(g, std::max(1, jobs));
