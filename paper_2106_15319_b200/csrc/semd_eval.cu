@@ -146,6 +146,7 @@ struct Strip {
     double* dst;           // where new values go (INIT: X, SIFT: the candidate; DETECT: none)
     const double4* tab0;   // side-0 segment table (side 1 at + tab_side)
     size_t stg;            // stage_off(side 0) + j0 * kTileKnots
+    unsigned* cnt0;        // scnt of tile j0, side 0 (side 1 at + A.G * tiles4)
     int to[2];             // lane l <= nt: knot offset (toff) of tile j0 + l, per side (SIFT)
 };
 
@@ -165,6 +166,7 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
                               : (S.mode == EM_SIFT ? A.bufs + buf_off(A, S.slot, sl.db) : nullptr);
     S.tab0 = A.ktab + tab_off(A, 0, S.slot);
     S.stg = stage_off(A, 0, S.slot) + (size_t)S.j0 * kTileKnots;
+    S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
     S.to[0] = S.to[1] = 0;
     if (S.mode == EM_SIFT) {
         const int j = S.j0 + min(lane, S.nt);
@@ -178,11 +180,13 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
 // Tile j's extrema are those of window [base-1, base+T-1); samples [base-2, base+T)
 // need table rows [toff[j], toff[j+1]+2].
 __device__ __forceinline__ void issue_tile(const Arena& A, const Strip& S, int i, WarpStage& st) {
-    int lo[2], hi[2];
+    int lo[2] = {0, 0}, hi[2] = {0, 0};
+    if (S.mode == EM_SIFT) {  // warp-uniform
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-        lo[s] = __shfl_sync(0xffffffffu, S.to[s], i);
-        hi[s] = __shfl_sync(0xffffffffu, S.to[s], i + 1);
+        for (int s = 0; s < 2; ++s) {
+            lo[s] = __shfl_sync(0xffffffffu, S.to[s], i);
+            hi[s] = __shfl_sync(0xffffffffu, S.to[s], i + 1);
+        }
     }
     if ((threadIdx.x & 31) != 0) return;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
@@ -369,21 +373,26 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
     c2 = __shfl_sync(0xffffffffu, nv[kSpt - 2], 31);  // carried into the next tile of the strip
     c1 = __shfl_sync(0xffffffffu, nv[kSpt - 1], 31);
 
-    unsigned fmax = 0, fmin = 0;
+    // extrema flags branch-free (find_extrema, emd.cpp:16-33); samples equal to a neighbour
+    // take the reference's plateau rule in a warp-uniform slow path
+    unsigned fmax = 0, fmin = 0, plat = 0;
 #pragma unroll
     for (int k = 0; k < kSpt; ++k) {
         const int t = t0 - 1 + k;
-        if (!Interior && (t < 1 || t > L - 2)) continue;
+        const bool in = Interior || (t >= 1 && t <= L - 2);
         const double l = w[k], v = w[k + 1], r = w[k + 2];
-        if (v != l && v != r) {
-            if (v > l && v > r) fmax |= 1u << k;
-            if (v < l && v < r) fmin |= 1u << k;
-        } else {
+        fmax |= (unsigned)(in && v > l && v > r) << k;
+        fmin |= (unsigned)(in && v < l && v < r) << k;
+        plat |= (unsigned)(in && (v == l || v == r)) << k;
+    }
+    if (__any_sync(0xffffffffu, plat != 0u)) {
+        for (int k = 0; k < kSpt; ++k) {
+            if (!(plat & (1u << k))) continue;
             int mn;
             Win6 win;
 #pragma unroll
             for (int z = 0; z < kSpt + 2; ++z) win.w[z] = w[z];
-            if (plateau_flags(A, S.slot, mode, t, win, t0, v, mn)) fmax |= 1u << k;
+            if (plateau_flags(A, S.slot, mode, t0 - 1 + k, win, t0, w[k + 1], mn)) fmax |= 1u << k;
             if (mn) fmin |= 1u << k;
         }
     }
@@ -415,9 +424,8 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         }
     }
     if (lane == 0) {
-        const size_t c = scnt_off(A, 0, S.slot) + j;
-        A.scnt[c] = total & 0xFFFF;
-        A.scnt[c + (size_t)A.G * tiles4(A)] = total >> 16;
+        S.cnt0[i] = total & 0xFFFF;
+        S.cnt0[i + (size_t)A.G * tiles4(A)] = total >> 16;
     }
 }
 
