@@ -1,6 +1,6 @@
 """Dev probe: fresh-arena vs reused-arena determinism (C4 EEMD), hazards."""
 import sys, os, hashlib
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_2106_15319_b200 as se
 from paper_2106_15319_b200 import workloads as W

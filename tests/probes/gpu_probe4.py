@@ -1,6 +1,6 @@
 """Dev probe: one C4 decomposition (NR=100) for kernel-level timing."""
 import sys, time, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2106_15319_b200 as se
 from paper_2106_15319_b200 import workloads as W
 s = se.concatenate(W.image_batch(), 10)

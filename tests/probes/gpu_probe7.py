@@ -1,6 +1,6 @@
 """Dev probe: determinism of repeated device-API EEMD calls."""
 import sys, os, ctypes as C, hashlib
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_2106_15319_b200 as se
 from paper_2106_15319_b200 import workloads as W, _native as N

@@ -1,6 +1,6 @@
 """Dev probe: run an EEMD config's realizations in chunks; report per-chunk steps and any engine stall."""
 import sys, time, os, ctypes as C
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_2106_15319_b200 as se
 from paper_2106_15319_b200 import workloads as W, _native as N
