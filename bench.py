@@ -174,15 +174,19 @@ def run_ours(args, rank, world, local):
     eval_s = stats_tot["eval_ms"] / 1e3
     peak, peak_kind = peaks()
     achieved = ALGO_BYTES_PER_SIFTED_SAMPLE * stats_tot["sifted_samples"] / eval_s / 1e9 if eval_s > 0 else None
-    traffic = None
+    traffic, traffic_note = None, None
     tf = os.path.join(ROOT, "profiles", "eval_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf):  # measured DRAM bytes of one SIFT-mode k_eval launch (ncu --set full capture)
         try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_sifted_sample")
+            t = json.load(open(tf))
+            traffic = t.get("traffic_bytes_per_launch")
+            traffic_note = {"algorithmic_bytes_per_launch": t.get("algorithmic_bytes_per_launch"),
+                            "dram_bytes_per_sifted_sample": t.get("dram_bytes_per_sifted_sample"),
+                            "source": t.get("source")}
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_detail": traffic_note,
             "kernel": "k_eval (sift pass)", "eval_ms_per_step": stats_tot["eval_ms"] / args.steps,
             "algorithmic_bytes": "16 B per sifted sample (SURVEY.md §8(d))"}
     # end-to-end through the public API, host buffers, copies inside the timed region
