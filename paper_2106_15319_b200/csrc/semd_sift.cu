@@ -654,12 +654,14 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             }
         }
         __syncthreads();
+        SOLVE_PROF(11);  // knot loads
         for (int q = tid; q < wn - 1; q += blockDim.x) {
             const double h = DP[spad(q + 1)] - DP[spad(q)];
             H[spad(q)] = h;
             RP[spad(q)] = 1.0 / h;
         }
         __syncthreads();
+        SOLVE_PROF(12);  // H, 1/H
         for (int q = tid + 1; q < wn - 1; q += blockDim.x) {  // emd.cpp:62 with exactly rounded divisions
             const double h0 = H[spad(q - 1)], h1 = H[spad(q)];
             RHS[spad(q)] = 6.0 * (div_rn(M[spad(q + 1)] - M[spad(q)], h1, RP[spad(q)]) - div_rn(M[spad(q)] - M[spad(q - 1)], h0, RP[spad(q - 1)]));

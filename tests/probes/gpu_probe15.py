@@ -23,8 +23,10 @@ c.check(c.lib.semd_solve_profile(c.ptr, buf))
 c.lib.semd_set_debug(c.ptr, 0)
 v = list(buf)
 blocks = max(1, v[10])
-names = ["setup", "stage+H+RHS", "phaseA", "phaseB", "1/d+phaseC", "phaseD", "outputs"]
-tot = sum(v[:7])
+names = ["setup", "RHS+table xy", "phaseA", "phaseB", "1/d+phaseC", "phaseD", "outputs"]
+tot = sum(v[:7]) + v[11] + v[12]
+print(f"{'knot loads':14s} {v[11] / blocks:10.0f} cycles/block  {100 * v[11] / max(1, tot):5.1f}%")
+print(f"{'H, 1/H':14s} {v[12] / blocks:10.0f} cycles/block  {100 * v[12] / max(1, tot):5.1f}%")
 print("blocks", blocks, "B rounds/block %.2f" % (v[8] / blocks), "D rounds/block %.2f" % (v[9] / blocks))
 for i, nm in enumerate(names):
     print(f"{nm:14s} {v[i] / blocks:10.0f} cycles/block  {100 * v[i] / max(1, tot):5.1f}%")
