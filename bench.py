@@ -237,25 +237,38 @@ def run_e2e(args, rank, world, local, ctx, x, cfg, scfg, ens, dev):
     L = M * Nch + D * (Nch - 1)
     host_in = torch.from_numpy(np.ascontiguousarray(x.T)).pin_memory()
     steps = max(1, args.e2e_steps)
+    out_buf = {}  # pinned host result buffer, allocated once (a caller reuses its buffers)
+
+    def one_step():
+        d_in = host_in.to(dev, non_blocking=True)  # H2D of the (M, N) multi-signal
+        s_dev = torch.empty(L, dtype=torch.float64, device=dev)
+        ctx.check(_concat_device(lib, ctx, d_in, s_dev, M, Nch, D))
+        imfs, res, st = decompose_sharded(cfg, s_dev, L, scfg, ens, rank, world, ctx)
+        nbytes = 0
+        if rank == 0:
+            modes = torch.cat([imfs, res[None, :]], 0).contiguous()
+            tensor = torch.empty((modes.shape[0], Nch, M), dtype=torch.float64, device=dev)
+            ctx.check(lib.semd_deconcatenate_device(ctx.ptr, C.c_void_p(modes.data_ptr()), modes.shape[0], L, M,
+                                                    Nch, D, C.c_void_p(tensor.data_ptr())))
+            host_out = out_buf.get(tuple(tensor.shape))
+            if host_out is None:
+                out_buf.clear()
+                host_out = out_buf[tuple(tensor.shape)] = torch.empty(tensor.shape, dtype=torch.float64,
+                                                                       pin_memory=True)
+            host_out.copy_(tensor)  # D2H of the (K+1, N, M) mode tensor
+            nbytes = host_out.numel() * 8
+        return st.get("sifted_samples", 0), nbytes
+
+    one_step()  # untimed: learns the mode count and allocates the pinned result buffer
     h2d = d2h = 0
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     sifted = 0
     for _ in range(steps):
-        d_in = host_in.to(dev, non_blocking=True)
+        sf, nb = one_step()
+        sifted += sf
         h2d += host_in.numel() * 8
-        s_dev = torch.empty(L, dtype=torch.float64, device=dev)
-        ctx.check(_concat_device(lib, ctx, d_in, s_dev, M, Nch, D))
-        imfs, res, st = decompose_sharded(cfg, s_dev, L, scfg, ens, rank, world, ctx)
-        sifted += st.get("sifted_samples", 0)
-        if rank == 0:
-            modes = torch.cat([imfs, res[None, :]], 0).contiguous()
-            tensor = torch.empty((modes.shape[0], Nch, M), dtype=torch.float64, device=dev)
-            ctx.check(lib.semd_deconcatenate_device(ctx.ptr, C.c_void_p(modes.data_ptr()), modes.shape[0], L, M,
-                                                         Nch, D, C.c_void_p(tensor.data_ptr())))
-            host_out = torch.empty(tensor.shape, dtype=torch.float64, pin_memory=True)
-            host_out.copy_(tensor)
-            d2h += host_out.numel() * 8
+        d2h += nb
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t0
     if world > 1:
