@@ -957,7 +957,78 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
     const unsigned nitems = nf > 0 ? (unsigned)tiles : 0u;
     static_assert(kFinalTile == 4 * 256, "4 consecutive samples per thread");
     const size_t L = (size_t)A.L;
-    while (true) {
+    // Short signals with many slots (C2/C3: 6k samples x 500 slots): too few tiles to keep the GPU
+    // busy, so the residue updates run per (slot, tile) and the ordered accumulation per element
+    // (each thread: one element, every finalising slot in slot order).
+    const bool split = nf > 1 && tiles * 2 < (int)gridDim.x;
+    if (split) {
+        const unsigned nR = (unsigned)nf * (unsigned)tiles;
+        const unsigned nS = (unsigned)((L + 255) / 256);
+        while (true) {
+            if (threadIdx.x == 0) s_ticket = atomicAdd(&C->ticket[3], 1u);
+            __syncthreads();
+            const unsigned q = s_ticket;
+            __syncthreads();
+            if (q >= nR + nS) break;
+            if (q < nR) {  // R = X - imf (emd.cpp:167), imf_out / res_out copies
+                const int li = (int)(q / (unsigned)tiles), tq = (int)(q % (unsigned)tiles);
+                const int sl = A.final_list[li];
+                const Slot& S = A.slots[sl];
+                const double* x = A.bufs + buf_off(A, sl, S.xb);
+                const double* imf = S.cb >= 0 ? A.bufs + buf_off(A, sl, S.cb) : x;
+                double* res = A.bufs + buf_off(A, sl, pick_free_buffer(S.xb, S.cb));
+                for (size_t t = (size_t)tq * kFinalTile + threadIdx.x; t < min(L, (size_t)(tq + 1) * kFinalTile);
+                     t += 256) {
+                    const double iv = imf[t];
+                    const double rv = x[t] - iv;
+                    res[t] = rv;
+                    if (S.imf_out) S.imf_out[t] = iv;
+                    if (S.res_out) S.res_out[t] = rv;
+                }
+            } else {  // sums[k0+k][t] += imf_s[t] in slot order (emd.cpp:249-251)
+                const size_t t = (size_t)(q - nR) * 256 + threadIdx.x;
+                double acc = 0.0;
+                double* accrow = nullptr;
+                for (int c0 = 0; c0 < nf; c0 += kFinalChunk) {
+                    const int cn = min(kFinalChunk, nf - c0);
+                    __syncthreads();
+                    for (int li = threadIdx.x; li < cn; li += blockDim.x) {
+                        const int sl = A.final_list[c0 + li];
+                        const Slot& S = A.slots[sl];
+                        FinalSlot f;
+                        f.x = A.bufs + buf_off(A, sl, S.xb);
+                        f.imf = S.cb >= 0 ? A.bufs + buf_off(A, sl, S.cb) : f.x;
+                        f.res = nullptr;
+                        f.imf_out = f.res_out = nullptr;
+                        const int r = S.k0 + S.k;
+                        f.row = (S.write_imf && imf_row_ok(A, S.k0, S.k)) ? A.sums + (size_t)r * A.L : nullptr;
+                        tab[li] = f;
+                    }
+                    __syncthreads();
+                    if (t >= L) continue;
+                    for (int g = 0; g < cn; g += 8) {
+                        double iv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) iv[u] = g + u < cn && tab[g + u].row ? tab[g + u].imf[t] : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (g + u >= cn) break;
+                            double* row = tab[g + u].row;
+                            if (!row) continue;
+                            if (row != accrow) {
+                                if (accrow) accrow[t] = acc;
+                                accrow = row;
+                                acc = accrow[t];
+                            }
+                            acc = acc + iv[u];
+                        }
+                    }
+                }
+                if (accrow && t < L) accrow[t] = acc;
+            }
+        }
+    }
+    while (!split) {
         if (threadIdx.x == 0) s_ticket = atomicAdd(&C->ticket[3], 1u);
         __syncthreads();
         const unsigned q = s_ticket;
