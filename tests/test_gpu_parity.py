@@ -482,3 +482,31 @@ def test_ceemdan_stage_api_matches_monolithic(se, oracle):
     o = oracle.decompose(x, 2, nr=nr)
     assert np.array_equal(imfs.cpu().numpy(), mono["imfs"]) and np.array_equal(res.cpu().numpy(), mono["residue"])
     assert np.array_equal(mono["imfs"], o[0]) and np.array_equal(mono["residue"], o[1])
+
+
+def test_eemd_shards_sum_to_whole(se):
+    """Realization sharding (the multi-GPU split) on one GPU: the partial sums of
+    [0, m) and [m, nr) add up to the partial sums of [0, nr), and K is the max of the shards' K."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2106_15319_b200 import _native as N
+    x = pickup_serialized(se, 50)
+    n, nr = x.size, 12
+    ctx = se.context()
+    xd = torch.from_numpy(x).cuda()
+
+    def part(mb, me):
+        sums = torch.zeros((32, n), dtype=torch.float64, device="cuda")
+        k = C.c_size_t()
+        ctx.check(ctx.lib.semd_eemd_partial_device(ctx.ptr, C.c_void_p(xd.data_ptr()), n,
+                                                   C.byref(N.SiftCfg(0.2, 300, 10)), C.byref(N.EnsCfg(0.2, nr, 0, 0)),
+                                                   mb, me, C.c_void_p(sums.data_ptr()), 32, C.byref(k)))
+        return sums.cpu().numpy(), int(k.value)
+
+    whole, kw = part(0, nr)
+    a, ka = part(0, 5)
+    b, kb = part(5, nr)
+    assert kw == max(ka, kb)
+    assert np.max(np.abs((a + b) - whole)) <= 1e-12 * np.max(np.abs(whole))
