@@ -250,7 +250,9 @@ struct semd_ctx {
         const long long per_slot = 96LL * L + 4096;  // slot buffers, knot lists, tables, stage, noise
         const long long mem_g = (long long)(0.5 * (double)free_b) / per_slot;
         g = std::max(1LL, std::min(g, mem_g));
-        return (int)std::min<long long>(g, std::max(1, jobs));
+        g = std::min<long long>(g, std::max(1, jobs));
+        const long long waves = (std::max(1, jobs) + g - 1) / g;  // the same wave count, evenly filled
+        return (int)((std::max(1, jobs) + waves - 1) / waves);
     }
 
     static int default_kcap(long long L, int max_imfs) {
@@ -494,16 +496,26 @@ struct semd_ctx {
         if (n < 4) raise(SEMD_INVALID_INPUT, "emd: signal too short (need at least 4 samples)");
         const int jobs = std::max(0, m_end - m_begin);
         const int G = auto_slots(n, jobs);
+        // W balanced waves (sizes differ by at most one): a short last wave would cost nearly a
+        // full wave of lockstep steps
+        const int W = jobs > 0 ? (jobs + G - 1) / G : 0;
+        auto wave = [&](int i, int& w0, int& g) {
+            const int base = jobs / W, extra = jobs % W;
+            w0 = m_begin + i * base + std::min(i, extra);
+            g = base + (i < extra ? 1 : 0);
+        };
         int kcap = default_kcap(n, cfg.max_imfs);
         const long long Ls = (n + 1) / 2 * 2;
         // the first wave's noise (side stream) overlaps the sequential std on the main stream
         bool first_noise_ready = false;
         if (!noise_override && jobs > 0) {
+            int fw0, fg;
+            wave(0, fw0, fg);
             noise.alloc((size_t)2 * G * Ls * 8);
-            semd::dev::launch_rng_ensemble(ens.base_seed, m_begin, std::min(G, jobs),
-                                           reinterpret_cast<uint64_t*>(noise.as<double>()), Ls, n, rng_stream);
-            semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(noise.as<double>()),
-                                         (long long)std::min(G, jobs) * Ls, 1.0, rng_stream);
+            semd::dev::launch_rng_ensemble(ens.base_seed, fw0, fg, reinterpret_cast<uint64_t*>(noise.as<double>()), Ls,
+                                           n, rng_stream);
+            semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(noise.as<double>()), (long long)fg * Ls, 1.0,
+                                         rng_stream);
             ck(cudaGetLastError(), "rng");
             ck(cudaEventRecord(noise_ready[0], rng_stream), "rng event");
             first_noise_ready = true;
@@ -521,8 +533,9 @@ struct semd_ctx {
             auto nbuf = [&](int b) { return noise.as<double>() + (size_t)b * G * Ls; };
             // noise of wave i lives in buffer i%2; generated on rng_stream (buffer i%2 was last read
             // by wave i-2, whose run() the host has already synchronized), signalled by noise_ready
-            auto make_noise = [&](int w0, int b) {
-                const int g = std::min(G, m_end - w0);
+            auto make_noise = [&](int wi, int b) {
+                int w0, g;
+                wave(wi, w0, g);
                 semd::dev::launch_rng_ensemble(ens.base_seed, w0, g, reinterpret_cast<uint64_t*>(nbuf(b)), Ls, n,
                                                rng_stream);
                 semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(nbuf(b)), (long long)g * Ls, 1.0, rng_stream);
@@ -530,15 +543,15 @@ struct semd_ctx {
                 ck(cudaEventRecord(noise_ready[b], rng_stream), "rng event");
             };
             try {
-                if (!noise_override && !first_noise_ready) make_noise(m_begin, 0);
+                if (!noise_override && !first_noise_ready && W > 0) make_noise(0, 0);
                 first_noise_ready = false;  // a capacity retry regenerates it
-                int wi = 0;
-                for (int w0 = m_begin; w0 < m_end; w0 += G, ++wi) {
-                    const int g = std::min(G, m_end - w0);
+                for (int wi = 0; wi < W; ++wi) {
+                    int w0, g;
+                    wave(wi, w0, g);
                     const int b = wi & 1;
                     std::vector<JobSpec> js(g);
                     if (!noise_override) {
-                        if (w0 + G < m_end) make_noise(w0 + G, b ^ 1);  // overlaps this wave's sifting
+                        if (wi + 1 < W) make_noise(wi + 1, b ^ 1);  // overlaps this wave's sifting
                         ck(cudaStreamWaitEvent(stream, noise_ready[b], 0), "noise wait");
                     }
                     for (int i = 0; i < g; ++i) {
