@@ -293,6 +293,9 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         // in 16-bit halves), and the lane's kSpt segments follow from kSpt-1 independent
         // compares -- no data-dependent branches.
         st.qmap[lane] = make_int2(0, 0);
+        // +inf sentinels after the tile's last row (which lies at or beyond the tile's end):
+        // the lane's look-ahead compares below need no bounds check (rows <= 64 + 3 + 2 < kWarpRows)
+        if (lane < 4) st.rows[lane >> 1][qmax[lane >> 1] + 2 + (lane & 1)].x = __longlong_as_double(0x7ff0000000000000LL);
         __syncwarp();
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
@@ -322,7 +325,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
             const int q0 = s == 0 ? (int)(qp & 0xFFFF) : (int)(qp >> 16);
             double xa[kSpt - 1];
 #pragma unroll
-            for (int u = 1; u < kSpt; ++u) xa[u - 1] = q0 + u <= qmax[s] ? R[q0 + u].x : 1e300;
+            for (int u = 1; u < kSpt; ++u) xa[u - 1] = R[q0 + u].x;
 #pragma unroll
             for (int k = 0; k < kSpt; ++k) {
                 const double tt = (double)(t0 + k);
