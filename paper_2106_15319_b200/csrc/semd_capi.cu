@@ -121,7 +121,7 @@ struct semd_ctx {
     // engine arena
     Arena A{};
     int cfg_L = -1, cfg_G = -1, cfg_kcap = -1, cfg_trace = -1;
-    DBuf bufs, kidx, toff, tbase, ctot, cnum, cden, ktab, sidx, scnt, tnum, tden, thash, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog, prof;
+    DBuf bufs, kidx, toff, tbase, ctot, cnum, cden, ktab, sidx, scnt, tnum, tden, thash, tflags, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog, prof;
     int* status_host = nullptr;
     int* status_host_dev = nullptr;
     std::vector<Slot> h_slots;
@@ -172,6 +172,7 @@ struct semd_ctx {
         tnum.alloc((size_t)G * t4 * 8);
         tden.alloc((size_t)G * t4 * 8);
         thash.alloc((size_t)2 * G * tiles * 8);
+        tflags.alloc((size_t)2 * G * tiles * 32);
         slots.alloc((size_t)G * sizeof(Slot));
         sums.alloc((size_t)kcap * L * 8);
         imf_sifts.alloc((size_t)kcap * 4);
@@ -200,6 +201,7 @@ struct semd_ctx {
         A.tnum = tnum.as<double>();
         A.tden = tden.as<double>();
         A.thash = thash.as<unsigned long long>();
+        A.tflags = tflags.as<unsigned char>();
         A.slots = slots.as<Slot>();
         A.sums = sums.as<double>();
         A.imf_sifts = imf_sifts.as<int>();

@@ -107,7 +107,6 @@ constexpr int kWarpSamp = kEvalTile + 8;      // staged samples [base-2, base+T)
 struct alignas(16) WarpStage {
     double4 rows[2][kWarpRows];
     double samp[kWarpSamp];
-    int2 qmap[32];            // per-lane first segment of each side (bucket map, SIFT mode)
     unsigned long long bar;   // mbarrier: the tile's bulk copies have landed
 };
 
@@ -141,7 +140,7 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parit
 
 // Per-strip constants of one warp.
 struct Strip {
-    int slot, j0, nt, mode;
+    int slot, j0, nt, mode, par;
     const double* src;     // the samples this pass reads (SIFT, DETECT)
     double* dst;           // where new values go (INIT: X, SIFT: the candidate; DETECT: none)
     const double4* tab0;   // side-0 segment table (side 1 at + tab_side)
@@ -161,6 +160,7 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
     const int state = sl.state;
     S.mode = state == ST_INIT ? EM_INIT : (state == ST_DETECT ? EM_DETECT : EM_SIFT);
     const int cb = sl.cb, xb = sl.xb;
+    S.par = sl.par;
     S.src = A.bufs + buf_off(A, S.slot, (S.mode == EM_SIFT && cb >= 0) ? cb : xb);
     S.dst = S.mode == EM_INIT ? A.bufs + buf_off(A, S.slot, xb)
                               : (S.mode == EM_SIFT ? A.bufs + buf_off(A, S.slot, sl.db) : nullptr);
@@ -230,6 +230,8 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
     const int j = S.j0 + i;
     const int base = j * kEvalTile;
     const int t0 = base + lane * kSpt;
+    // this lane's extrema flags from the detection that produced the current knots (SIFT)
+    const unsigned oflags = mode == EM_SIFT ? A.tflags[tfl_off(A, S.par, S.slot) + (size_t)j * 32 + lane] : 0u;
     int qmax[2] = {0, 0};
     if (mode == EM_SIFT) {
 #pragma unroll
@@ -286,52 +288,29 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
 
     double nv[kSpt];
     if (mode == EM_SIFT) {
-        // seg(t) = last staged row q <= qmax with x_q < t (the reference's march, emd.cpp:79).
-        // Knot positions are distinct integers, so at most one row boundary lies between
-        // consecutive samples: the warp finds each lane's first segment with a bucket map
-        // (row r -> first lane whose t0 exceeds x_r; prefix max over lanes, both sides packed
-        // in 16-bit halves), and the lane's kSpt segments follow from kSpt-1 independent
-        // compares -- no data-dependent branches.
-        st.qmap[lane] = make_int2(0, 0);
-        // +inf sentinels after the tile's last row (which lies at or beyond the tile's end):
-        // the lane's look-ahead compares below need no bounds check (rows <= 64 + 3 + 2 < kWarpRows)
-        if (lane < 4) st.rows[lane >> 1][qmax[lane >> 1] + 2 + (lane & 1)].x = __longlong_as_double(0x7ff0000000000000LL);
-        __syncwarp();
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const double4* R = st.rows[s];
-#pragma unroll
-            for (int q = 0; q < (kWarpRows + 31) / 32; ++q) {
-                const int r = 1 + lane + 32 * q;
-                if (r <= qmax[s]) {
-                    const int d = (int)R[r].x - base;  // x integral; bucket = first lane with t0 > x
-                    const int bk = d < 0 ? 0 : d / kSpt + 1;
-                    if (bk < 32) atomicMax(s == 0 ? &st.qmap[bk].x : &st.qmap[bk].y, r);
-                }
-            }
-        }
-        __syncwarp();
-        const int2 qq = st.qmap[lane];
-        unsigned qp = (unsigned)qq.x | ((unsigned)qq.y << 16);
+        // seg(t) = last staged row q with x_q < t (the reference's march, emd.cpp:79). Rows 0-1
+        // precede the tile's detection window and rows 2.. are its extrema in order, so
+        // seg(t) = 1 + #(window extrema at positions < t): the lane's first segment is an
+        // exclusive warp scan of the previous detection's per-lane counts (plus its own
+        // window position t0-1), and each further sample adds the extrema it passes.
+        const unsigned ocnt = (unsigned)__popc(oflags & 0xFu) | ((unsigned)__popc(oflags >> 4) << 16);
+        unsigned oincl = ocnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, qp, o);
-            if (lane >= o) qp = __vmaxu2(qp, y);
+            const unsigned y = __shfl_up_sync(0xffffffffu, oincl, o);
+            if (lane >= o) oincl += y;
         }
+        const unsigned oexcl = oincl - ocnt;
         double env0[kSpt];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const double4* R = st.rows[s];
-            const int q0 = s == 0 ? (int)(qp & 0xFFFF) : (int)(qp >> 16);
-            double xa[kSpt - 1];
-#pragma unroll
-            for (int u = 1; u < kSpt; ++u) xa[u - 1] = R[q0 + u].x;
+            const unsigned fl = (oflags >> (4 * s)) & 0xFu;  // window positions t0-1 .. t0+2
+            const int q0 = 1 + (int)(s == 0 ? (oexcl & 0xFFFFu) : (oexcl >> 16)) + (int)(fl & 1u);
 #pragma unroll
             for (int k = 0; k < kSpt; ++k) {
                 const double tt = (double)(t0 + k);
-                int q = q0;
-#pragma unroll
-                for (int u = 1; u <= k; ++u) q += xa[u - 1] < tt;
+                const int q = q0 + __popc((fl >> 1) & ((1u << k) - 1u));
                 const double4 r0 = R[q], r1 = R[q + 1];
                 const double h = r1.x - r0.x;
                 const double e = spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
@@ -399,6 +378,8 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
             if (mn) fmin |= 1u << k;
         }
     }
+
+    A.tflags[tfl_off(A, 1 - S.par, S.slot) + (size_t)j * 32 + lane] = (unsigned char)(fmax | (fmin << 4));
 
     // tile-local ordered compaction (warp scan of packed counts)
     const unsigned packed = (unsigned)__popc(fmax) | ((unsigned)__popc(fmin) << 16);

@@ -154,6 +154,7 @@ struct Arena {
     double* tnum;
     double* tden;
     unsigned long long* thash;
+    unsigned char* tflags;  // [2 par][G][tiles][32] extrema flags of each lane's detection window (fmax | fmin << 4)
     Slot* slots;
     double* sums;
     int* imf_sifts;   // [kcap] sift count per IMF of slot 0 (plain EMD / extract_imf)
@@ -214,6 +215,9 @@ struct ToffView {
 };
 __device__ __forceinline__ ToffView toff_view(const Arena& a, int par, int side, int slot) {
     return ToffView{a.toff + toff_off(a, par, side, slot), a.tbase + tbase_off(a, par, side, slot), a.chunks - 1};
+}
+__host__ __device__ inline size_t tfl_off(const Arena& a, int par, int slot) {
+    return ((size_t)par * a.G + slot) * (size_t)a.tiles * 32;
 }
 __host__ __device__ inline size_t tab_off(const Arena& a, int side, int slot) {
     return ((size_t)side * a.G + slot) * (size_t)(a.cap + 8);
