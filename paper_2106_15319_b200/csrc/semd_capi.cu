@@ -172,7 +172,7 @@ struct semd_ctx {
         tnum.alloc((size_t)G * t4 * 8);
         tden.alloc((size_t)G * t4 * 8);
         thash.alloc((size_t)2 * G * tiles * 8);
-        tflags.alloc((size_t)2 * G * tiles * 32);
+        tflags.alloc((size_t)2 * G * tiles * 32 * 4);
         slots.alloc((size_t)G * sizeof(Slot));
         sums.alloc((size_t)kcap * L * 8);
         imf_sifts.alloc((size_t)kcap * 4);
@@ -201,7 +201,7 @@ struct semd_ctx {
         A.tnum = tnum.as<double>();
         A.tden = tden.as<double>();
         A.thash = thash.as<unsigned long long>();
-        A.tflags = tflags.as<unsigned char>();
+        A.tflags = tflags.as<unsigned>();
         A.slots = slots.as<Slot>();
         A.sums = sums.as<double>();
         A.imf_sifts = imf_sifts.as<int>();
@@ -249,7 +249,7 @@ struct semd_ctx {
         if (max_slots > 0) g = std::min<long long>(g, max_slots);
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
-        const long long per_slot = 96LL * L + 4096;  // slot buffers, knot lists, tables, stage, noise
+        const long long per_slot = 98LL * L + 4096;  // slot buffers, knot lists, tables, stage, flags, noise
         const long long mem_g = (long long)(0.5 * (double)free_b) / per_slot;
         g = std::max(1LL, std::min(g, mem_g));
         g = std::min<long long>(g, std::max(1, jobs));

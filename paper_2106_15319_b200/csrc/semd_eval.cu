@@ -107,6 +107,7 @@ constexpr int kWarpSamp = kEvalTile + 8;      // staged samples [base-2, base+T)
 struct alignas(16) WarpStage {
     double4 rows[2][kWarpRows];
     double samp[kWarpSamp];
+    unsigned ow[32];          // SIFT: the previous detection's per-lane words of this tile (tflags)
     unsigned long long bar;   // mbarrier: the tile's bulk copies have landed
 };
 
@@ -143,7 +144,10 @@ struct Strip {
     int slot, j0, nt, mode, par;
     const double* src;     // the samples this pass reads (SIFT, DETECT)
     double* dst;           // where new values go (INIT: X, SIFT: the candidate; DETECT: none)
-    const double4* tab0;   // side-0 segment table (side 1 at + tab_side)
+    const double4* tab0;   // side-0 segment table
+    const double4* tab1;   // side-1 segment table
+    const unsigned* ow;    // SIFT: tflags words of tile j0 (current knot parity)
+    unsigned* nw;          // tflags words of tile j0 (parity of the new detection)
     size_t stg;            // stage_off(side 0) + j0 * kTileKnots
     unsigned* cnt0;        // scnt of tile j0, side 0 (side 1 at + A.G * tiles4)
     int to[2];             // lane l <= nt: knot offset (toff) of tile j0 + l, per side (SIFT)
@@ -165,6 +169,9 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
     S.dst = S.mode == EM_INIT ? A.bufs + buf_off(A, S.slot, xb)
                               : (S.mode == EM_SIFT ? A.bufs + buf_off(A, S.slot, sl.db) : nullptr);
     S.tab0 = A.ktab + tab_off(A, 0, S.slot);
+    S.tab1 = A.ktab + tab_off(A, 1, S.slot);
+    S.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
+    S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
     S.stg = stage_off(A, 0, S.slot) + (size_t)S.j0 * kTileKnots;
     S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
     S.to[0] = S.to[1] = 0;
@@ -196,11 +203,12 @@ __device__ __forceinline__ void issue_tile(const Arena& A, const Strip& S, int i
         const unsigned sb = (unsigned)(base + kEvalTile - e0) * 8u;
         const unsigned r0 = S.mode == EM_SIFT ? (unsigned)(hi[0] + 3 - lo[0]) * 32u : 0u;
         const unsigned r1 = S.mode == EM_SIFT ? (unsigned)(hi[1] + 3 - lo[1]) * 32u : 0u;
-        bar_arrive_tx(&st.bar, sb + r0 + r1);
+        bar_arrive_tx(&st.bar, sb + r0 + r1 + (S.mode == EM_SIFT ? 128u : 0u));
         bulk_g2s(&st.samp[e0 - (base - 2)], S.src + e0, sb, &st.bar);
         if (S.mode == EM_SIFT) {
             bulk_g2s(st.rows[0], S.tab0 + lo[0], r0, &st.bar);
-            bulk_g2s(st.rows[1], S.tab0 + (size_t)A.G * (A.cap + 8) + lo[1], r1, &st.bar);
+            bulk_g2s(st.rows[1], S.tab1 + lo[1], r1, &st.bar);
+            bulk_g2s(st.ow, S.ow + i * 32, 128u, &st.bar);
         }
     } else {
         bar_arrive_tx(&st.bar, 0u);
@@ -230,8 +238,6 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
     const int j = S.j0 + i;
     const int base = j * kEvalTile;
     const int t0 = base + lane * kSpt;
-    // this lane's extrema flags from the detection that produced the current knots (SIFT)
-    const unsigned oflags = mode == EM_SIFT ? A.tflags[tfl_off(A, S.par, S.slot) + (size_t)j * 32 + lane] : 0u;
     int qmax[2] = {0, 0};
     if (mode == EM_SIFT) {
 #pragma unroll
@@ -290,23 +296,16 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
     if (mode == EM_SIFT) {
         // seg(t) = last staged row q with x_q < t (the reference's march, emd.cpp:79). Rows 0-1
         // precede the tile's detection window and rows 2.. are its extrema in order, so
-        // seg(t) = 1 + #(window extrema at positions < t): the lane's first segment is an
-        // exclusive warp scan of the previous detection's per-lane counts (plus its own
-        // window position t0-1), and each further sample adds the extrema it passes.
-        const unsigned ocnt = (unsigned)__popc(oflags & 0xFu) | ((unsigned)__popc(oflags >> 4) << 16);
-        unsigned oincl = ocnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, oincl, o);
-            if (lane >= o) oincl += y;
-        }
-        const unsigned oexcl = oincl - ocnt;
+        // seg(t) = 1 + #(window extrema at positions < t): the previous detection stored, per
+        // lane, its flags for window positions t0-1 .. t0+2 and its rank among the tile's
+        // extrema of each side; each further sample adds the extrema it passes.
+        const unsigned ow = st.ow[lane];
         double env0[kSpt];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const double4* R = st.rows[s];
-            const unsigned fl = (oflags >> (4 * s)) & 0xFu;  // window positions t0-1 .. t0+2
-            const int q0 = 1 + (int)(s == 0 ? (oexcl & 0xFFFFu) : (oexcl >> 16)) + (int)(fl & 1u);
+            const unsigned fl = (ow >> (4 * s)) & 0xFu;  // window positions t0-1 .. t0+2
+            const int q0 = 1 + (int)((ow >> (8 + 8 * s)) & 0xFFu) + (int)(fl & 1u);
 #pragma unroll
             for (int k = 0; k < kSpt; ++k) {
                 const double tt = (double)(t0 + k);
@@ -379,8 +378,6 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         }
     }
 
-    A.tflags[tfl_off(A, 1 - S.par, S.slot) + (size_t)j * 32 + lane] = (unsigned char)(fmax | (fmin << 4));
-
     // tile-local ordered compaction (warp scan of packed counts)
     const unsigned packed = (unsigned)__popc(fmax) | ((unsigned)__popc(fmin) << 16);
     unsigned incl = packed;
@@ -391,6 +388,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
     }
     const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
     const unsigned excl = incl - packed;
+    S.nw[i * 32 + lane] = fmax | (fmin << 4) | ((excl & 0xFFu) << 8) | ((excl >> 16) << 16);
     if (fmax | fmin) {
         const size_t side1 = (size_t)A.G * A.tiles * kTileKnots;
         const size_t o = S.stg + (size_t)i * kTileKnots;

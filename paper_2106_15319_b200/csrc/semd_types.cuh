@@ -154,7 +154,7 @@ struct Arena {
     double* tnum;
     double* tden;
     unsigned long long* thash;
-    unsigned char* tflags;  // [2 par][G][tiles][32] extrema flags of each lane's detection window (fmax | fmin << 4)
+    unsigned* tflags;  // [2 par][G][tiles][32 lanes] per detection lane: flags (max | min << 4) | max rank << 8 | min rank << 16
     Slot* slots;
     double* sums;
     int* imf_sifts;   // [kcap] sift count per IMF of slot 0 (plain EMD / extract_imf)
