@@ -121,7 +121,7 @@ struct semd_ctx {
     // engine arena
     Arena A{};
     int cfg_L = -1, cfg_G = -1, cfg_kcap = -1, cfg_trace = -1;
-    DBuf bufs, kidx, toff, tbase, ctot, cnum, cden, ktab, sidx, scnt, tnum, tden, thash, tflags, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog, prof;
+    DBuf bufs, kidx, toff, tbase, ctot, cnum, cden, ktab, scnt, tnum, tden, thash, tflags, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog, prof;
     int* status_host = nullptr;
     int* status_host_dev = nullptr;
     std::vector<Slot> h_slots;
@@ -167,7 +167,6 @@ struct semd_ctx {
         cnum.alloc((size_t)G * chunks * 8);
         cden.alloc((size_t)G * chunks * 8);
         ktab.alloc(((size_t)2 * G * (cap + 8) + 16) * 32);
-        sidx.alloc((size_t)2 * G * tiles * semd::dev::kTileKnots * 4);
         scnt.alloc((size_t)2 * G * t4 * 4);
         tnum.alloc((size_t)G * t4 * 8);
         tden.alloc((size_t)G * t4 * 8);
@@ -196,7 +195,6 @@ struct semd_ctx {
         A.cden = cden.as<double>();
         A.chunks = chunks;
         A.ktab = ktab.as<double4>();
-        A.sidx = sidx.as<int>();
         A.scnt = scnt.as<unsigned>();
         A.tnum = tnum.as<double>();
         A.tden = tden.as<double>();
@@ -249,7 +247,7 @@ struct semd_ctx {
         if (max_slots > 0) g = std::min<long long>(g, max_slots);
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
-        const long long per_slot = 98LL * L + 4096;  // slot buffers, knot lists, tables, stage, flags, noise
+        const long long per_slot = 94LL * L + 4096;  // slot buffers, knot lists, tables, detection words, noise
         const long long mem_g = (long long)(0.5 * (double)free_b) / per_slot;
         g = std::max(1LL, std::min(g, mem_g));
         g = std::min<long long>(g, std::max(1, jobs));

@@ -148,7 +148,6 @@ struct Strip {
     const double4* tab1;   // side-1 segment table
     const unsigned* ow;    // SIFT: tflags words of tile j0 (current knot parity)
     unsigned* nw;          // tflags words of tile j0 (parity of the new detection)
-    size_t stg;            // stage_off(side 0) + j0 * kTileKnots
     unsigned* cnt0;        // scnt of tile j0, side 0 (side 1 at + A.G * tiles4)
     int to[2];             // lane l <= nt: knot offset (toff) of tile j0 + l, per side (SIFT)
 };
@@ -172,7 +171,6 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
     S.tab1 = A.ktab + tab_off(A, 1, S.slot);
     S.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
     S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
-    S.stg = stage_off(A, 0, S.slot) + (size_t)S.j0 * kTileKnots;
     S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
     S.to[0] = S.to[1] = 0;
     if (S.mode == EM_SIFT) {
@@ -378,7 +376,8 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         }
     }
 
-    // tile-local ordered compaction (warp scan of packed counts)
+    // tile-local ranks (warp scan of packed counts): with the flags they are the tile's ordered
+    // extrema lists, expanded into the knot lists by k_compact and read back by the next sift
     const unsigned packed = (unsigned)__popc(fmax) | ((unsigned)__popc(fmin) << 16);
     unsigned incl = packed;
 #pragma unroll
@@ -389,22 +388,6 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
     const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
     const unsigned excl = incl - packed;
     S.nw[i * 32 + lane] = fmax | (fmin << 4) | ((excl & 0xFFu) << 8) | ((excl >> 16) << 16);
-    if (fmax | fmin) {
-        const size_t side1 = (size_t)A.G * A.tiles * kTileKnots;
-        const size_t o = S.stg + (size_t)i * kTileKnots;
-        unsigned omax = excl & 0xFFFF, omin = excl >> 16;
-#pragma unroll
-        for (int k = 0; k < kSpt; ++k) {
-            if (fmax & (1u << k)) {
-                A.sidx[o + omax] = t0 - 1 + k;
-                ++omax;
-            }
-            if (fmin & (1u << k)) {
-                A.sidx[side1 + o + omin] = t0 - 1 + k;
-                ++omin;
-            }
-        }
-    }
     if (lane == 0) {
         S.cnt0[i] = total & 0xFFFF;
         S.cnt0[i + (size_t)A.G * tiles4(A)] = total >> 16;

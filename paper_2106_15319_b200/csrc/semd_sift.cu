@@ -365,41 +365,69 @@ constexpr int kCompactStrip = 16;
 __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
     pdl_begin();
     __shared__ int s_last;
+    __shared__ int sbuf[kCompactThreads / 32][2][kEvalTile / 2];  // one tile's ordered extrema per side
     Ctrl* C = A.ctrl;
     const int lane = threadIdx.x & 31;
     const int wpb = kCompactThreads / 32;
+    int(*sb)[kEvalTile / 2] = sbuf[threadIdx.x >> 5];
     const int strips = (A.tiles + kCompactStrip - 1) / kCompactStrip;
-    const unsigned per_slot = 2u * (unsigned)strips;
-    const unsigned nitems = (unsigned)C->n_compact * per_slot;
+    const unsigned nitems = (unsigned)C->n_compact * (unsigned)strips;
     const bool tracing = A.trace != nullptr;
     for (unsigned it = blockIdx.x * wpb + (threadIdx.x >> 5); it < nitems; it += gridDim.x * wpb) {
-        const int s = A.compact_list[it / per_slot];
-        const unsigned r = it % per_slot;
-        const int side = (int)(r / (unsigned)strips);
-        const int sx = (int)(r % (unsigned)strips);
+        const int s = A.compact_list[it / (unsigned)strips];
+        const int sx = (int)(it % (unsigned)strips);
         const int j0 = sx * kCompactStrip;
         const int nt = min(kCompactStrip, A.tiles - j0);
         const int cpar = A.slots[s].cpar;
-        unsigned cnt = 0, off = 0;
+        unsigned off0 = 0, off1 = 0;
         if (lane < nt) {
-            cnt = A.scnt[scnt_off(A, side, s) + j0 + lane];
-            off = toff_view(A, cpar, side, s)[j0 + lane];
+            off0 = toff_view(A, cpar, 0, s)[j0 + lane];
+            off1 = toff_view(A, cpar, 1, s)[j0 + lane];
         }
-        const int* si = A.sidx + stage_off(A, side, s) + (size_t)j0 * kTileKnots;
-        int* gi = A.kidx + knot_off(A, cpar, side, s);
-        uint64_t h = 0;
+        // eval's per-lane detection words: window flags of samples t0-1 .. t0+2 and the lane's
+        // rank among the tile's extrema of each side; ranked into shared memory, then written
+        // to the knot lists coalesced
+        const unsigned* wd = A.tflags + tfl_off(A, cpar, s) + (size_t)j0 * 32 + lane;
+        int* gi0 = A.kidx + knot_off(A, cpar, 0, s);
+        int* gi1 = A.kidx + knot_off(A, cpar, 1, s);
+        uint64_t h0 = 0, h1 = 0;
+        unsigned wn = wd[0];
         for (int u = 0; u < nt; ++u) {
-            const unsigned cu = __shfl_sync(0xffffffffu, cnt, u);
-            const unsigned ou = __shfl_sync(0xffffffffu, off, u);
-            for (unsigned i = lane; i < cu; i += 32) {
-                const int t = si[u * kTileKnots + i];
-                gi[ou + i] = t;
-                if (tracing) h += knot_hash(side, ou + i, (unsigned)t);
+            const unsigned w = wn;
+            if (u + 1 < nt) wn = wd[(u + 1) * 32];
+            const int p0 = (j0 + u) * kEvalTile + lane * kSpt - 1;
+            unsigned n[2];
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+                const unsigned fl = (w >> (4 * side)) & 0xFu;
+                const unsigned r = (w >> (8 + 8 * side)) & 0xFFu;
+#pragma unroll
+                for (int k = 0; k < kSpt; ++k)
+                    if ((fl >> k) & 1u) sb[side][r + __popc(fl & ((1u << k) - 1u))] = p0 + k;
+                n[side] = __reduce_add_sync(0xffffffffu, (unsigned)__popc(fl));
             }
+            __syncwarp();
+            const unsigned o0 = __shfl_sync(0xffffffffu, off0, u);
+            const unsigned o1 = __shfl_sync(0xffffffffu, off1, u);
+            for (unsigned i = lane; i < n[0]; i += 32) {
+                const int t = sb[0][i];
+                gi0[o0 + i] = t;
+                if (tracing) h0 += knot_hash(0, o0 + i, (unsigned)t);
+            }
+            for (unsigned i = lane; i < n[1]; i += 32) {
+                const int t = sb[1][i];
+                gi1[o1 + i] = t;
+                if (tracing) h1 += knot_hash(1, o1 + i, (unsigned)t);
+            }
+            __syncwarp();
         }
         if (tracing) {
-            h = warp_sum(h);
-            if (lane == 0) A.thash[((size_t)side * A.G + s) * A.tiles + sx] = h;
+            h0 = warp_sum(h0);
+            h1 = warp_sum(h1);
+            if (lane == 0) {
+                A.thash[(size_t)s * A.tiles + sx] = h0;
+                A.thash[((size_t)A.G + s) * A.tiles + sx] = h1;
+            }
         }
     }
     __syncthreads();

@@ -8,7 +8,7 @@
 //
 // HBM layout per engine (L = serialized length, G = slots, T = eval tile):
 //   bufs    f64 [G][3][L]        rotating X (IMF input), C (candidate), R (next residue)
-//   sidx    i32 [2 side][G][tiles*T/2]    tile-local extrema found by k_eval (stage)
+//   tflags  u32 [2 par][G][tiles][32]     k_eval's detection word per lane: window flags + tile ranks
 //   scnt    u32 [2 side][G][tiles]        extrema per tile
 //   kidx    i32 [2 par][2 side][G][cap]   compacted extrema indices (cap = L/2+2)
 //   (extremum values are not stored: value r = candidate[idx[r]], gathered by k_solve)
@@ -29,7 +29,6 @@ constexpr int kEvalTile = 128;                  // samples per eval tile (one wa
 constexpr int kEvalThreads = 256;              // 8 independent warps per CTA
 constexpr int kSpt = kEvalTile / 32;            // samples per lane (consecutive)
 constexpr int kKnotCapTile = kEvalTile / 2 + 4; // knots of one side touching a tile
-constexpr int kTileKnots = kEvalTile / 2;       // stage capacity per tile and side
 
 constexpr int kSolveChains = 64;                         // speculative chains per block
 constexpr int kSolveChunk = 16;                          // rows per chain
@@ -149,7 +148,6 @@ struct Arena {
     double* cden;
     int chunks;  // scan chunks per (slot, side): ceil(tiles / kScanChunk)
     double4* ktab;
-    int* sidx;
     unsigned* scnt;
     double* tnum;
     double* tden;
@@ -221,9 +219,6 @@ __host__ __device__ inline size_t tfl_off(const Arena& a, int par, int slot) {
 }
 __host__ __device__ inline size_t tab_off(const Arena& a, int side, int slot) {
     return ((size_t)side * a.G + slot) * (size_t)(a.cap + 8);
-}
-__host__ __device__ inline size_t stage_off(const Arena& a, int side, int slot) {
-    return ((size_t)side * a.G + slot) * (size_t)a.tiles * kTileKnots;
 }
 __host__ __device__ inline size_t scnt_off(const Arena& a, int side, int slot) {
     return ((size_t)side * a.G + slot) * tiles4(a);
