@@ -11,7 +11,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsemd_b200.so")
+# SEMD_LIB: an alternative in-tree build of the same library (A/B tuning runs)
+LIB_PATH = os.environ.get("SEMD_LIB") or os.path.join(HERE, "libsemd_b200.so")
 
 SEMD_OK = 0
 SEMD_INVALID_INPUT = 1
@@ -109,6 +110,7 @@ SIGNATURES = {
 EXTRA = {"semd_set_noise_override": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t]),
          "semd_set_debug": (C.c_int, [C.c_void_p, C.c_int]),
          "semd_solve_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+         "semd_kernel_spans": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
          "semd_hazard_log": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
          "semd_mt19937_64_device_test": (C.c_int, [C.c_void_p, C.c_uint64, C.c_size_t, C.POINTER(C.c_uint64)])}
 

@@ -237,7 +237,7 @@ struct semd_ctx {
         static const long long v = [] {
             const char* e = std::getenv("SEMD_STEP_SAMPLES");
             const long long x = e ? std::atoll(e) : 0;
-            return x > 0 ? x : (256LL << 20);  // C5: 15 realizations per wave (fewer steps, amortised fixed costs)
+            return x > 0 ? x : (512LL << 20);  // C5: 31 realizations per wave (fewer steps, amortised fixed costs)
         }();
         return v;
     }
@@ -365,6 +365,16 @@ struct semd_ctx {
         }
         stats.solve_hazards += (uint64_t)c.hazards;
         if (timing) stats.eval_ms += (double)c.ev_ns * 1e-6;
+        for (int id = 0; id < 5; ++id) {  // the spans the last two steps left unfolded
+            unsigned long long ns = c.kns[id];
+            for (int p = 0; p < 2; ++p) {
+                const unsigned long long a = c.kt[p][id][0], b = c.kt[p][id][1];
+                if (a && b && b > ~a) ns += b - ~a;
+            }
+            span_ms[id] += (double)ns * 1e-6;
+        }
+        span_strips[0] += c.strips[0];
+        span_strips[1] += c.strips[1];
         if (c.hz_count > 0) {
             const int n = std::min(c.hz_count, kHzCap);
             const size_t old = h_hz.size();
@@ -386,6 +396,8 @@ struct semd_ctx {
         ck(cudaMemcpyAsync(A.ctrl, &z, sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
     }
     long long trace_total = 0;
+    double span_ms[5] = {};                 // device spans of the step kernels (semd_kernel_spans)
+    unsigned long long span_strips[2] = {};  // eval strips: DETECT/INIT mode, SIFT mode
     static constexpr int kHzCap = 4096;
     int debug_flags = 0;
     std::vector<int> h_hz;  // solve-hazard records since reset_stats (test hook)
@@ -1171,6 +1183,22 @@ int semd_solve_profile(semd_ctx* ctx, uint64_t* out) {
         if (!ctx->prof.p) raise(SEMD_INVALID_INPUT, "no engine configured");
         ck(cudaMemcpy(out, ctx->prof.p, 16 * 8, cudaMemcpyDeviceToHost), "prof");
         ck(cudaMemset(ctx->prof.p, 0, 16 * 8), "prof");
+    });
+}
+
+// Profiling hook: device spans (ms) of k_solve, k_eval, k_scan, k_compact, k_final summed over
+// the steps since the last call, and the eval strips processed in DETECT/INIT and SIFT mode.
+int semd_kernel_spans(semd_ctx* ctx, double* ms, uint64_t* strips) {
+    return guard([&] {
+        need_ctx(ctx);
+        for (int i = 0; i < 5; ++i) {
+            ms[i] = ctx->span_ms[i];
+            ctx->span_ms[i] = 0.0;
+        }
+        for (int i = 0; i < 2; ++i) {
+            strips[i] = ctx->span_strips[i];
+            ctx->span_strips[i] = 0;
+        }
     });
 }
 

@@ -406,7 +406,11 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     pdl_begin();
     extern __shared__ __align__(16) unsigned char eval_smem[];
-    if (threadIdx.x == 0) atomicMin(&A.ctrl->ev_t0, globaltimer());
+    const int kstep_ = A.ctrl->step;
+    if (threadIdx.x == 0) {
+        atomicMin(&A.ctrl->ev_t0, globaltimer());
+        span_begin(A.ctrl, KID_EVAL);
+    }
     const int lane = threadIdx.x & 31;
     WarpStage* stage = reinterpret_cast<WarpStage*>(eval_smem) + 2 * (threadIdx.x >> 5);
     const unsigned strips = ((unsigned)A.tiles + kStripTiles - 1) / kStripTiles;
@@ -428,6 +432,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     while (item < nstrips) {
         if (lane == 0) next = atomicAdd(tk, 1u);
         const Strip S = strip_setup(A, item, strips);
+        if (lane == 0) atomicAdd(&A.ctrl->strips[S.mode == EM_SIFT ? 1 : 0], 1ull);
         issue_tile(A, S, 0, stage[b]);
         double c2 = 0.0, c1 = 0.0, snum = 0.0, sden = 0.0;
         for (int i = 0; i < S.nt; ++i) {
@@ -453,7 +458,10 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
         item = __shfl_sync(0xffffffffu, next, 0);
     }
     __syncthreads();
-    if (threadIdx.x == 0) atomicMax(&A.ctrl->ev_t1, globaltimer());
+    if (threadIdx.x == 0) {
+        atomicMax(&A.ctrl->ev_t1, globaltimer());
+        span_end(A.ctrl, KID_EVAL, kstep_);
+    }
 }
 
 size_t eval_smem_bytes() { return sizeof(WarpStage) * 2 * (kEvalThreads / 32); }

@@ -237,6 +237,8 @@ __device__ void decide_after_eval(const Arena& A) {
 // tbase and applies extract_imf's control flow.
 __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
     pdl_begin();
+    const int kstep_ = A.ctrl->step;
+    if (threadIdx.x == 0) span_begin(A.ctrl, KID_SCAN);
     constexpr int W = kScanThreads / 32;
     __shared__ unsigned s_w[W];
     __shared__ double s_red[2][W];
@@ -335,6 +337,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
             C->ev_t1 = 0;
         }
     }
+    if (threadIdx.x == 0) span_end(A.ctrl, KID_SCAN, kstep_);
 }
 
 // ---------------------------------------------------------------- compact
@@ -364,6 +367,8 @@ constexpr int kCompactThreads = 128;
 constexpr int kCompactStrip = 16;
 __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
     pdl_begin();
+    const int kstep_ = A.ctrl->step;
+    if (threadIdx.x == 0) span_begin(A.ctrl, KID_COMPACT);
     __shared__ int s_last;
     __shared__ int sbuf[kCompactThreads / 32][2][kEvalTile / 2];  // one tile's ordered extrema per side
     Ctrl* C = A.ctrl;
@@ -456,6 +461,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
             C->done[1] = 0;
         }
     }
+    if (threadIdx.x == 0) span_end(A.ctrl, KID_COMPACT, kstep_);
 }
 
 // ------------------------------------------------------------------ solve
@@ -592,6 +598,9 @@ __device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) 
 
 __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena A) {
     pdl_begin();
+    const int kstep_ = A.ctrl->step;
+    if (threadIdx.x == 0) span_begin(A.ctrl, KID_SOLVE);
+    if (threadIdx.x == 0 && blockIdx.x == 0) span_fold(A.ctrl, (kstep_ & 1) ^ 1);
     const bool prof_on = (A.debug & 2) && A.prof;
     long long prof_t = clock64();
     extern __shared__ double sm[];
@@ -929,6 +938,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             C->done[2] = 0;
         }
     }
+    if (tid == 0) span_end(A.ctrl, KID_SOLVE, kstep_);
 }
 
 // ------------------------------------------------------------------ final
@@ -976,6 +986,8 @@ __device__ void decide_after_final(const Arena& A) {
 
 __global__ void __launch_bounds__(256) k_final(Arena A) {
     pdl_begin();
+    const int kstep_ = A.ctrl->step;
+    if (threadIdx.x == 0) span_begin(A.ctrl, KID_FINAL);
     __shared__ unsigned s_ticket;
     __shared__ int s_last;
     __shared__ FinalSlot tab[kFinalChunk];
@@ -1164,6 +1176,7 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
             C->done[3] = 0;
         }
     }
+    if (threadIdx.x == 0) span_end(A.ctrl, KID_FINAL, kstep_);
 }
 
 // --------------------------------------------------------------- launchers

@@ -120,7 +120,37 @@ struct Ctrl {
     unsigned long long ev_t0;  // k_eval span of this step (globaltimer): min CTA start, max CTA end
     unsigned long long ev_t1;
     unsigned long long ev_ns;  // accumulated k_eval spans of this run (timing mode)
+    // per-kernel device spans (globaltimer), double-buffered by step parity: [p][kernel][0] = max
+    // of ~start over CTAs (i.e. ~min start), [1] = max end; the next step's k_solve folds the
+    // previous step's spans into kns (profiling: semd_kernel_spans)
+    unsigned long long kt[2][5][2];
+    unsigned long long kns[5];     // solve, eval, scan, compact, final
+    unsigned long long strips[2];  // eval strips in DETECT/INIT mode, in SIFT mode
 };
+
+enum KernelId : int { KID_SOLVE = 0, KID_EVAL = 1, KID_SCAN = 2, KID_COMPACT = 3, KID_FINAL = 4 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// thread 0 of every CTA, after pdl_begin() / at the end of the kernel
+__device__ __forceinline__ void span_begin(Ctrl* C, int id) {
+    atomicMax(&C->kt[C->step & 1][id][0], ~gtimer());
+}
+__device__ __forceinline__ void span_end(Ctrl* C, int id, int step) {
+    atomicMax(&C->kt[step & 1][id][1], gtimer());
+}
+// fold parity p's spans into kns and clear them (all of that step's kernels have completed)
+__device__ __forceinline__ void span_fold(Ctrl* C, int p) {
+    for (int id = 0; id < 5; ++id) {
+        const unsigned long long a = C->kt[p][id][0], b = C->kt[p][id][1];
+        if (a && b && b > ~a) C->kns[id] += b - ~a;
+        C->kt[p][id][0] = 0;
+        C->kt[p][id][1] = 0;
+    }
+}
 
 // Programmatic dependent launch: every step kernel starts with pdl_begin(): the grid
 // may be launched while its predecessor drains (launch latency and ramp overlap the
