@@ -375,6 +375,8 @@ struct semd_ctx {
         }
         span_strips[0] += c.strips[0];
         span_strips[1] += c.strips[1];
+        span_strips[2] += c.strip_cyc[0];
+        span_strips[3] += c.strip_cyc[1];
         if (c.hz_count > 0) {
             const int n = std::min(c.hz_count, kHzCap);
             const size_t old = h_hz.size();
@@ -397,7 +399,7 @@ struct semd_ctx {
     }
     long long trace_total = 0;
     double span_ms[5] = {};                 // device spans of the step kernels (semd_kernel_spans)
-    unsigned long long span_strips[2] = {};  // eval strips: DETECT/INIT mode, SIFT mode
+    unsigned long long span_strips[4] = {};  // eval strips: DETECT/INIT mode, SIFT mode; their warp cycles
     static constexpr int kHzCap = 4096;
     int debug_flags = 0;
     std::vector<int> h_hz;  // solve-hazard records since reset_stats (test hook)
@@ -1187,7 +1189,8 @@ int semd_solve_profile(semd_ctx* ctx, uint64_t* out) {
 }
 
 // Profiling hook: device spans (ms) of k_solve, k_eval, k_scan, k_compact, k_final summed over
-// the steps since the last call, and the eval strips processed in DETECT/INIT and SIFT mode.
+// the steps since the last call, and the eval strips processed in DETECT/INIT and SIFT mode
+// and their summed warp cycles (strips[4]).
 int semd_kernel_spans(semd_ctx* ctx, double* ms, uint64_t* strips) {
     return guard([&] {
         need_ctx(ctx);
@@ -1195,7 +1198,7 @@ int semd_kernel_spans(semd_ctx* ctx, double* ms, uint64_t* strips) {
             ms[i] = ctx->span_ms[i];
             ctx->span_ms[i] = 0.0;
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             strips[i] = ctx->span_strips[i];
             ctx->span_strips[i] = 0;
         }

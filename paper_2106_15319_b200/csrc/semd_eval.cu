@@ -213,6 +213,24 @@ __device__ __forceinline__ void issue_tile(const Arena& A, const Strip& S, int i
     }
 }
 
+// DETECT passes stream samples only: the stage's row area holds kDetChunk tiles, so one bulk
+// copy (staged from the chunk's base - 2) feeds kDetChunk tiles and the per-tile copy latency
+// is amortised.
+constexpr int kDetChunk = 4;
+static_assert((kDetChunk * kEvalTile + 2) * sizeof(double) <= sizeof(WarpStage) - sizeof(unsigned long long),
+              "a DETECT chunk fits one stage");
+__device__ __forceinline__ double* stage_flat(WarpStage& st) { return reinterpret_cast<double*>(&st); }
+__device__ __forceinline__ void issue_chunk(const Strip& S, int c, WarpStage& st) {
+    if ((threadIdx.x & 31) != 0) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
+    const int base = (S.j0 + c * kDetChunk) * kEvalTile;
+    const int end = (S.j0 + min(S.nt, (c + 1) * kDetChunk)) * kEvalTile;  // <= Lp (whole tiles)
+    const int e0 = base > 0 ? base - 2 : 0;                                 // 16-byte aligned
+    const unsigned sb = (unsigned)(end - e0) * 8u;
+    bar_arrive_tx(&st.bar, sb);
+    bulk_g2s(stage_flat(st) + (e0 - (base - 2)), S.src + e0, sb, &st.bar);
+}
+
 __device__ __forceinline__ int smem_search(const double4* R, int hi, double t) {  // last q <= hi with x_q < t
     int lo = 0;
     while (lo < hi) {
@@ -227,11 +245,11 @@ __device__ __forceinline__ int smem_search(const double4* R, int hi, double t) {
 // kSpt = 4 consecutive samples per lane; c2/c1 carry the new values at base-2/base-1.
 // Interior: the whole tile and its detection windows lie inside [1, L-2] (every tile but the
 // first and the last of a slot) -- no per-sample bound checks.
-template <bool Interior>
-__device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i, WarpStage& st, double& c2,
-                                          double& c1, double& snum, double& sden) {
+template <bool Interior, bool Det>
+__device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i, const WarpStage& st,
+                                          const double* samp, double& c2, double& c1, double& snum, double& sden) {
     const int lane = threadIdx.x & 31;
-    const int mode = S.mode;
+    const int mode = Det ? (int)EM_DETECT : S.mode;  // Det: the chunked DETECT loop
     const int L = A.L;
     const int j = S.j0 + i;
     const int base = j * kEvalTile;
@@ -250,7 +268,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
             if (mode == EM_INIT) {
                 cc[u] = init_value(A, S.slot, t);
             } else if (mode == EM_DETECT) {
-                cc[u] = st.samp[u];
+                cc[u] = samp[u];
             } else {
                 const double tt = (double)t;
                 double e[2];
@@ -262,7 +280,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
                     const double h = r1.x - r0.x;
                     e[s] = spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
                 }
-                cc[u] = st.samp[u] - 0.5 * (e[0] + e[1]);
+                cc[u] = samp[u] - 0.5 * (e[0] + e[1]);
             }
         }
         c2 = cc[0];
@@ -281,7 +299,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
             cv[k] = t < L ? (kind == 1 ? a[t] + beta * b[t] : a[t]) : 0.0;
         }
     } else {
-        const double* sp = st.samp + 2 + lane * kSpt;
+        const double* sp = samp + 2 + lane * kSpt;
 #pragma unroll
         for (int k = 0; k < kSpt; k += 2) {
             const double2 v = *reinterpret_cast<const double2*>(sp + k);
@@ -432,20 +450,42 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     while (item < nstrips) {
         if (lane == 0) next = atomicAdd(tk, 1u);
         const Strip S = strip_setup(A, item, strips);
-        if (lane == 0) atomicAdd(&A.ctrl->strips[S.mode == EM_SIFT ? 1 : 0], 1ull);
-        issue_tile(A, S, 0, stage[b]);
+        const long long cyc0 = clock64();
         double c2 = 0.0, c1 = 0.0, snum = 0.0, sden = 0.0;
-        for (int i = 0; i < S.nt; ++i) {
-            if (i + 1 < S.nt) issue_tile(A, S, i + 1, stage[b ^ 1]);
-            bar_wait(&stage[b].bar, (phase >> b) & 1u);
-            phase ^= 1u << b;
-            const int base = (S.j0 + i) * kEvalTile;
-            if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
-                eval_tile<true>(A, S, i, stage[b], c2, c1, snum, sden);
-            else
-                eval_tile<false>(A, S, i, stage[b], c2, c1, snum, sden);
-            __syncwarp();  // stage b is refilled next
-            b ^= 1;
+        if (S.mode == EM_DETECT) {
+            const int nch = (S.nt + kDetChunk - 1) / kDetChunk;
+            issue_chunk(S, 0, stage[b]);
+            for (int c = 0; c < nch; ++c) {
+                if (c + 1 < nch) issue_chunk(S, c + 1, stage[b ^ 1]);
+                bar_wait(&stage[b].bar, (phase >> b) & 1u);
+                phase ^= 1u << b;
+                const double* flat = stage_flat(stage[b]);
+                const int i1 = min(S.nt, (c + 1) * kDetChunk);
+                for (int i = c * kDetChunk; i < i1; ++i) {
+                    const int base = (S.j0 + i) * kEvalTile;
+                    const double* sp = flat + (i - c * kDetChunk) * kEvalTile;
+                    if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
+                        eval_tile<true, true>(A, S, i, stage[b], sp, c2, c1, snum, sden);
+                    else
+                        eval_tile<false, true>(A, S, i, stage[b], sp, c2, c1, snum, sden);
+                }
+                __syncwarp();  // stage b is refilled next
+                b ^= 1;
+            }
+        } else {
+            issue_tile(A, S, 0, stage[b]);
+            for (int i = 0; i < S.nt; ++i) {
+                if (i + 1 < S.nt) issue_tile(A, S, i + 1, stage[b ^ 1]);
+                bar_wait(&stage[b].bar, (phase >> b) & 1u);
+                phase ^= 1u << b;
+                const int base = (S.j0 + i) * kEvalTile;
+                if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
+                    eval_tile<true, false>(A, S, i, stage[b], stage[b].samp, c2, c1, snum, sden);
+                else
+                    eval_tile<false, false>(A, S, i, stage[b], stage[b].samp, c2, c1, snum, sden);
+                __syncwarp();  // stage b is refilled next
+                b ^= 1;
+            }
         }
         if (S.mode == EM_SIFT) {
             snum = warp_sum(snum);
@@ -454,6 +494,10 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
                 A.tnum[tsd_off(A, S.slot) + S.j0 / kStripTiles] = snum;
                 A.tden[tsd_off(A, S.slot) + S.j0 / kStripTiles] = sden;
             }
+        }
+        if (lane == 0) {
+            atomicAdd(&A.ctrl->strips[S.mode == EM_SIFT ? 1 : 0], 1ull);
+            atomicAdd(&A.ctrl->strip_cyc[S.mode == EM_SIFT ? 1 : 0], (unsigned long long)(clock64() - cyc0));
         }
         item = __shfl_sync(0xffffffffu, next, 0);
     }

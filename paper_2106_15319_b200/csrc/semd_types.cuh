@@ -126,6 +126,7 @@ struct Ctrl {
     unsigned long long kt[2][5][2];
     unsigned long long kns[5];     // solve, eval, scan, compact, final
     unsigned long long strips[2];  // eval strips in DETECT/INIT mode, in SIFT mode
+    unsigned long long strip_cyc[2];  // SM cycles spent on those strips (clock64, per warp)
 };
 
 enum KernelId : int { KID_SOLVE = 0, KID_EVAL = 1, KID_SCAN = 2, KID_COMPACT = 3, KID_FINAL = 4 };

@@ -25,7 +25,7 @@ c = se.context()
 sums = torch.zeros((64, n), dtype=torch.float64, device="cuda")
 k = C.c_size_t()
 ms = (C.c_double * 5)()
-strips = (C.c_uint64 * 2)()
+strips = (C.c_uint64 * 4)()
 
 
 def run(nr):
@@ -49,4 +49,6 @@ for _ in range(2):
     print(key, "nr", nr, "wall %.1f ms" % (el * 1e3), "steps", st["steps"], "waves", st["waves"],
           "sifted %.3e" % st["sifted_samples"], "rate %.3e" % (st["sifted_samples"] / el), flush=True)
     print("   spans ms: " + "  ".join("%s %.1f (%.0f%%)" % (a, b, 100 * b / el / 1e3) for a, b in zip(names, ms)),
-          " sum %.1f" % tot, " strips detect %d sift %d" % (strips[0], strips[1]), flush=True)
+          " sum %.1f" % tot, " strips detect %d sift %d" % (strips[0], strips[1]),
+          " warp-cycles/strip detect %.0f sift %.0f" % (strips[2] / max(1, strips[0]), strips[3] / max(1, strips[1])),
+          flush=True)
