@@ -360,9 +360,9 @@ __device__ void emit_trace(const Arena& A, const Slot& S, uint64_t h) {
     }
 }
 
-// One warp per (compact slot, side, strip of 16 tiles) item, grid-stride: lanes load
-// the strip's tile counts and offsets in one coalesced access, then the warp
-// copies each tile's extrema (16 tiles x <= 64 knots).
+// One warp per (compact slot, strip of 16 tiles) item, grid-stride: lanes load the
+// strip's tile offsets in one coalesced access and the 16 detection words of their
+// lane; each lane then writes its own extrema of both sides to the knot lists.
 constexpr int kCompactThreads = 128;
 constexpr int kCompactStrip = 16;
 __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
@@ -370,11 +370,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
     const int kstep_ = A.ctrl->step;
     if (threadIdx.x == 0) span_begin(A.ctrl, KID_COMPACT);
     __shared__ int s_last;
-    __shared__ int sbuf[kCompactThreads / 32][2][kEvalTile / 2];  // one tile's ordered extrema per side
     Ctrl* C = A.ctrl;
     const int lane = threadIdx.x & 31;
     const int wpb = kCompactThreads / 32;
-    int(*sb)[kEvalTile / 2] = sbuf[threadIdx.x >> 5];
     const int strips = (A.tiles + kCompactStrip - 1) / kCompactStrip;
     const unsigned nitems = (unsigned)C->n_compact * (unsigned)strips;
     const bool tracing = A.trace != nullptr;
@@ -390,41 +388,32 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
             off1 = toff_view(A, cpar, 1, s)[j0 + lane];
         }
         // eval's per-lane detection words: window flags of samples t0-1 .. t0+2 and the lane's
-        // rank among the tile's extrema of each side; ranked into shared memory, then written
-        // to the knot lists coalesced
+        // rank among the tile's extrema of each side. Extremum e of a lane lands at knot
+        // toff[tile] + rank + e: every lane writes its own (the tile's knots are contiguous)
         const unsigned* wd = A.tflags + tfl_off(A, cpar, s) + (size_t)j0 * 32 + lane;
-        int* gi0 = A.kidx + knot_off(A, cpar, 0, s);
-        int* gi1 = A.kidx + knot_off(A, cpar, 1, s);
+        int* gi[2] = {A.kidx + knot_off(A, cpar, 0, s), A.kidx + knot_off(A, cpar, 1, s)};
         uint64_t h0 = 0, h1 = 0;
-        unsigned wn = wd[0];
-        for (int u = 0; u < nt; ++u) {
-            const unsigned w = wn;
-            if (u + 1 < nt) wn = wd[(u + 1) * 32];
+        unsigned wv[kCompactStrip];  // all of the strip's words in flight at once
+#pragma unroll
+        for (int u = 0; u < kCompactStrip; ++u) wv[u] = u < nt ? __ldcs(wd + u * 32) : 0u;
+#pragma unroll
+        for (int u = 0; u < kCompactStrip; ++u) {
+            const unsigned w = wv[u];
             const int p0 = (j0 + u) * kEvalTile + lane * kSpt - 1;
-            unsigned n[2];
+            const unsigned o[2] = {__shfl_sync(0xffffffffu, off0, u), __shfl_sync(0xffffffffu, off1, u)};
 #pragma unroll
             for (int side = 0; side < 2; ++side) {
                 const unsigned fl = (w >> (4 * side)) & 0xFu;
-                const unsigned r = (w >> (8 + 8 * side)) & 0xFFu;
+                const unsigned r = o[side] + ((w >> (8 + 8 * side)) & 0xFFu);
 #pragma unroll
-                for (int k = 0; k < kSpt; ++k)
-                    if ((fl >> k) & 1u) sb[side][r + __popc(fl & ((1u << k) - 1u))] = p0 + k;
-                n[side] = __reduce_add_sync(0xffffffffu, (unsigned)__popc(fl));
+                for (int k = 0; k < kSpt; ++k) {
+                    if ((fl >> k) & 1u) {
+                        const unsigned q = r + __popc(fl & ((1u << k) - 1u));
+                        gi[side][q] = p0 + k;
+                        if (tracing) (side ? h1 : h0) += knot_hash(side, q, (unsigned)(p0 + k));
+                    }
+                }
             }
-            __syncwarp();
-            const unsigned o0 = __shfl_sync(0xffffffffu, off0, u);
-            const unsigned o1 = __shfl_sync(0xffffffffu, off1, u);
-            for (unsigned i = lane; i < n[0]; i += 32) {
-                const int t = sb[0][i];
-                gi0[o0 + i] = t;
-                if (tracing) h0 += knot_hash(0, o0 + i, (unsigned)t);
-            }
-            for (unsigned i = lane; i < n[1]; i += 32) {
-                const int t = sb[1][i];
-                gi1[o1 + i] = t;
-                if (tracing) h1 += knot_hash(1, o1 + i, (unsigned)t);
-            }
-            __syncwarp();
         }
         if (tracing) {
             h0 = warp_sum(h0);
