@@ -102,14 +102,20 @@ __device__ __noinline__ unsigned plateau_flags(const Arena& A, int slot, int mod
 // ------------------------------------------------------------- staging
 
 constexpr int kWarpRows = kEvalTile / 2 + 6;  // table rows one tile can touch per side
-constexpr int kWarpSamp = kEvalTile + 8;      // staged samples [base-2, base+T)
-
+// A stage holds one group of g consecutive tiles, laid out
+//   samples [base-2, base + g*T)  |  g x 32 detection words (SIFT)  |  rows side 0  |  rows side 1
+// (one bulk copy each). SIFT groups take as many tiles (<= kGroupMax) as fit; one tile
+// always fits (kWarpRows rows per side).
+constexpr int kStageBytes = 7040;
+constexpr int kGroupMax = 4;
 struct alignas(16) WarpStage {
-    double4 rows[2][kWarpRows];
-    double samp[kWarpSamp];
-    unsigned ow[32];          // SIFT: the previous detection's per-lane words of this tile (tflags)
-    unsigned long long bar;   // mbarrier: the tile's bulk copies have landed
+    double flat[kStageBytes / 8];
+    unsigned long long bar;  // mbarrier: the group's bulk copies have landed
 };
+__host__ __device__ constexpr int group_bytes(int g, int rows) {
+    return (g * kEvalTile + 2) * 8 + g * 32 * 4 + rows * 32;
+}
+static_assert(group_bytes(1, 2 * kWarpRows) <= kStageBytes, "one SIFT tile fits a stage");
 
 constexpr int kStripTiles = 16;  // consecutive tiles one warp walks, carrying boundary values
 
@@ -181,45 +187,47 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
     return S;
 }
 
-// Issue tile i's copies (lane 0 arms the barrier; every call completes one phase).
-// Tile j's extrema are those of window [base-1, base+T-1); samples [base-2, base+T)
-// need table rows [toff[j], toff[j+1]+2].
-__device__ __forceinline__ void issue_tile(const Arena& A, const Strip& S, int i, WarpStage& st) {
-    int lo[2] = {0, 0}, hi[2] = {0, 0};
-    if (S.mode == EM_SIFT) {  // warp-uniform
+// SIFT group of tiles i .. i+g-1: as many tiles (<= kGroupMax, <= the strip) as fit a stage.
+// Tile j's extrema are those of window [base-1, base+T-1); its samples [base-2, base+T) need
+// table rows [toff[j], toff[j+1]+2], so the group needs rows [toff[j_i], toff[j_i+g]+2].
+__device__ __forceinline__ int group_tiles(const Strip& S, int i) {
+    const int lo0 = __shfl_sync(0xffffffffu, S.to[0], i), lo1 = __shfl_sync(0xffffffffu, S.to[1], i);
+    int g = 1;
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            lo[s] = __shfl_sync(0xffffffffu, S.to[s], i);
-            hi[s] = __shfl_sync(0xffffffffu, S.to[s], i + 1);
-        }
+    for (int c = 2; c <= kGroupMax; ++c) {
+        const int e = min(i + c, S.nt);  // lanes >= nt hold toff of the strip's end
+        const int rows = __shfl_sync(0xffffffffu, S.to[0], e) - lo0 + __shfl_sync(0xffffffffu, S.to[1], e) - lo1 + 6;
+        if (i + c <= S.nt && group_bytes(c, rows) <= kStageBytes) g = c;
     }
+    return g;
+}
+
+// Issue group (i, g)'s copies: samples, detection words, both sides' rows (lane 0 arms the barrier).
+__device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpStage& st) {
+    const int lo0 = __shfl_sync(0xffffffffu, S.to[0], i), lo1 = __shfl_sync(0xffffffffu, S.to[1], i);
+    const int n0 = __shfl_sync(0xffffffffu, S.to[0], i + g) + 3 - lo0;
+    const int n1 = __shfl_sync(0xffffffffu, S.to[1], i + g) + 3 - lo1;
     if ((threadIdx.x & 31) != 0) return;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
-    if (S.mode != EM_INIT) {
-        const int base = (S.j0 + i) * kEvalTile;
-        const int e0 = base > 0 ? base - 2 : 0;  // 16-byte aligned; Lp = whole tiles
-        const unsigned sb = (unsigned)(base + kEvalTile - e0) * 8u;
-        const unsigned r0 = S.mode == EM_SIFT ? (unsigned)(hi[0] + 3 - lo[0]) * 32u : 0u;
-        const unsigned r1 = S.mode == EM_SIFT ? (unsigned)(hi[1] + 3 - lo[1]) * 32u : 0u;
-        bar_arrive_tx(&st.bar, sb + r0 + r1 + (S.mode == EM_SIFT ? 128u : 0u));
-        bulk_g2s(&st.samp[e0 - (base - 2)], S.src + e0, sb, &st.bar);
-        if (S.mode == EM_SIFT) {
-            bulk_g2s(st.rows[0], S.tab0 + lo[0], r0, &st.bar);
-            bulk_g2s(st.rows[1], S.tab1 + lo[1], r1, &st.bar);
-            bulk_g2s(st.ow, S.ow + i * 32, 128u, &st.bar);
-        }
-    } else {
-        bar_arrive_tx(&st.bar, 0u);
-    }
+    const int base = (S.j0 + i) * kEvalTile;
+    const int e0 = base > 0 ? base - 2 : 0;  // 16-byte aligned; Lp = whole tiles
+    const unsigned sb = (unsigned)(base + g * kEvalTile - e0) * 8u;
+    double* f = st.flat;
+    unsigned* ow = reinterpret_cast<unsigned*>(f + g * kEvalTile + 2);
+    double4* r0 = reinterpret_cast<double4*>(ow + g * 32);
+    bar_arrive_tx(&st.bar, sb + (unsigned)g * 128u + (unsigned)(n0 + n1) * 32u);
+    bulk_g2s(f + (e0 - (base - 2)), S.src + e0, sb, &st.bar);
+    bulk_g2s(ow, S.ow + i * 32, (unsigned)g * 128u, &st.bar);
+    bulk_g2s(r0, S.tab0 + lo0, (unsigned)n0 * 32u, &st.bar);
+    bulk_g2s(r0 + n0, S.tab1 + lo1, (unsigned)n1 * 32u, &st.bar);
 }
 
 // DETECT passes stream samples only: the stage's row area holds kDetChunk tiles, so one bulk
 // copy (staged from the chunk's base - 2) feeds kDetChunk tiles and the per-tile copy latency
 // is amortised.
-constexpr int kDetChunk = 4;
-static_assert((kDetChunk * kEvalTile + 2) * sizeof(double) <= sizeof(WarpStage) - sizeof(unsigned long long),
-              "a DETECT chunk fits one stage");
-__device__ __forceinline__ double* stage_flat(WarpStage& st) { return reinterpret_cast<double*>(&st); }
+constexpr int kDetChunk = 6;
+static_assert((kDetChunk * kEvalTile + 2) * 8 <= kStageBytes, "a DETECT chunk fits one stage");
+__device__ __forceinline__ double* stage_flat(WarpStage& st) { return st.flat; }
 __device__ __forceinline__ void issue_chunk(const Strip& S, int c, WarpStage& st) {
     if ((threadIdx.x & 31) != 0) return;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
@@ -245,11 +253,12 @@ __device__ __forceinline__ int smem_search(const double4* R, int hi, double t) {
 // kSpt = 4 consecutive samples per lane; c2/c1 carry the new values at base-2/base-1.
 // Interior: the whole tile and its detection windows lie inside [1, L-2] (every tile but the
 // first and the last of a slot) -- no per-sample bound checks.
-template <bool Interior, bool Det>
-__device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i, const WarpStage& st,
-                                          const double* samp, double& c2, double& c1, double& snum, double& sden) {
+template <bool Interior, int M>
+__device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i, const double* samp,
+                                          const unsigned* ows, const double4* R0, const double4* R1, double& c2,
+                                          double& c1, double& snum, double& sden) {
     const int lane = threadIdx.x & 31;
-    const int mode = Det ? (int)EM_DETECT : S.mode;  // Det: the chunked DETECT loop
+    constexpr int mode = M;  // the pass's mode (each loop instantiates its own)
     const int L = A.L;
     const int j = S.j0 + i;
     const int base = j * kEvalTile;
@@ -274,7 +283,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
                 double e[2];
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
-                    const double4* R = st.rows[s];
+                    const double4* R = s ? R1 : R0;
                     const int qq = smem_search(R, qmax[s], tt);
                     const double4 r0 = R[qq], r1 = R[qq + 1];
                     const double h = r1.x - r0.x;
@@ -315,11 +324,11 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         // seg(t) = 1 + #(window extrema at positions < t): the previous detection stored, per
         // lane, its flags for window positions t0-1 .. t0+2 and its rank among the tile's
         // extrema of each side; each further sample adds the extrema it passes.
-        const unsigned ow = st.ow[lane];
+        const unsigned ow = ows[lane];
         double env0[kSpt];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            const double4* R = st.rows[s];
+            const double4* R = s ? R1 : R0;
             const unsigned fl = (ow >> (4 * s)) & 0xFu;  // window positions t0-1 .. t0+2
             const int q0 = 1 + (int)((ow >> (8 + 8 * s)) & 0xFFu) + (int)(fl & 1u);
 #pragma unroll
@@ -465,27 +474,45 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
                     const int base = (S.j0 + i) * kEvalTile;
                     const double* sp = flat + (i - c * kDetChunk) * kEvalTile;
                     if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
-                        eval_tile<true, true>(A, S, i, stage[b], sp, c2, c1, snum, sden);
+                        eval_tile<true, EM_DETECT>(A, S, i, sp, nullptr, nullptr, nullptr, c2, c1, snum, sden);
                     else
-                        eval_tile<false, true>(A, S, i, stage[b], sp, c2, c1, snum, sden);
+                        eval_tile<false, EM_DETECT>(A, S, i, sp, nullptr, nullptr, nullptr, c2, c1, snum, sden);
                 }
                 __syncwarp();  // stage b is refilled next
                 b ^= 1;
             }
-        } else {
-            issue_tile(A, S, 0, stage[b]);
-            for (int i = 0; i < S.nt; ++i) {
-                if (i + 1 < S.nt) issue_tile(A, S, i + 1, stage[b ^ 1]);
+        } else if (S.mode == EM_SIFT) {
+            int g = group_tiles(S, 0);
+            issue_group(S, 0, g, stage[b]);
+            for (int i = 0; i < S.nt;) {
+                const int gn = i + g < S.nt ? group_tiles(S, i + g) : 0;
+                if (gn) issue_group(S, i + g, gn, stage[b ^ 1]);
                 bar_wait(&stage[b].bar, (phase >> b) & 1u);
                 phase ^= 1u << b;
-                const int base = (S.j0 + i) * kEvalTile;
-                if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
-                    eval_tile<true, false>(A, S, i, stage[b], stage[b].samp, c2, c1, snum, sden);
-                else
-                    eval_tile<false, false>(A, S, i, stage[b], stage[b].samp, c2, c1, snum, sden);
+                const double* flat = stage_flat(stage[b]);
+                const unsigned* ows = reinterpret_cast<const unsigned*>(flat + g * kEvalTile + 2);
+                const double4* R0 = reinterpret_cast<const double4*>(ows + g * 32);
+                const int lo0 = __shfl_sync(0xffffffffu, S.to[0], i), lo1 = __shfl_sync(0xffffffffu, S.to[1], i);
+                const double4* R1 = R0 + (__shfl_sync(0xffffffffu, S.to[0], i + g) + 3 - lo0);
+                for (int u = 0; u < g; ++u) {
+                    const int t = i + u;
+                    const int base = (S.j0 + t) * kEvalTile;
+                    const double4* T0 = R0 + (__shfl_sync(0xffffffffu, S.to[0], t) - lo0);
+                    const double4* T1 = R1 + (__shfl_sync(0xffffffffu, S.to[1], t) - lo1);
+                    const double* sp = flat + u * kEvalTile;
+                    if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
+                        eval_tile<true, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, c2, c1, snum, sden);
+                    else
+                        eval_tile<false, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, c2, c1, snum, sden);
+                }
                 __syncwarp();  // stage b is refilled next
                 b ^= 1;
+                i += g;
+                g = gn;
             }
+        } else {  // INIT: values computed from the job's inputs, nothing staged
+            for (int i = 0; i < S.nt; ++i)
+                eval_tile<false, EM_INIT>(A, S, i, nullptr, nullptr, nullptr, nullptr, c2, c1, snum, sden);
         }
         if (S.mode == EM_SIFT) {
             snum = warp_sum(snum);
