@@ -716,10 +716,12 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             const int ws = max(1, cs - W0);
             double d, r;
             fwd_first(cx, ws, d, r);  // exact when ws == 1, otherwise a guess
+#pragma unroll 4
             for (int i = ws + 1; i < cs; ++i) fwd_step(cx, i, d, r);
             if (ws < cs) fwd_step(cx, cs, d, r);
             DP[spad(cs - wa)] = d;
             RP[spad(cs - wa)] = r;
+#pragma unroll 4
             for (int i = cs + 1; i < ce; ++i) {
                 fwd_step(cx, i, d, r);
                 DP[spad(i - wa)] = d;
@@ -768,6 +770,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         if (back) {
             const int top = min(ce + W0, rb);
             double m = 0.0;  // exact when top == N-1, otherwise a guess
+#pragma unroll 4
             for (int i = top - 1; i >= cs; --i) {
                 m = div_rn(RP[spad(i - wa)] - upper(i) * m, DP[spad(i - wa)], RHS[spad(i - wa)]);
                 if (i < ce) M[spad(i - wa)] = m;
