@@ -403,21 +403,20 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         }
     }
 
-    // tile-local ranks (warp scan of packed counts): with the flags they are the tile's ordered
-    // extrema lists, expanded into the knot lists by k_compact and read back by the next sift
-    const unsigned packed = (unsigned)__popc(fmax) | ((unsigned)__popc(fmin) << 16);
-    unsigned incl = packed;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-    const unsigned excl = incl - packed;
-    S.nw[i * 32 + lane] = fmax | (fmin << 4) | ((excl & 0xFFu) << 8) | ((excl >> 16) << 16);
+    // tile-local ranks: with the flags they are the tile's ordered extrema lists, expanded into
+    // the knot lists by k_compact and read back by the next sift. A lane holds at most 2 extrema
+    // of a side (no two maxima or minima are adjacent), so the exclusive prefix of the per-lane
+    // counts is two ballots per side (count bits 0 and 1) instead of a shuffle scan.
+    const unsigned nmax = (unsigned)__popc(fmax), nmin = (unsigned)__popc(fmin);
+    const unsigned a0 = __ballot_sync(0xffffffffu, nmax & 1u), a1 = __ballot_sync(0xffffffffu, nmax >> 1);
+    const unsigned b0 = __ballot_sync(0xffffffffu, nmin & 1u), b1 = __ballot_sync(0xffffffffu, nmin >> 1);
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned emax = (unsigned)__popc(a0 & lt) + 2u * (unsigned)__popc(a1 & lt);
+    const unsigned emin = (unsigned)__popc(b0 & lt) + 2u * (unsigned)__popc(b1 & lt);
+    S.nw[i * 32 + lane] = fmax | (fmin << 4) | (emax << 8) | (emin << 16);
     if (lane == 0) {
-        S.cnt0[i] = total & 0xFFFF;
-        S.cnt0[i + (size_t)A.G * tiles4(A)] = total >> 16;
+        S.cnt0[i] = (unsigned)__popc(a0) + 2u * (unsigned)__popc(a1);
+        S.cnt0[i + (size_t)A.G * tiles4(A)] = (unsigned)__popc(b0) + 2u * (unsigned)__popc(b1);
     }
 }
 
