@@ -994,14 +994,29 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
     // (each thread: one element, every finalising slot in slot order).
     const bool split = nf > 1 && tiles * 2 < (int)gridDim.x;
     if (split) {
+        // Static assignment (no ticket atomics: thousands of short items would serialise on one
+        // counter): CTAs [0, nS) take one element block each -- the long, ordered accumulations
+        // start first -- and the remaining CTAs stride over the (slot, tile) residue items.
         const unsigned nR = (unsigned)nf * (unsigned)tiles;
         const unsigned nS = (unsigned)((L + 255) / 256);
-        while (true) {
-            if (threadIdx.x == 0) s_ticket = atomicAdd(&C->ticket[3], 1u);
-            __syncthreads();
-            const unsigned q = s_ticket;
-            __syncthreads();
-            if (q >= nR + nS) break;
+        const unsigned G = gridDim.x;
+        const bool sep = nS < G;  // else every CTA strides over all items
+        const unsigned rb = sep ? nS : 0u, rs = sep ? G - nS : G;
+        for (unsigned k = 0;; ++k) {
+            unsigned q;
+            if (sep && blockIdx.x < nS) {
+                if (k > 0) break;
+                q = nR + blockIdx.x;
+            } else {
+                const unsigned r = (blockIdx.x - rb) + k * rs;
+                if (sep) {
+                    if (r >= nR) break;
+                    q = r;
+                } else {
+                    if (r >= nR + nS) break;
+                    q = r;
+                }
+            }
             if (q < nR) {  // R = X - imf (emd.cpp:167), imf_out / res_out copies
                 const int li = (int)(q / (unsigned)tiles), tq = (int)(q % (unsigned)tiles);
                 const int sl = A.final_list[li];
@@ -1009,13 +1024,15 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
                 const double* x = A.bufs + buf_off(A, sl, S.xb);
                 const double* imf = S.cb >= 0 ? A.bufs + buf_off(A, sl, S.cb) : x;
                 double* res = A.bufs + buf_off(A, sl, pick_free_buffer(S.xb, S.cb));
+                double* const io = S.imf_out;
+                double* const ro = S.res_out;
                 for (size_t t = (size_t)tq * kFinalTile + threadIdx.x; t < min(L, (size_t)(tq + 1) * kFinalTile);
                      t += 256) {
                     const double iv = imf[t];
                     const double rv = x[t] - iv;
                     res[t] = rv;
-                    if (S.imf_out) S.imf_out[t] = iv;
-                    if (S.res_out) S.res_out[t] = rv;
+                    if (io) io[t] = iv;
+                    if (ro) ro[t] = rv;
                 }
             } else {  // sums[k0+k][t] += imf_s[t] in slot order (emd.cpp:249-251)
                 const size_t t = (size_t)(q - nR) * 256 + threadIdx.x;
