@@ -399,19 +399,17 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
 #pragma unroll
         for (int u = 0; u < kCompactStrip; ++u) {
             const unsigned w = wv[u];
+            if (!__any_sync(0xffffffffu, (w & 0xFFu) != 0u)) continue;  // no extrema in the tile (sparse IMFs)
             const int p0 = (j0 + u) * kEvalTile + lane * kSpt - 1;
             const unsigned o[2] = {__shfl_sync(0xffffffffu, off0, u), __shfl_sync(0xffffffffu, off1, u)};
 #pragma unroll
             for (int side = 0; side < 2; ++side) {
-                const unsigned fl = (w >> (4 * side)) & 0xFu;
-                const unsigned r = o[side] + ((w >> (8 + 8 * side)) & 0xFFu);
-#pragma unroll
-                for (int k = 0; k < kSpt; ++k) {
-                    if ((fl >> k) & 1u) {
-                        const unsigned q = r + __popc(fl & ((1u << k) - 1u));
-                        gi[side][q] = p0 + k;
-                        if (tracing) (side ? h1 : h0) += knot_hash(side, q, (unsigned)(p0 + k));
-                    }
+                unsigned fl = (w >> (4 * side)) & 0xFu;
+                unsigned q = o[side] + ((w >> (8 + 8 * side)) & 0xFFu);
+                for (; fl; fl &= fl - 1u, ++q) {  // the lane's extrema in order (at most 2)
+                    const int t = p0 + __ffs(fl) - 1;
+                    gi[side][q] = t;
+                    if (tracing) (side ? h1 : h0) += knot_hash(side, q, (unsigned)t);
                 }
             }
         }
