@@ -495,6 +495,7 @@ __device__ __forceinline__ void fwd_step(const SolveCtx& c, int i, double& d, do
 struct SolveShared {
     unsigned ticket;
     int item, b, last, any;
+    int pf, pf_lo;  // the next block's knot indices were bulk-copied to the idx buffer from rank pf_lo
     int dirty[kSolveMaxChains];
     int moved[kSolveMaxChains];
 };
@@ -583,6 +584,15 @@ __device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) 
         }                                                                          \
     } while (0)
 
+// Staged rows [wa, wb] of block b of an N-row system (see k_solve).
+__device__ __forceinline__ void solve_window(int b, int N, int& wa, int& wb) {
+    const int r0 = 1 + b * kSolveBlock;
+    const int r1 = min(r0 + kSolveBlock, N - 1);
+    wb = min(r1 + kSolveHalo, N - 1);
+    wa = max(0, max(1, r0 - kSolveHalo) - kSolveWarm - 1);
+}
+constexpr int kSolveIdxBuf = kSolveWin + 8;  // ints: one window's knot ranks, 16-byte aligned both ends
+
 __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena A) {
     pdl_begin();
     const int kstep_ = A.ctrl->step;
@@ -596,6 +606,11 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
     const int tid = threadIdx.x;
     const int nblocks = C->solve_blocks;
     const int nitems = C->n_solve;
+    // the next block's knot indices are bulk-copied into IB while this block is solved, so its
+    // staging waits only for the dependent value gather
+    int* IB = reinterpret_cast<int*>(sm + 5 * kSolvePadWin);
+    unsigned long long* pbar = reinterpret_cast<unsigned long long*>(IB + kSolveIdxBuf);
+    unsigned pfph = 0;  // parity of the idx buffer's next completion
     // dynamic block tickets (C->ticket[2]); the (slot, side) item of a block is the last i
     // with solve_off[i] <= block. The next ticket and its item are fetched by an idle helper
     // thread during this block's forward sweep.
@@ -611,6 +626,8 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
     if (tid == 0) {
         sh.b = (int)atomicAdd(&C->ticket[2], 1u);
         if (sh.b < nblocks) sh.item = find_item(sh.b, 0);
+        sh.pf = 0;
+        bar_init(pbar);
     }
     __syncthreads();
     while (true) {
@@ -620,10 +637,29 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         const int code = A.solve_item[item];
         const int slot = code >> 1, side = code & 1, b = blk - A.solve_off[item];
         __syncthreads();  // sh.b / sh.item consumed
-        auto prefetch = [&]() {  // one thread: the next block and its item
+        auto prefetch = [&]() {  // one thread: the next block, its item and its knot indices
             const int nb2 = (int)atomicAdd(&C->ticket[2], 1u);
             sh.b = nb2;
-            if (nb2 < nblocks) sh.item = find_item(nb2, item);
+            sh.pf = 0;
+            if (nb2 >= nblocks) return;
+            const int it2 = find_item(nb2, item);
+            sh.item = it2;
+            const int code2 = A.solve_item[it2];
+            const int sl2 = code2 >> 1, sd2 = code2 & 1;
+            const Slot& S2 = A.slots[sl2];
+            const int n2 = (int)S2.n[sd2];
+            if (n2 + 2 <= kSolveSeqMax) return;  // solve_small: no staging
+            int wa2, wb2;
+            solve_window(nb2 - A.solve_off[it2], n2 + 4, wa2, wb2);
+            const int rlo = wa2 <= 1 ? 0 : wa2 - 2;           // ranks of rows wa2..wb2 (vknot_rank)
+            const int rhi = wb2 >= n2 + 2 ? n2 - 1 : wb2 - 2;
+            const int lo4 = rlo & ~3;
+            const unsigned bytes = (unsigned)((rhi + 1 - lo4 + 3) & ~3) * 4u;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // IB's earlier generic reads
+            bar_arrive_tx(pbar, bytes);
+            bulk_g2s(IB, A.kidx + knot_off(A, S2.par, sd2, sl2) + lo4, bytes, pbar);
+            sh.pf = 1;
+            sh.pf_lo = lo4;
         };
         const Slot& S = A.slots[slot];
         KnotView kv;
@@ -658,10 +694,21 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             constexpr int U = (kSolveWin + kSolveThreads - 1) / kSolveThreads;
             int iv[U];
             double yv[U];
+            if (sh.pf) {  // prefetched during the previous block
+                bar_wait(pbar, pfph);
+                pfph ^= 1u;
+                const int lo = sh.pf_lo;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int q = u * kSolveThreads + tid;
-                if (q < wn) iv[u] = kv.idx[vknot_rank(kv.n, wa + q)];
+                for (int u = 0; u < U; ++u) {
+                    const int q = u * kSolveThreads + tid;
+                    if (q < wn) iv[u] = IB[vknot_rank(kv.n, wa + q) - lo];
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = u * kSolveThreads + tid;
+                    if (q < wn) iv[u] = kv.idx[vknot_rank(kv.n, wa + q)];
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -1189,7 +1236,7 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
 // --------------------------------------------------------------- launchers
 
 size_t solve_smem_bytes() {
-    const size_t chunked = (size_t)5 * kSolvePadWin * sizeof(double);
+    const size_t chunked = (size_t)5 * kSolvePadWin * sizeof(double) + kSolveIdxBuf * sizeof(int) + 8;
     const size_t seq = (size_t)4 * (kSolveSeqMax + 4) * sizeof(double);
     return chunked > seq ? chunked : seq;
 }
