@@ -247,8 +247,11 @@ struct semd_ctx {
         if (max_slots > 0) g = std::min<long long>(g, max_slots);
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
+        // the engine's own slot-scaled buffers count as available (they are reused or regrown)
+        const size_t held = bufs.bytes + kidx.bytes + toff.bytes + ktab.bytes + scnt.bytes + tnum.bytes + tden.bytes +
+                            thash.bytes + tflags.bytes + sb.bytes + noise.bytes;
         const long long per_slot = 94LL * L + 4096;  // slot buffers, knot lists, tables, detection words, noise
-        const long long mem_g = (long long)(0.5 * (double)free_b) / per_slot;
+        const long long mem_g = (long long)(0.5 * (double)(free_b + held)) / per_slot;
         g = std::max(1LL, std::min(g, mem_g));
         g = std::min<long long>(g, std::max(1, jobs));
         const long long waves = (std::max(1, jobs) + g - 1) / g;  // the same wave count, evenly filled
