@@ -496,6 +496,7 @@ struct SolveShared {
     unsigned ticket;
     int item, b, last, any;
     int pf, pf_lo;  // the next block's knot indices were bulk-copied to the idx buffer from rank pf_lo
+    int bb;         // block index of sh.b within its (slot, side) item
     int dirty[kSolveMaxChains];
     int moved[kSolveMaxChains];
 };
@@ -623,9 +624,27 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         }
         return lo;
     };
+    // A slot's two items (sides 0 and 1, consecutive in the lists) take their blocks
+    // alternately, so both envelopes' blocks over the same stretch of the candidate run
+    // together and the second side's value gathers hit L2.
+    auto decode = [&](int blk, int lo, int& it, int& bb) {
+        const int p = find_item(blk, lo) & ~1;
+        const int o = A.solve_off[p];
+        const int n0 = A.solve_off[p + 1] - o, n1 = A.solve_off[p + 2] - A.solve_off[p + 1];
+        const int t = blk - o, m = min(n0, n1);
+        int sd;
+        if (t < 2 * m) {
+            sd = t & 1;
+            bb = t >> 1;
+        } else {
+            sd = n0 > n1 ? 0 : 1;
+            bb = m + (t - 2 * m);
+        }
+        it = p + sd;
+    };
     if (tid == 0) {
         sh.b = (int)atomicAdd(&C->ticket[2], 1u);
-        if (sh.b < nblocks) sh.item = find_item(sh.b, 0);
+        if (sh.b < nblocks) decode(sh.b, 0, sh.item, sh.bb);
         sh.pf = 0;
         bar_init(pbar);
     }
@@ -635,22 +654,24 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         if (blk >= nblocks) break;
         const int item = sh.item;
         const int code = A.solve_item[item];
-        const int slot = code >> 1, side = code & 1, b = blk - A.solve_off[item];
+        const int slot = code >> 1, side = code & 1, b = sh.bb;
         __syncthreads();  // sh.b / sh.item consumed
         auto prefetch = [&]() {  // one thread: the next block, its item and its knot indices
             const int nb2 = (int)atomicAdd(&C->ticket[2], 1u);
             sh.b = nb2;
             sh.pf = 0;
             if (nb2 >= nblocks) return;
-            const int it2 = find_item(nb2, item);
+            int it2, bb2;
+            decode(nb2, item & ~1, it2, bb2);
             sh.item = it2;
+            sh.bb = bb2;
             const int code2 = A.solve_item[it2];
             const int sl2 = code2 >> 1, sd2 = code2 & 1;
             const Slot& S2 = A.slots[sl2];
             const int n2 = (int)S2.n[sd2];
             if (n2 + 2 <= kSolveSeqMax) return;  // solve_small: no staging
             int wa2, wb2;
-            solve_window(nb2 - A.solve_off[it2], n2 + 4, wa2, wb2);
+            solve_window(bb2, n2 + 4, wa2, wb2);
             const int rlo = wa2 <= 1 ? 0 : wa2 - 2;           // ranks of rows wa2..wb2 (vknot_rank)
             const int rhi = wb2 >= n2 + 2 ? n2 - 1 : wb2 - 2;
             const int lo4 = rlo & ~3;
