@@ -1092,12 +1092,23 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
                 double* res = A.bufs + buf_off(A, sl, pick_free_buffer(S.xb, S.cb));
                 double* const io = S.imf_out;
                 double* const ro = S.res_out;
-                for (size_t t = (size_t)tq * kFinalTile + threadIdx.x; t < min(L, (size_t)(tq + 1) * kFinalTile);
-                     t += 256) {
-                    const double iv = imf[t];
-                    const double rv = x[t] - iv;
+                // all of the item's loads first (the stores may alias them as far as the compiler
+                // knows, which would serialise the iterations on the load latency)
+                constexpr int kPer = kFinalTile / 256;
+                double iv[kPer], xv[kPer];
+#pragma unroll
+                for (int e = 0; e < kPer; ++e) {
+                    const size_t t = (size_t)tq * kFinalTile + (size_t)e * 256 + threadIdx.x;
+                    iv[e] = t < L ? imf[t] : 0.0;
+                    xv[e] = t < L ? x[t] : 0.0;
+                }
+#pragma unroll
+                for (int e = 0; e < kPer; ++e) {
+                    const size_t t = (size_t)tq * kFinalTile + (size_t)e * 256 + threadIdx.x;
+                    if (t >= L) break;
+                    const double rv = xv[e] - iv[e];  // emd.cpp:167
                     res[t] = rv;
-                    if (io) io[t] = iv;
+                    if (io) io[t] = iv[e];
                     if (ro) ro[t] = rv;
                 }
             } else {  // sums[k0+k][t] += imf_s[t] in slot order (emd.cpp:249-251)
@@ -1239,12 +1250,11 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
     __syncthreads();
     if (s_last) {
         __threadfence();
-        if (threadIdx.x == 0) {
-            for (int li = 0; li < nf; ++li) {
-                const Slot& S = A.slots[A.final_list[li]];
-                if (S.write_imf && !imf_row_ok(A, S.k0, S.k)) atomicAdd(&C->k_overflow, 1);
-            }
+        for (int li = threadIdx.x; li < nf; li += blockDim.x) {  // (one thread per slot: 500-slot waves)
+            const Slot& S = A.slots[A.final_list[li]];
+            if (S.write_imf && !imf_row_ok(A, S.k0, S.k)) atomicAdd(&C->k_overflow, 1);
         }
+        __syncthreads();
         decide_after_final(A);
         if (threadIdx.x == 0) {
             C->ticket[3] = 0;
