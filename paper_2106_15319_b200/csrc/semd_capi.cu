@@ -124,6 +124,8 @@ struct semd_ctx {
     DBuf bufs, kidx, toff, tbase, ctot, cnum, cden, ktab, scnt, tnum, tden, thash, tflags, slots, sums, imf_sifts, ctrl, lists, sb, trace, hzlog, prof;
     int* status_host = nullptr;
     int* status_host_dev = nullptr;
+    unsigned char* pin_jobs = nullptr;  // pinned staging of a run's slots, control block and eval list
+    size_t pin_jobs_bytes = 0;
     std::vector<Slot> h_slots;
     std::vector<TraceRec> h_trace;
     // scratch
@@ -135,6 +137,7 @@ struct semd_ctx {
 
     ~semd_ctx() {
         if (status_host) cudaFreeHost(status_host);
+        if (pin_jobs) cudaFreeHost(pin_jobs);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (t0) cudaEventDestroy(t0);
@@ -296,19 +299,29 @@ struct semd_ctx {
                 S.state = semd::dev::ST_FREE;
             }
         }
-        ck(cudaMemcpyAsync(A.slots, h_slots.data(), (size_t)G * sizeof(Slot), cudaMemcpyHostToDevice, stream),
-           "upload slots");
-        Ctrl c{};
+        // one pinned staging block: the uploads are truly asynchronous and the first step is
+        // launched right behind them (the previous run's kernels have completed: run() synced)
+        const size_t sb = (size_t)G * sizeof(Slot), cb = sizeof(Ctrl), lb = (size_t)G * 4;
+        if (pin_jobs_bytes < sb + cb + lb) {
+            if (pin_jobs) cudaFreeHost(pin_jobs);
+            pin_jobs = nullptr;
+            pin_jobs_bytes = 0;
+            ck(cudaHostAlloc(reinterpret_cast<void**>(&pin_jobs), sb + cb + lb, cudaHostAllocDefault), "pinned jobs");
+            pin_jobs_bytes = sb + cb + lb;
+        }
+        std::memcpy(pin_jobs, h_slots.data(), sb);
+        Ctrl& c = *reinterpret_cast<Ctrl*>(pin_jobs + sb);
+        c = Ctrl{};
         c.ev_t0 = ~0ull;
-        std::vector<int> el;
-        for (int s = 0; s < (int)jobs.size() && s < G; ++s) el.push_back(s);
-        c.n_eval = (int)el.size();
-        c.active = (int)el.size();
-        ck(cudaMemcpyAsync(A.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "upload ctrl");
-        if (!el.empty())
-            ck(cudaMemcpyAsync(A.eval_list, el.data(), el.size() * 4, cudaMemcpyHostToDevice, stream), "lists");
+        int* el = reinterpret_cast<int*>(pin_jobs + sb + cb);
+        const int ne = std::min((int)jobs.size(), G);
+        for (int s = 0; s < ne; ++s) el[s] = s;
+        c.n_eval = ne;
+        c.active = ne;
+        ck(cudaMemcpyAsync(A.slots, pin_jobs, sb, cudaMemcpyHostToDevice, stream), "upload slots");
+        ck(cudaMemcpyAsync(A.ctrl, &c, cb, cudaMemcpyHostToDevice, stream), "upload ctrl");
+        if (ne) ck(cudaMemcpyAsync(A.eval_list, el, (size_t)ne * 4, cudaMemcpyHostToDevice, stream), "lists");
         ck(cudaMemsetAsync(A.solve_off, 0, 4, stream), "lists");
-        ck(cudaStreamSynchronize(stream), "sync");  // h_slots / el are reused by the caller
         status_host[1] = 0;
         *(volatile int*)status_host = c.active;
     }
