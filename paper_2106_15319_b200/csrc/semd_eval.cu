@@ -405,6 +405,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     pdl_begin();
+    if (A.ctrl->finished) return;  // a step launched past the run's end
     extern __shared__ __align__(16) unsigned char eval_smem[];
     const int kstep_ = A.ctrl->step;
     if (threadIdx.x == 0) {

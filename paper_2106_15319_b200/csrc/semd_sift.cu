@@ -237,6 +237,7 @@ __device__ void decide_after_eval(const Arena& A) {
 // tbase and applies extract_imf's control flow.
 __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
     pdl_begin();
+    if (A.ctrl->finished) return;  // a step launched past the run's end
     const int kstep_ = A.ctrl->step;
     if (threadIdx.x == 0) span_begin(A.ctrl, KID_SCAN);
     constexpr int W = kScanThreads / 32;
@@ -367,6 +368,7 @@ constexpr int kCompactThreads = 128;
 constexpr int kCompactStrip = 16;
 __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
     pdl_begin();
+    if (A.ctrl->finished) return;  // a step launched past the run's end
     const int kstep_ = A.ctrl->step;
     if (threadIdx.x == 0) span_begin(A.ctrl, KID_COMPACT);
     __shared__ int s_last;
@@ -596,6 +598,7 @@ constexpr int kSolveIdxBuf = kSolveWin + 8;  // ints: one window's knot ranks, 1
 
 __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena A) {
     pdl_begin();
+    if (A.ctrl->finished) return;  // a step launched past the run's end
     const int kstep_ = A.ctrl->step;
     if (threadIdx.x == 0) span_begin(A.ctrl, KID_SOLVE);
     if (threadIdx.x == 0 && blockIdx.x == 0) span_fold(A.ctrl, (kstep_ & 1) ^ 1);
@@ -1040,10 +1043,13 @@ __device__ void decide_after_final(const Arena& A) {
         __threadfence_system();  // the host reads the step counter, then `active`
         hs[1] = C->step;
     }
+    // the host launches up to LAG steps past the last one: those return at once
+    if (threadIdx.x == 0 && C->active == 0) C->finished = 1;
 }
 
 __global__ void __launch_bounds__(256) k_final(Arena A) {
     pdl_begin();
+    if (A.ctrl->finished) return;  // a step launched past the run's end
     const int kstep_ = A.ctrl->step;
     if (threadIdx.x == 0) span_begin(A.ctrl, KID_FINAL);
     __shared__ unsigned s_ticket;

@@ -116,7 +116,8 @@ struct Ctrl {
     int k_overflow;
     int step;
     int hz_count;  // hazard log records produced
-    int pad[5];
+    int finished;  // the run's last step has published active == 0: later steps return at once
+    int pad[4];
     unsigned long long ev_t0;  // k_eval span of this step (globaltimer): min CTA start, max CTA end
     unsigned long long ev_t1;
     unsigned long long ev_ns;  // accumulated k_eval spans of this run (timing mode)
