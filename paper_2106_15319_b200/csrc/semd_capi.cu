@@ -269,6 +269,23 @@ struct semd_ctx {
     }
 
     // ---- one lockstep run over the configured slots -------------------------
+    // Pinned staging: [G slots][Ctrl][G eval-list ints][a reset Ctrl, never modified]
+    void ensure_pin(int G) {
+        const size_t sb = (size_t)G * sizeof(Slot), cb = sizeof(Ctrl), lb = (size_t)G * 4;
+        if (pin_jobs_bytes >= sb + 2 * cb + lb) return;
+        if (pin_jobs) cudaFreeHost(pin_jobs);
+        pin_jobs = nullptr;
+        pin_jobs_bytes = 0;
+        ck(cudaHostAlloc(reinterpret_cast<void**>(&pin_jobs), sb + 2 * cb + lb, cudaHostAllocDefault), "pinned jobs");
+        pin_jobs_bytes = sb + 2 * cb + lb;
+        Ctrl& z = *reinterpret_cast<Ctrl*>(pin_jobs + pin_jobs_bytes - cb);
+        z = Ctrl{};
+        z.ev_t0 = ~0ull;
+    }
+    const Ctrl* pin_reset_ctrl() const {
+        return reinterpret_cast<const Ctrl*>(pin_jobs + pin_jobs_bytes - sizeof(Ctrl));
+    }
+
     void set_jobs(const std::vector<JobSpec>& jobs) {
         const int G = A.G;
         for (int s = 0; s < G; ++s) {
@@ -302,13 +319,7 @@ struct semd_ctx {
         // one pinned staging block: the uploads are truly asynchronous and the first step is
         // launched right behind them (the previous run's kernels have completed: run() synced)
         const size_t sb = (size_t)G * sizeof(Slot), cb = sizeof(Ctrl), lb = (size_t)G * 4;
-        if (pin_jobs_bytes < sb + cb + lb) {
-            if (pin_jobs) cudaFreeHost(pin_jobs);
-            pin_jobs = nullptr;
-            pin_jobs_bytes = 0;
-            ck(cudaHostAlloc(reinterpret_cast<void**>(&pin_jobs), sb + cb + lb, cudaHostAllocDefault), "pinned jobs");
-            pin_jobs_bytes = sb + cb + lb;
-        }
+        ensure_pin(G);
         std::memcpy(pin_jobs, h_slots.data(), sb);
         Ctrl& c = *reinterpret_cast<Ctrl*>(pin_jobs + sb);
         c = Ctrl{};
@@ -370,11 +381,16 @@ struct semd_ctx {
                 raise(SEMD_CUDA_ERROR, "engine did not converge within %d steps;%s", max_steps, d.c_str());
             }
         }
+        // slots and control block back through the pinned block, one synchronisation
+        ensure_pin(A.G);
+        const size_t sb = (size_t)A.G * sizeof(Slot);
+        ck(cudaMemcpyAsync(pin_jobs, A.slots, sb, cudaMemcpyDeviceToHost, stream), "download slots");
+        ck(cudaMemcpyAsync(pin_jobs + sb, A.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream), "download ctrl");
         ck(cudaStreamSynchronize(stream), "engine run");
         stats.steps += step + 1;
-        ck(cudaMemcpy(h_slots.data(), A.slots, (size_t)A.G * sizeof(Slot), cudaMemcpyDeviceToHost), "download slots");
-        Ctrl c{};
-        ck(cudaMemcpy(&c, A.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost), "download ctrl");
+        std::memcpy(h_slots.data(), pin_jobs, sb);
+        Ctrl c;
+        std::memcpy(&c, pin_jobs + sb, sizeof(Ctrl));
         for (const Slot& S : h_slots) {
             stats.sifted_samples += (uint64_t)S.sifted;
             stats.sift_iterations += (uint64_t)(S.sifted / std::max(1, A.L));
@@ -409,9 +425,7 @@ struct semd_ctx {
             trace_total += c.trace_count;
         }
         // reset counters for the next run
-        Ctrl z{};
-        z.ev_t0 = ~0ull;
-        ck(cudaMemcpyAsync(A.ctrl, &z, sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
+        ck(cudaMemcpyAsync(A.ctrl, pin_reset_ctrl(), sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
     }
     long long trace_total = 0;
     double span_ms[5] = {};                 // device spans of the step kernels (semd_kernel_spans)
