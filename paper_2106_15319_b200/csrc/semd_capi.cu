@@ -354,8 +354,17 @@ struct semd_ctx {
         }
     }
 
+    // steps launched ahead of the one the host waits for (SEMD_LAG overrides; tuning)
+    static int lag_steps() {
+        static const int v = [] {
+            const char* e = std::getenv("SEMD_LAG");
+            const int x = e ? std::atoi(e) : 0;
+            return x > 0 ? x : 2;
+        }();
+        return v;
+    }
     void run(int max_steps) {
-        const int LAG = 3;
+        const int LAG = lag_steps();
         int step = 0;
         for (;; ++step) {
             semd::dev::launch_step(A, sms, stream);
