@@ -6,7 +6,7 @@ O=gpurun_out/prof
 mkdir -p $O
 timeout 900 python bench.py > $O/bench_c5_n1.json 2> $O/bench_c5.err
 timeout 600 python bench.py --config c4 --no-cpu > $O/bench_c4_n1.json 2> $O/bench_c4.err
-timeout 600 python bench.py --config c3 > $O/bench_c3_n1.json 2> $O/bench_c3.err
+timeout 600 python bench.py --config c3 --e2e-steps 5 > $O/bench_c3_n1.json 2> $O/bench_c3.err
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $O/launches_c5.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu > $O/ncu_launches.log 2>&1
 python tests/probes/ncu_summary.py $O/launches_c5.csv > $O/launches_c5_summary.txt 2>&1
