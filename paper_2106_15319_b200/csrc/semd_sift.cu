@@ -499,6 +499,7 @@ struct SolveShared {
     int item, b, last, any;
     int pf, pf_lo;  // the next block's knot indices were bulk-copied to the idx buffer from rank pf_lo
     int bb;         // block index of sh.b within its (slot, side) item
+    int slot, side, n, par, srcb;  // the block's item, read ahead by the helper: slot, side, extrema, knot parity, candidate buffer
     int dirty[kSolveMaxChains];
     int moved[kSolveMaxChains];
 };
@@ -630,6 +631,16 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
     // A slot's two items (sides 0 and 1, consecutive in the lists) take their blocks
     // alternately, so both envelopes' blocks over the same stretch of the candidate run
     // together and the second side's value gathers hit L2.
+    auto load_item = [&](int it) {  // one thread: the item's slot state the block needs
+        const int code = A.solve_item[it];
+        const int sl = code >> 1, sd = code & 1;
+        const Slot& S = A.slots[sl];
+        sh.slot = sl;
+        sh.side = sd;
+        sh.n = (int)S.n[sd];
+        sh.par = S.par;
+        sh.srcb = S.cb >= 0 ? S.cb : S.xb;
+    };
     auto decode = [&](int blk, int lo, int& it, int& bb) {
         const int p = find_item(blk, lo) & ~1;
         const int o = A.solve_off[p];
@@ -647,7 +658,10 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
     };
     if (tid == 0) {
         sh.b = (int)atomicAdd(&C->ticket[2], 1u);
-        if (sh.b < nblocks) decode(sh.b, 0, sh.item, sh.bb);
+        if (sh.b < nblocks) {
+            decode(sh.b, 0, sh.item, sh.bb);
+            load_item(sh.item);
+        }
         sh.pf = 0;
         bar_init(pbar);
     }
@@ -656,9 +670,9 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         const int blk = sh.b;
         if (blk >= nblocks) break;
         const int item = sh.item;
-        const int code = A.solve_item[item];
-        const int slot = code >> 1, side = code & 1, b = sh.bb;
-        __syncthreads();  // sh.b / sh.item consumed
+        const int slot = sh.slot, side = sh.side, b = sh.bb;
+        const int s_n = sh.n, s_par = sh.par, s_srcb = sh.srcb;
+        __syncthreads();  // sh.b / sh.item / the item's state consumed
         auto prefetch = [&]() {  // one thread: the next block, its item and its knot indices
             const int nb2 = (int)atomicAdd(&C->ticket[2], 1u);
             sh.b = nb2;
@@ -668,10 +682,8 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             decode(nb2, item & ~1, it2, bb2);
             sh.item = it2;
             sh.bb = bb2;
-            const int code2 = A.solve_item[it2];
-            const int sl2 = code2 >> 1, sd2 = code2 & 1;
-            const Slot& S2 = A.slots[sl2];
-            const int n2 = (int)S2.n[sd2];
+            load_item(it2);
+            const int sl2 = sh.slot, sd2 = sh.side, n2 = sh.n;
             if (n2 + 2 <= kSolveSeqMax) return;  // solve_small: no staging
             int wa2, wb2;
             solve_window(bb2, n2 + 4, wa2, wb2);
@@ -681,15 +693,14 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             const unsigned bytes = (unsigned)((rhi + 1 - lo4 + 3) & ~3) * 4u;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // IB's earlier generic reads
             bar_arrive_tx(pbar, bytes);
-            bulk_g2s(IB, A.kidx + knot_off(A, S2.par, sd2, sl2) + lo4, bytes, pbar);
+            bulk_g2s(IB, A.kidx + knot_off(A, sh.par, sd2, sl2) + lo4, bytes, pbar);
             sh.pf = 1;
             sh.pf_lo = lo4;
         };
-        const Slot& S = A.slots[slot];
         KnotView kv;
-        kv.idx = A.kidx + knot_off(A, S.par, side, slot);
-        kv.src = A.bufs + buf_off(A, slot, S.cb >= 0 ? S.cb : S.xb);
-        kv.n = (int)S.n[side];
+        kv.idx = A.kidx + knot_off(A, s_par, side, slot);
+        kv.src = A.bufs + buf_off(A, slot, s_srcb);
+        kv.n = s_n;
         kv.e2 = 2.0 * (double)(A.L - 1);
         kv.mom = nullptr;
         double4* tab = A.ktab + tab_off(A, side, slot);
