@@ -187,6 +187,9 @@ struct semd_ctx {
         A.Lp = Lp;
         A.G = G;
         A.tiles = tiles;
+        // short signals (C2/C3: ~50 tiles, hundreds of slots): shorter strips spread a step's
+        // work over more warps (the step is as long as its longest strip)
+        A.strip = tiles < 128 ? 4 : 16;
         A.cap = cap;
         A.kcap = kcap;
         A.bufs = bufs.as<double>();

@@ -117,7 +117,7 @@ __host__ __device__ constexpr int group_bytes(int g, int rows) {
 }
 static_assert(group_bytes(1, 2 * kWarpRows) <= kStageBytes, "one SIFT tile fits a stage");
 
-constexpr int kStripTiles = 16;  // consecutive tiles one warp walks, carrying boundary values
+constexpr int kStripTiles = 16;  // longest strip (A.strip tiles): consecutive tiles one warp walks
 
 // Per-strip constants of one warp.
 struct Strip {
@@ -132,13 +132,14 @@ struct Strip {
     int to[2];             // lane l <= nt: knot offset (toff) of tile j0 + l, per side (SIFT)
 };
 
+template <int ST>
 __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsigned strips) {
     const int lane = threadIdx.x & 31;
     Strip S;
     const unsigned sx = item % strips;
     S.slot = A.eval_list[item / strips];
-    S.j0 = (int)sx * kStripTiles;
-    S.nt = min(kStripTiles, A.tiles - S.j0);
+    S.j0 = (int)sx * ST;
+    S.nt = min(ST, A.tiles - S.j0);
     const Slot& sl = A.slots[S.slot];
     const int state = sl.state;
     S.mode = state == ST_INIT ? EM_INIT : (state == ST_DETECT ? EM_DETECT : EM_SIFT);
@@ -403,6 +404,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+// ST: tiles per strip (A.strip), a compile-time constant of each instantiation
+template <int ST>
 __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     pdl_begin();
     if (A.ctrl->finished) return;  // a step launched past the run's end
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     }
     const int lane = threadIdx.x & 31;
     WarpStage* stage = reinterpret_cast<WarpStage*>(eval_smem) + 2 * (threadIdx.x >> 5);
-    const unsigned strips = ((unsigned)A.tiles + kStripTiles - 1) / kStripTiles;
+    const unsigned strips = ((unsigned)A.tiles + ST - 1) / ST;
     const unsigned nstrips = (unsigned)A.ctrl->n_eval * strips;
     if (lane == 0) {
         bar_init(&stage[0].bar);
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     item = __shfl_sync(0xffffffffu, item, 0);
     while (item < nstrips) {
         if (lane == 0) next = atomicAdd(tk, 1u);
-        const Strip S = strip_setup(A, item, strips);
+        const Strip S = strip_setup<ST>(A, item, strips);
         const long long cyc0 = clock64();
         double c2 = 0.0, c1 = 0.0, snum = 0.0, sden = 0.0;
         if (S.mode == EM_DETECT) {
@@ -492,8 +495,8 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
             snum = warp_sum(snum);
             sden = warp_sum(sden);
             if (lane == 0) {
-                A.tnum[tsd_off(A, S.slot) + S.j0 / kStripTiles] = snum;
-                A.tden[tsd_off(A, S.slot) + S.j0 / kStripTiles] = sden;
+                A.tnum[tsd_off(A, S.slot) + S.j0 / ST] = snum;
+                A.tden[tsd_off(A, S.slot) + S.j0 / ST] = sden;
             }
         }
         if (lane == 0) {
@@ -511,7 +514,10 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
 
 size_t eval_smem_bytes() { return sizeof(WarpStage) * 2 * (kEvalThreads / 32); }
 cudaError_t eval_setup() {
-    return cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eval_smem_bytes());
+    const cudaError_t e = cudaFuncSetAttribute(k_eval<kStripTiles>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)eval_smem_bytes());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_eval<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eval_smem_bytes());
 }
 
 void launch_eval(const Arena& A, int sms, cudaStream_t st) {
@@ -525,7 +531,10 @@ void launch_eval(const Arena& A, int sms, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_eval, A);
+    if (A.strip == 4)
+        cudaLaunchKernelEx(&cfg, k_eval<4>, A);
+    else
+        cudaLaunchKernelEx(&cfg, k_eval<kStripTiles>, A);
 }
 
 }  // namespace dev

@@ -296,13 +296,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
             A.ctot[chunk_off(A, side, s) + c] = tot;
         }
         if (side == 0 && S.state == ST_SIFT) {  // SD sums (emd.cpp:145-146), fixed reduction order
-            // k_eval leaves one partial per 16-tile strip; this chunk owns strips [jb/16, ceil(je/16))
-            static_assert(kScanChunk == 16 * kScanThreads, "one strip per scan thread");
-            const int sx = jb / 16 + tid;
+            // k_eval leaves one partial per strip of A.strip tiles; this chunk owns strips
+            // [jb/strip, ceil(je/strip)), taken by the threads in order (a fixed reduction order)
+            static_assert(kScanChunk == 16 * kScanThreads, "one 16-tile strip per scan thread");
+            const int st = A.strip;
+            const int sb0 = jb / st, sb1 = (je + st - 1) / st;
             double a = 0.0, b = 0.0;
-            if (sx < (je + 15) / 16) {
-                a = A.tnum[tsd_off(A, s) + sx];
-                b = A.tden[tsd_off(A, s) + sx];
+            for (int sx = sb0 + tid; sx < sb1; sx += kScanThreads) {
+                a += A.tnum[tsd_off(A, s) + sx];
+                b += A.tden[tsd_off(A, s) + sx];
             }
             a = warp_sum(a);
             b = warp_sum(b);

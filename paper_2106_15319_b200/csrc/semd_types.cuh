@@ -166,6 +166,7 @@ __device__ __forceinline__ void pdl_begin() {
 
 struct Arena {
     int L, G, tiles, cap, kcap;
+    int strip;     // tiles per eval strip (one warp work item, one SD partial): 16, or 4 for short signals
     int kper;      // > 0: IMF rows per job (batched jobs own rows [k0, k0 + kper)); 0: all kcap rows
     long long Lp;  // slot-buffer stride = tiles * kEvalTile (16-byte aligned; whole tiles readable)
     double sd_threshold;
