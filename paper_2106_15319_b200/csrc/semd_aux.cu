@@ -344,6 +344,31 @@ __global__ void k_envelope_eval(const double* xs, const double* ys, const double
 }
 
 // CEEMDAN stage mean (emd.cpp:301-304 / :331-336): mode *= inv, flag any nonzero.
+// Number of maxima and minima find_extrema (emd.cpp:10-35) reports for x: runs of exactly
+// equal samples with both neighbours, strictly above (below) both; the thread at each run's
+// first sample decides (CEEMDAN's residue test, emd.cpp:311, needs only the total).
+__global__ void k_count_extrema(const double* x, long long n, unsigned long long* cnt) {
+    unsigned long long mx = 0, mn = 0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+        const double v = x[t];
+        if (t == 0 || x[t - 1] == v) continue;  // runs touching index 0 never count; not a run start
+        long long re = t;
+        while (re + 1 < n && x[re + 1] == v) ++re;
+        if (re == n - 1) continue;
+        const double l = x[t - 1], r = x[re + 1];
+        mx += (v > l && v > r) ? 1ull : 0ull;
+        mn += (v < l && v < r) ? 1ull : 0ull;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mx += __shfl_xor_sync(0xffffffffu, mx, o);
+        mn += __shfl_xor_sync(0xffffffffu, mn, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (mx) atomicAdd(&cnt[0], mx);
+        if (mn) atomicAdd(&cnt[1], mn);
+    }
+}
+
 __global__ void k_stage_scale(double* mode, long long n, double inv, int* nonzero) {
     int nz = 0;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
@@ -473,6 +498,10 @@ void launch_envelope(const double* xs, const double* ys, int n, double* mom, dou
     k_envelope_solve<<<1, 32, 0, st>>>(xs, ys, n, mom, work);
     count_launches(1);
     k_envelope_eval<<<grid_for(length), 256, 0, st>>>(xs, ys, mom, n, length, out);
+    count_launches(1);
+}
+void launch_count_extrema(const double* x, long long n, unsigned long long* cnt, cudaStream_t st) {
+    k_count_extrema<<<grid_for(n), 256, 0, st>>>(x, n, cnt);
     count_launches(1);
 }
 void launch_stage_scale(double* mode, long long n, double inv, int* nonzero, cudaStream_t st) {

@@ -720,6 +720,18 @@ struct semd_ctx {
     // find_extrema(residue).total() (emd.cpp:311)
     long long ceemdan_residue_extrema() {
         if (!cs.active) raise(SEMD_INVALID_INPUT, "ceemdan: no active shard (call begin)");
+        if (!A.trace) {  // untraced: one counting kernel instead of an engine run
+            const long long n = cs.n;
+            if (n < 3) raise(SEMD_INVALID_INPUT, "find_extrema: signal too short (need at least 3 samples)");
+            scalar.alloc((2 + 2 * 256 + 8) * 8);
+            unsigned long long* d = reinterpret_cast<unsigned long long*>(scalar.p) + (2 + 2 * 256);  // spare tail
+            ck(cudaMemsetAsync(d, 0, 16, stream), "count");
+            semd::dev::launch_count_extrema(cs_residue(), n, d, stream);
+            unsigned long long h[2] = {0, 0};
+            ck(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, stream), "count");
+            ck(cudaStreamSynchronize(stream), "count");
+            return (long long)(h[0] + h[1]);
+        }
         JobSpec J;
         J.m = -1;
         J.task = 3;

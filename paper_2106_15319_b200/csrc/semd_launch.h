@@ -40,6 +40,7 @@ void launch_deconcatenate(const double* modes, long long K, long long Lm, long l
 void launch_envelope(const double* xs, const double* ys, int n, double* mom, double* work, long long length,
                      double* out, cudaStream_t st);
 void launch_stage_scale(double* mode, long long n, double inv, int* nonzero, cudaStream_t st);
+void launch_count_extrema(const double* x, long long n, unsigned long long* cnt, cudaStream_t st);
 void launch_sub(double* residue, const double* mode, long long n, cudaStream_t st);
 void launch_envelope_knots(const unsigned long long* idx, const double* val, long long n, long long length,
                            double* xs, double* ys, cudaStream_t st);

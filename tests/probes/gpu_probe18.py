@@ -12,7 +12,7 @@ s = se.concatenate(W.config_input("c3"), 50)
 c = se.context()
 ms = (C.c_double * 5)()
 strips = (C.c_uint64 * 4)()
-for it in range(4):
+for it in range(int(os.environ.get("ITERS", "4"))):
     c.check(c.lib.semd_kernel_spans(c.ptr, ms, strips))
     t = time.time()
     d = se.decompose_full(s, "ceemdan", max_sift_iters=5000, nr=500)

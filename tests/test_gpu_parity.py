@@ -484,6 +484,25 @@ def test_ceemdan_stage_api_matches_monolithic(se, oracle):
     assert np.array_equal(mono["imfs"], o[0]) and np.array_equal(mono["residue"], o[1])
 
 
+def test_ceemdan_residue_extrema_count(se, oracle):
+    """CEEMDAN's residue test (emd.cpp:311) counts find_extrema's maxima + minima with one kernel
+    when untraced: equal to the oracle's find_extrema on plateau-rich and smooth signals."""
+    import torch
+
+    from paper_2106_15319_b200.parallel import GpuCeemdanShard
+    ctx = se.context()
+    rng = np.random.default_rng(7)
+    cases = [rng.integers(-2, 3, size=int(rng.integers(4, 9000))).astype(float) for _ in range(6)]
+    cases += [rng.standard_normal(int(rng.integers(4, 9000))) for _ in range(4)]
+    cases += [np.concatenate([np.zeros(10), np.ones(5000), np.zeros(3000), -np.ones(7001), np.zeros(3)]),
+              np.array([1.0, 1.0, 1.0, 1.0]), np.array([0.0, 1.0, 1.0, 0.0, 2.0, 2.0, 2.0])]
+    for x in cases:
+        eng = GpuCeemdanShard(ctx, torch.from_numpy(x).cuda(), x.size, {}, {"nr": 2})
+        eng.begin(0, 2)  # the shard's residue starts as x
+        max_idx, _, min_idx, _ = oracle.find_extrema(x)
+        assert eng.residue_extrema() == len(max_idx) + len(min_idx)
+
+
 def test_eemd_shards_sum_to_whole(se):
     """Realization sharding (the multi-GPU split) on one GPU: the partial sums of
     [0, m) and [m, nr) add up to the partial sums of [0, nr), and K is the max of the shards' K."""
