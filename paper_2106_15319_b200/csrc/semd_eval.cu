@@ -106,7 +106,7 @@ constexpr int kWarpRows = kEvalTile / 2 + 6;  // table rows one tile can touch p
 //   samples [base-2, base + g*T)  |  g x 32 detection words (SIFT)  |  rows side 0  |  rows side 1
 // (one bulk copy each). SIFT groups take as many tiles (<= kGroupMax) as fit; one tile
 // always fits (kWarpRows rows per side).
-constexpr int kStageBytes = 7040;
+constexpr int kStageBytes = 6912;
 constexpr int kGroupMax = 4;
 struct alignas(16) WarpStage {
     double flat[kStageBytes / 8];
@@ -159,6 +159,49 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
 #pragma unroll
         for (int s = 0; s < 2; ++s) S.to[s] = (int)toff_view(A, sl.par, s, S.slot)[j];
     }
+    return S;
+}
+
+// The next strip, set up during the current strip's last group (its first bulk copy issued into
+// the free stage), parked in shared memory so it does not hold registers meanwhile.
+struct alignas(16) StripStash {
+    int to[2][32];
+    int slot, mode, par, srcb, dstb, g, pad[2];
+};
+template <int ST>
+__device__ __forceinline__ void stash_strip(const Arena& A, const Strip& S, int g, StripStash& st) {
+    const int lane = threadIdx.x & 31;
+    st.to[0][lane] = S.to[0];
+    st.to[1][lane] = S.to[1];
+    if (lane == 0) {
+        const Slot& sl = A.slots[S.slot];
+        st.slot = S.slot;
+        st.mode = S.mode;
+        st.par = S.par;
+        st.srcb = (S.mode == EM_SIFT && sl.cb >= 0) ? sl.cb : sl.xb;
+        st.dstb = S.mode == EM_INIT ? sl.xb : sl.db;
+        st.g = g;
+    }
+    __syncwarp();
+}
+template <int ST>
+__device__ __forceinline__ Strip strip_from(const Arena& A, unsigned item, unsigned strips, const StripStash& st) {
+    const int lane = threadIdx.x & 31;
+    Strip S;
+    S.slot = st.slot;
+    S.j0 = (int)(item % strips) * ST;
+    S.nt = min(ST, A.tiles - S.j0);
+    S.mode = st.mode;
+    S.par = st.par;
+    S.src = A.bufs + buf_off(A, S.slot, st.srcb);
+    S.dst = S.mode == EM_DETECT ? nullptr : A.bufs + buf_off(A, S.slot, st.dstb);
+    S.tab0 = A.ktab + tab_off(A, 0, S.slot);
+    S.tab1 = A.ktab + tab_off(A, 1, S.slot);
+    S.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
+    S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
+    S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
+    S.to[0] = st.to[0][lane];
+    S.to[1] = st.to[1][lane];
     return S;
 }
 
@@ -433,16 +476,39 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     unsigned item = 0, next = 0;
     if (lane == 0) item = atomicAdd(tk, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
+    StripStash& stash = reinterpret_cast<StripStash*>(reinterpret_cast<WarpStage*>(eval_smem) +
+                                                      2 * (kEvalThreads / 32))[threadIdx.x >> 5];
+    bool pre = false;  // this strip was set up (and its first copy issued) by the previous one
     while (item < nstrips) {
         if (lane == 0) next = atomicAdd(tk, 1u);
-        const Strip S = strip_setup<ST>(A, item, strips);
+        const Strip S = pre ? strip_from<ST>(A, item, strips, stash) : strip_setup<ST>(A, item, strips);
+        const int g_pre = pre ? stash.g : 0;
+        bool pre_next = false;
+        // during this strip's last group: set up the next strip and issue its first copy into
+        // the free stage (SIFT / DETECT strips; INIT strips stage nothing)
+        auto prefetch_next = [&](int fb) {
+            const unsigned nx = __shfl_sync(0xffffffffu, next, 0);
+            if (nx >= nstrips) return;
+            const Strip S2 = strip_setup<ST>(A, nx, strips);
+            if (S2.mode == EM_INIT) return;
+            int g2 = 0;
+            if (S2.mode == EM_SIFT) {
+                g2 = group_tiles(S2, 0);
+                issue_group(S2, 0, g2, stage[fb]);
+            } else {
+                issue_chunk(S2, 0, stage[fb]);
+            }
+            stash_strip<ST>(A, S2, g2, stash);
+            pre_next = true;
+        };
         const long long cyc0 = clock64();
         double c2 = 0.0, c1 = 0.0, snum = 0.0, sden = 0.0;
         if (S.mode == EM_DETECT) {
             const int nch = (S.nt + kDetChunk - 1) / kDetChunk;
-            issue_chunk(S, 0, stage[b]);
+            if (!pre) issue_chunk(S, 0, stage[b]);
             for (int c = 0; c < nch; ++c) {
                 if (c + 1 < nch) issue_chunk(S, c + 1, stage[b ^ 1]);
+                else prefetch_next(b ^ 1);
                 bar_wait(&stage[b].bar, (phase >> b) & 1u);
                 phase ^= 1u << b;
                 const double* flat = stage_flat(stage[b]);
@@ -459,11 +525,12 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
                 b ^= 1;
             }
         } else if (S.mode == EM_SIFT) {
-            int g = group_tiles(S, 0);
-            issue_group(S, 0, g, stage[b]);
+            int g = pre ? g_pre : group_tiles(S, 0);
+            if (!pre) issue_group(S, 0, g, stage[b]);
             for (int i = 0; i < S.nt;) {
                 const int gn = i + g < S.nt ? group_tiles(S, i + g) : 0;
                 if (gn) issue_group(S, i + g, gn, stage[b ^ 1]);
+                else prefetch_next(b ^ 1);
                 bar_wait(&stage[b].bar, (phase >> b) & 1u);
                 phase ^= 1u << b;
                 const double* flat = stage_flat(stage[b]);
@@ -504,6 +571,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
             atomicAdd(&A.ctrl->strip_cyc[S.mode == EM_SIFT ? 1 : 0], (unsigned long long)(clock64() - cyc0));
         }
         item = __shfl_sync(0xffffffffu, next, 0);
+        pre = pre_next;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -512,7 +580,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     }
 }
 
-size_t eval_smem_bytes() { return sizeof(WarpStage) * 2 * (kEvalThreads / 32); }
+size_t eval_smem_bytes() { return (sizeof(WarpStage) * 2 + sizeof(StripStash)) * (kEvalThreads / 32); }
 cudaError_t eval_setup() {
     const cudaError_t e = cudaFuncSetAttribute(k_eval<kStripTiles>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)eval_smem_bytes());
