@@ -380,12 +380,23 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
     const int strips = (A.tiles + kCompactStrip - 1) / kCompactStrip;
     const unsigned nitems = (unsigned)C->n_compact * (unsigned)strips;
     const bool tracing = A.trace != nullptr;
-    for (unsigned it = blockIdx.x * wpb + (threadIdx.x >> 5); it < nitems; it += gridDim.x * wpb) {
-        const int s = A.compact_list[it / (unsigned)strips];
+    // each warp takes a contiguous run of items (consecutive strips of one slot share the slot's
+    // state, read once per slot instead of per item)
+    const unsigned nw = gridDim.x * wpb;
+    const unsigned per = (nitems + nw - 1) / nw;
+    const unsigned it0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * per;
+    const unsigned it1 = min(nitems, it0 + per);
+    int cur_li = -1, s = 0, cpar = 0;
+    for (unsigned it = it0; it < it1; ++it) {
+        const int li = (int)(it / (unsigned)strips);
+        if (li != cur_li) {
+            cur_li = li;
+            s = A.compact_list[li];
+            cpar = A.slots[s].cpar;
+        }
         const int sx = (int)(it % (unsigned)strips);
         const int j0 = sx * kCompactStrip;
         const int nt = min(kCompactStrip, A.tiles - j0);
-        const int cpar = A.slots[s].cpar;
         unsigned off0 = 0, off1 = 0;
         if (lane < nt) {
             off0 = toff_view(A, cpar, 0, s)[j0 + lane];
