@@ -34,7 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ALGO_BYTES_PER_SIFTED_SAMPLE = 16  # one f64 read + one f64 write of the candidate
-METRIC = "serial-EEMD sifted samples/sec"
+METRIC = "serial-EEMD/CEEMDAN sifted samples/sec"  # BASELINE.json metric (the % of HBM roofline is `roofline.frac`)
 
 
 def peaks():
