@@ -235,6 +235,11 @@ __device__ void decide_after_eval(const Arena& A) {
 // prefix of the per-tile extrema counts -> toff, the chunk total -> ctot, and
 // (side 0) the chunk's SD partials. The last CTA scans the chunk totals into
 // tbase and applies extract_imf's control flow.
+__host__ __device__ inline bool scan_by_warp(const Arena& A) { return A.chunks == 1 && A.tiles <= 32 * kScanPer; }
+__host__ __device__ inline int scan_grid(const Arena& A) {
+    return scan_by_warp(A) ? (2 * A.G + kScanThreads / 32 - 1) / (kScanThreads / 32) : 2 * A.G * A.chunks;
+}
+
 __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
     pdl_begin();
     if (A.ctrl->finished) return;  // a step launched past the run's end
@@ -247,6 +252,65 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
     Ctrl* C = A.ctrl;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int P = A.chunks;
+    if (scan_by_warp(A)) {
+        // short signals (one chunk of at most 32 * kScanPer tiles): one warp per (slot, side); the
+        // same tile prefix, and the same SD partial sums (the strips sit in one warp either way)
+        const int item = blockIdx.x * W + wid;
+        const int li = item >> 1, side = item & 1;
+        if (li < C->n_eval) {
+            const int s = A.eval_list[li];
+            const Slot& S = A.slots[s];
+            const int np = 1 - S.par;
+            const int T = A.tiles;
+            const int j0 = lane * kScanPer;
+            const unsigned* cnt = A.scnt + scnt_off(A, side, s);
+            unsigned v[kScanPer];
+            unsigned sum = 0;
+#pragma unroll
+            for (int q = 0; q < kScanPer / 4; ++q) {
+                uint4 u = make_uint4(0u, 0u, 0u, 0u);
+                if (j0 + 4 * q < T) u = *reinterpret_cast<const uint4*>(cnt + j0 + 4 * q);  // rows padded to 4
+                v[4 * q] = j0 + 4 * q < T ? u.x : 0u;
+                v[4 * q + 1] = j0 + 4 * q + 1 < T ? u.y : 0u;
+                v[4 * q + 2] = j0 + 4 * q + 2 < T ? u.z : 0u;
+                v[4 * q + 3] = j0 + 4 * q + 3 < T ? u.w : 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < kScanPer; ++i) sum += v[i];
+            unsigned incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+            unsigned run = incl - sum;
+            unsigned* to = A.toff + toff_off(A, np, side, s);
+#pragma unroll
+            for (int i = 0; i < kScanPer; ++i) {
+                if (j0 + i < T) to[j0 + i] = run;
+                run += v[i];
+            }
+            if (lane == 0) {
+                to[T] = tot;
+                A.ctot[chunk_off(A, side, s)] = tot;
+            }
+            if (side == 0 && S.state == ST_SIFT) {  // SD sums (emd.cpp:145-146)
+                const int st = A.strip, sb1 = (T + st - 1) / st;
+                double a = 0.0, b = 0.0;
+                for (int sx = lane; sx < sb1; sx += 32) {
+                    a += A.tnum[tsd_off(A, s) + sx];
+                    b += A.tden[tsd_off(A, s) + sx];
+                }
+                a = warp_sum(a);
+                b = warp_sum(b);
+                if (lane == 0) {
+                    A.cnum[chunk_off(A, 0, s)] = a;
+                    A.cden[chunk_off(A, 0, s)] = b;
+                }
+            }
+        }
+    } else {
     const int item = blockIdx.x / P, c = blockIdx.x - item * P;
     const int li = item >> 1, side = item & 1;
     if (li < C->n_eval) {
@@ -324,6 +388,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
             }
         }
     }
+    }  // one CTA per (slot, side, chunk)
     if (tid == 0) {
         __threadfence();
         s_last = atomicAdd(&C->done[4], 1u) == gridDim.x - 1;
@@ -1338,7 +1403,7 @@ static void launch_pdl(Kernel kernel, int grid, int block, size_t smem, cudaStre
 void launch_step(const Arena& A, int sms, cudaStream_t st) {
     launch_pdl(k_solve, kSolveCtasPerSm * sms, kSolveThreads, solve_smem_bytes(), st, A);
     launch_eval(A, sms, st);
-    launch_pdl(k_scan, 2 * A.G * A.chunks, kScanThreads, 0, st, A);
+    launch_pdl(k_scan, scan_grid(A), kScanThreads, 0, st, A);
     launch_pdl(k_compact, sms * 8, kCompactThreads, 0, st, A);
     launch_pdl(k_final, 2 * sms, 256, 0, st, A);
     count_launches(5);
