@@ -441,11 +441,6 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
 // Warp-level software pipeline: tile i is computed while the bulk copies of tile
 // i+1 are in flight. SD partials are summed per lane over the strip and reduced
 // once per strip (tnum/tden are indexed by strip).
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 // ST: tiles per strip (A.strip), a compile-time constant of each instantiation
 template <int ST>
@@ -455,7 +450,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     extern __shared__ __align__(16) unsigned char eval_smem[];
     const int kstep_ = A.ctrl->step;
     if (threadIdx.x == 0) {
-        atomicMin(&A.ctrl->ev_t0, globaltimer());
+        atomicMin(&A.ctrl->ev_t0, gtimer());
         span_begin(A.ctrl, KID_EVAL);
     }
     const int lane = threadIdx.x & 31;
@@ -575,7 +570,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        atomicMax(&A.ctrl->ev_t1, globaltimer());
+        atomicMax(&A.ctrl->ev_t1, gtimer());
         span_end(A.ctrl, KID_EVAL, kstep_);
     }
 }

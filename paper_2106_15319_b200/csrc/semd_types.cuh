@@ -28,7 +28,6 @@ namespace dev {
 constexpr int kEvalTile = 128;                  // samples per eval tile (one warp)
 constexpr int kEvalThreads = 256;              // 8 independent warps per CTA
 constexpr int kSpt = kEvalTile / 32;            // samples per lane (consecutive)
-constexpr int kKnotCapTile = kEvalTile / 2 + 4; // knots of one side touching a tile
 
 constexpr int kSolveChains = 64;                         // speculative chains per block
 constexpr int kSolveChunk = 16;                          // rows per chain
