@@ -438,9 +438,10 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
     }
 }
 
-// Warp-level software pipeline: tile i is computed while the bulk copies of tile
-// i+1 are in flight. SD partials are summed per lane over the strip and reduced
-// once per strip (tnum/tden are indexed by strip).
+// Warp-level software pipeline over two stages: a group of tiles (SIFT) or a chunk (DETECT) is
+// computed while the next one's bulk copies are in flight; during a strip's last group the next
+// strip is set up and its first copy issued. SD partials are summed per lane over the strip and
+// reduced once per strip (tnum/tden are indexed by strip).
 
 // ST: tiles per strip (A.strip), a compile-time constant of each instantiation
 template <int ST>
