@@ -92,10 +92,25 @@ __device__ __forceinline__ double spline_eval_fast(double x0, double x1, double 
     return a * y0 + b * y1 + div_rn(p, 6.0, 1.0 / 6.0);
 }
 
-// The segment table of one envelope (written by k_solve): row v holds the
-// mirrored knot {x_v, y_v, m_v, RN(1/(x_{v+1}-x_v))}.
+// The segment table of one envelope (written by k_solve), in two planes of 16-byte rows:
+// a[v] = {x_v, y_v}, b[v] = {m_v, RN(1/(x_{v+1}-x_v))} of the mirrored knot v; b = a + cap + 8.
+// Staged in shared memory, consecutive rows are consecutive 16-byte words, so the lanes of a
+// warp reading neighbouring rows hit distinct banks (32-byte rows would collide two-way).
+struct TabPlanes {
+    double2* a;
+    double2* b;
+    __device__ __forceinline__ void set(int v, double x, double y, double m, double rh) const {
+        a[v] = make_double2(x, y);
+        b[v] = make_double2(m, rh);
+    }
+};
+__host__ __device__ inline TabPlanes tab_planes(const Arena& A, int side, int slot) {
+    double2* base = reinterpret_cast<double2*>(A.ktab + tab_off(A, side, slot));
+    return TabPlanes{base, base + A.cap + 8};
+}
+
 struct TabView {
-    const double4* tab;
+    TabPlanes tp;
     const int* idx;  // the real extrema positions (for the segment count)
     int n;
 };
@@ -110,9 +125,10 @@ __device__ inline double envelope_tab(const TabView& tv, int t) {
         else hi = mid;
     }
     const int seg = 1 + lo;
-    const double4 r0 = tv.tab[seg], r1 = tv.tab[seg + 1];
-    const double h = r1.x - r0.x;
-    return spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, (double)t);
+    const double2 a0 = tv.tp.a[seg], b0 = tv.tp.b[seg], a1 = tv.tp.a[seg + 1];
+    const double m1 = tv.tp.b[seg + 1].x;
+    const double h = a1.x - a0.x;
+    return spline_eval_fast(a0.x, a1.x, a0.y, a1.y, b0.x, m1, h, b0.y, h * h, (double)t);
 }
 
 // Bulk (TMA-engine) copies global -> shared completed on an mbarrier (one thread issues).

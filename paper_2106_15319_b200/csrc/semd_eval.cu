@@ -52,7 +52,7 @@ __device__ EvalCtx make_ctx(const Arena& A, int slot, int mode) {
     J.src = A.bufs + buf_off(A, slot, (mode == EM_SIFT && sl.cb >= 0) ? sl.cb : sl.xb);
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-        J.tv[s].tab = A.ktab + tab_off(A, s, slot);
+        J.tv[s].tp = tab_planes(A, s, slot);
         J.tv[s].idx = A.kidx + knot_off(A, sl.par, s, slot);
         J.tv[s].n = (int)sl.n[s];
     }
@@ -124,8 +124,8 @@ struct Strip {
     int slot, j0, nt, mode, par;
     const double* src;     // the samples this pass reads (SIFT, DETECT)
     double* dst;           // where new values go (INIT: X, SIFT: the candidate; DETECT: none)
-    const double4* tab0;   // side-0 segment table
-    const double4* tab1;   // side-1 segment table
+    const double2* tab0;   // side-0 segment table, {x, y} plane ({m, 1/h} plane at + cap + 8)
+    const double2* tab1;   // side-1 segment table
     const unsigned* ow;    // SIFT: tflags words of tile j0 (current knot parity)
     unsigned* nw;          // tflags words of tile j0 (parity of the new detection)
     unsigned* cnt0;        // scnt of tile j0, side 0 (side 1 at + A.G * tiles4)
@@ -148,8 +148,8 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
     S.src = A.bufs + buf_off(A, S.slot, (S.mode == EM_SIFT && cb >= 0) ? cb : xb);
     S.dst = S.mode == EM_INIT ? A.bufs + buf_off(A, S.slot, xb)
                               : (S.mode == EM_SIFT ? A.bufs + buf_off(A, S.slot, sl.db) : nullptr);
-    S.tab0 = A.ktab + tab_off(A, 0, S.slot);
-    S.tab1 = A.ktab + tab_off(A, 1, S.slot);
+    S.tab0 = tab_planes(A, 0, S.slot).a;
+    S.tab1 = tab_planes(A, 1, S.slot).a;
     S.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
     S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
     S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
@@ -195,8 +195,8 @@ __device__ __forceinline__ Strip strip_from(const Arena& A, unsigned item, unsig
     S.par = st.par;
     S.src = A.bufs + buf_off(A, S.slot, st.srcb);
     S.dst = S.mode == EM_DETECT ? nullptr : A.bufs + buf_off(A, S.slot, st.dstb);
-    S.tab0 = A.ktab + tab_off(A, 0, S.slot);
-    S.tab1 = A.ktab + tab_off(A, 1, S.slot);
+    S.tab0 = tab_planes(A, 0, S.slot).a;
+    S.tab1 = tab_planes(A, 1, S.slot).a;
     S.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
     S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
     S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
@@ -221,7 +221,7 @@ __device__ __forceinline__ int group_tiles(const Strip& S, int i) {
 }
 
 // Issue group (i, g)'s copies: samples, detection words, both sides' rows (lane 0 arms the barrier).
-__device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpStage& st) {
+__device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpStage& st, int bofs) {
     const int lo0 = __shfl_sync(0xffffffffu, S.to[0], i), lo1 = __shfl_sync(0xffffffffu, S.to[1], i);
     const int n0 = __shfl_sync(0xffffffffu, S.to[0], i + g) + 3 - lo0;
     const int n1 = __shfl_sync(0xffffffffu, S.to[1], i + g) + 3 - lo1;
@@ -232,12 +232,14 @@ __device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpSt
     const unsigned sb = (unsigned)(base + g * kEvalTile - e0) * 8u;
     double* f = st.flat;
     unsigned* ow = reinterpret_cast<unsigned*>(f + g * kEvalTile + 2);
-    double4* r0 = reinterpret_cast<double4*>(ow + g * 32);
+    double2* r0 = reinterpret_cast<double2*>(ow + g * 32);  // {x,y} side 0 | side 1, then {m,1/h} side 0 | side 1
     bar_arrive_tx(&st.bar, sb + (unsigned)g * 128u + (unsigned)(n0 + n1) * 32u);
     bulk_g2s(f + (e0 - (base - 2)), S.src + e0, sb, &st.bar);
     bulk_g2s(ow, S.ow + i * 32, (unsigned)g * 128u, &st.bar);
-    bulk_g2s(r0, S.tab0 + lo0, (unsigned)n0 * 32u, &st.bar);
-    bulk_g2s(r0 + n0, S.tab1 + lo1, (unsigned)n1 * 32u, &st.bar);
+    bulk_g2s(r0, S.tab0 + lo0, (unsigned)n0 * 16u, &st.bar);
+    bulk_g2s(r0 + n0, S.tab1 + lo1, (unsigned)n1 * 16u, &st.bar);
+    bulk_g2s(r0 + n0 + n1, S.tab0 + bofs + lo0, (unsigned)n0 * 16u, &st.bar);
+    bulk_g2s(r0 + 2 * n0 + n1, S.tab1 + bofs + lo1, (unsigned)n1 * 16u, &st.bar);
 }
 
 // DETECT passes stream samples only: the stage's row area holds kDetChunk tiles, so one bulk
@@ -257,7 +259,7 @@ __device__ __forceinline__ void issue_chunk(const Strip& S, int c, WarpStage& st
     bulk_g2s(stage_flat(st) + (e0 - (base - 2)), S.src + e0, sb, &st.bar);
 }
 
-__device__ __forceinline__ int smem_search(const double4* R, int hi, double t) {  // last q <= hi with x_q < t
+__device__ __forceinline__ int smem_search(const double2* R, int hi, double t) {  // last q <= hi with x_q < t
     int lo = 0;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -273,7 +275,7 @@ __device__ __forceinline__ int smem_search(const double4* R, int hi, double t) {
 // first and the last of a slot) -- no per-sample bound checks.
 template <bool Interior, int M>
 __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i, const double* samp,
-                                          const unsigned* ows, const double4* R0, const double4* R1, double& c2,
+                                          const unsigned* ows, const double2* R0, const double2* R1, int nab, double& c2,
                                           double& c1, double& snum, double& sden) {
     const int lane = threadIdx.x & 31;
     constexpr int mode = M;  // the pass's mode (each loop instantiates its own)
@@ -301,11 +303,12 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
                 double e[2];
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
-                    const double4* R = s ? R1 : R0;
+                    const double2* R = s ? R1 : R0;
                     const int qq = smem_search(R, qmax[s], tt);
-                    const double4 r0 = R[qq], r1 = R[qq + 1];
-                    const double h = r1.x - r0.x;
-                    e[s] = spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
+                    const double2 a0 = R[qq], b0 = R[nab + qq], a1 = R[qq + 1];
+                    const double m1 = R[nab + qq + 1].x;
+                    const double h = a1.x - a0.x;
+                    e[s] = spline_eval_fast(a0.x, a1.x, a0.y, a1.y, b0.x, m1, h, b0.y, h * h, tt);
                 }
                 cc[u] = samp[u] - 0.5 * (e[0] + e[1]);
             }
@@ -346,16 +349,17 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         double env0[kSpt];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            const double4* R = s ? R1 : R0;
+            const double2* R = s ? R1 : R0;
             const unsigned fl = (ow >> (4 * s)) & 0xFu;  // window positions t0-1 .. t0+2
             const int q0 = 1 + (int)((ow >> (8 + 8 * s)) & 0xFFu) + (int)(fl & 1u);
 #pragma unroll
             for (int k = 0; k < kSpt; ++k) {
                 const double tt = (double)(t0 + k);
                 const int q = q0 + __popc((fl >> 1) & ((1u << k) - 1u));
-                const double4 r0 = R[q], r1 = R[q + 1];
-                const double h = r1.x - r0.x;
-                const double e = spline_eval_fast(r0.x, r1.x, r0.y, r1.y, r0.z, r1.z, h, r0.w, h * h, tt);
+                const double2 a0 = R[q], b0 = R[nab + q], a1 = R[q + 1];
+                const double m1 = R[nab + q + 1].x;
+                const double h = a1.x - a0.x;
+                const double e = spline_eval_fast(a0.x, a1.x, a0.y, a1.y, b0.x, m1, h, b0.y, h * h, tt);
                 if (s == 0) {
                     env0[k] = e;
                 } else {
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
             int g2 = 0;
             if (S2.mode == EM_SIFT) {
                 g2 = group_tiles(S2, 0);
-                issue_group(S2, 0, g2, stage[fb]);
+                issue_group(S2, 0, g2, stage[fb], A.cap + 8);
             } else {
                 issue_chunk(S2, 0, stage[fb]);
             }
@@ -513,37 +517,39 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
                     const int base = (S.j0 + i) * kEvalTile;
                     const double* sp = flat + (i - c * kDetChunk) * kEvalTile;
                     if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
-                        eval_tile<true, EM_DETECT>(A, S, i, sp, nullptr, nullptr, nullptr, c2, c1, snum, sden);
+                        eval_tile<true, EM_DETECT>(A, S, i, sp, nullptr, nullptr, nullptr, 0, c2, c1, snum, sden);
                     else
-                        eval_tile<false, EM_DETECT>(A, S, i, sp, nullptr, nullptr, nullptr, c2, c1, snum, sden);
+                        eval_tile<false, EM_DETECT>(A, S, i, sp, nullptr, nullptr, nullptr, 0, c2, c1, snum, sden);
                 }
                 __syncwarp();  // stage b is refilled next
                 b ^= 1;
             }
         } else if (S.mode == EM_SIFT) {
             int g = pre ? g_pre : group_tiles(S, 0);
-            if (!pre) issue_group(S, 0, g, stage[b]);
+            if (!pre) issue_group(S, 0, g, stage[b], A.cap + 8);
             for (int i = 0; i < S.nt;) {
                 const int gn = i + g < S.nt ? group_tiles(S, i + g) : 0;
-                if (gn) issue_group(S, i + g, gn, stage[b ^ 1]);
+                if (gn) issue_group(S, i + g, gn, stage[b ^ 1], A.cap + 8);
                 else prefetch_next(b ^ 1);
                 bar_wait(&stage[b].bar, (phase >> b) & 1u);
                 phase ^= 1u << b;
                 const double* flat = stage_flat(stage[b]);
                 const unsigned* ows = reinterpret_cast<const unsigned*>(flat + g * kEvalTile + 2);
-                const double4* R0 = reinterpret_cast<const double4*>(ows + g * 32);
+                const double2* R0 = reinterpret_cast<const double2*>(ows + g * 32);
                 const int lo0 = __shfl_sync(0xffffffffu, S.to[0], i), lo1 = __shfl_sync(0xffffffffu, S.to[1], i);
-                const double4* R1 = R0 + (__shfl_sync(0xffffffffu, S.to[0], i + g) + 3 - lo0);
+                const int n0 = __shfl_sync(0xffffffffu, S.to[0], i + g) + 3 - lo0;
+                const double2* R1 = R0 + n0;
+                const int nab = n0 + __shfl_sync(0xffffffffu, S.to[1], i + g) + 3 - lo1;  // rows of both sides
                 for (int u = 0; u < g; ++u) {
                     const int t = i + u;
                     const int base = (S.j0 + t) * kEvalTile;
-                    const double4* T0 = R0 + (__shfl_sync(0xffffffffu, S.to[0], t) - lo0);
-                    const double4* T1 = R1 + (__shfl_sync(0xffffffffu, S.to[1], t) - lo1);
+                    const double2* T0 = R0 + (__shfl_sync(0xffffffffu, S.to[0], t) - lo0);
+                    const double2* T1 = R1 + (__shfl_sync(0xffffffffu, S.to[1], t) - lo1);
                     const double* sp = flat + u * kEvalTile;
                     if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
-                        eval_tile<true, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, c2, c1, snum, sden);
+                        eval_tile<true, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, nab, c2, c1, snum, sden);
                     else
-                        eval_tile<false, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, c2, c1, snum, sden);
+                        eval_tile<false, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, nab, c2, c1, snum, sden);
                 }
                 __syncwarp();  // stage b is refilled next
                 b ^= 1;
@@ -552,7 +558,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
             }
         } else {  // INIT: values computed from the job's inputs, nothing staged
             for (int i = 0; i < S.nt; ++i)
-                eval_tile<false, EM_INIT>(A, S, i, nullptr, nullptr, nullptr, nullptr, c2, c1, snum, sden);
+                eval_tile<false, EM_INIT>(A, S, i, nullptr, nullptr, nullptr, nullptr, 0, c2, c1, snum, sden);
         }
         if (S.mode == EM_SIFT) {
             snum = warp_sum(snum);

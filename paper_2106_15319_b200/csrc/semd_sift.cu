@@ -582,7 +582,7 @@ struct SolveShared {
     int moved[kSolveMaxChains];
 };
 
-__device__ void solve_small(const KnotView& kv, double4* tab, double* sm) {
+__device__ void solve_small(const KnotView& kv, const TabPlanes tab, double* sm) {
     // one thread runs the reference Thomas algorithm verbatim
     const int N = kv.n + 4;
     double* X = sm;
@@ -604,12 +604,12 @@ __device__ void solve_small(const KnotView& kv, double4* tab, double* sm) {
             rp[i] -= w * rp[i - 1];
         }
         double m = 0.0;
-        tab[N - 1] = make_double4(X[N - 1], Y[N - 1], 0.0, 0.0);
+        tab.set(N - 1, X[N - 1], Y[N - 1], 0.0, 0.0);
         for (int i = N - 2; i >= 1; --i) {
             m = (rp[i] - (X[i + 1] - X[i]) * m) / dp[i];
-            tab[i] = make_double4(X[i], Y[i], m, 1.0 / (X[i + 1] - X[i]));
+            tab.set(i, X[i], Y[i], m, 1.0 / (X[i + 1] - X[i]));
         }
-        tab[0] = make_double4(X[0], Y[0], 0.0, 1.0 / (X[1] - X[0]));
+        tab.set(0, X[0], Y[0], 0.0, 1.0 / (X[1] - X[0]));
     }
     __syncthreads();
 }
@@ -617,7 +617,7 @@ __device__ void solve_small(const KnotView& kv, double4* tab, double* sm) {
 // Exact fallback for an envelope whose speculative block boundaries disagreed:
 // the reference's sequential Thomas algorithm (emd.cpp:57-73, IEEE divisions)
 // run by one thread, using the segment-table rows as forward-sweep scratch.
-__device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) {
+__device__ __noinline__ void solve_sequential(const KnotView& kv, const TabPlanes tab) {
     const int N = kv.n + 4;
     double xp, yp, xc, yc;
     vknot(kv, 0, xp, yp);
@@ -636,7 +636,7 @@ __device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) 
             d = 2.0 * (h0 + h1) - w * h0;
             r = rhs - w * r;
         }
-        tab[i] = make_double4(xc, yc, d, r);
+        tab.set(i, xc, yc, d, r);  // forward-sweep scratch in the b plane
         xp = xc;
         yp = yc;
         xc = xn;
@@ -644,17 +644,17 @@ __device__ __noinline__ void solve_sequential(const KnotView& kv, double4* tab) 
     }
     double xn, yn;
     vknot(kv, N - 1, xn, yn);
-    tab[N - 1] = make_double4(xn, yn, 0.0, 0.0);
+    tab.set(N - 1, xn, yn, 0.0, 0.0);
     double m = 0.0;
     for (int i = N - 2; i >= 1; --i) {  // emd.cpp:70-73
-        const double4 t = tab[i];
-        m = (t.w - (xn - t.x) * m) / t.z;
-        tab[i] = make_double4(t.x, t.y, m, 1.0 / (xn - t.x));
-        xn = t.x;
+        const double2 ta = tab.a[i], tb = tab.b[i];  // {x, y}, {diag, rhs}
+        m = (tb.y - (xn - ta.x) * m) / tb.x;
+        tab.set(i, ta.x, ta.y, m, 1.0 / (xn - ta.x));
+        xn = ta.x;
     }
     double x0, y0;
     vknot(kv, 0, x0, y0);
-    tab[0] = make_double4(x0, y0, 0.0, 1.0 / (xn - x0));
+    tab.set(0, x0, y0, 0.0, 1.0 / (xn - x0));
 }
 
 #define SOLVE_PROF(k)                                                              \
@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         kv.n = s_n;
         kv.e2 = 2.0 * (double)(A.L - 1);
         kv.mom = nullptr;
-        double4* tab = A.ktab + tab_off(A, side, slot);
+        const TabPlanes tab = tab_planes(A, side, slot);
         const int N = kv.n + 4;
         if (N - 2 <= kSolveSeqMax) {
             if (tid == kSolveThreads - 1) prefetch();
@@ -850,11 +850,11 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             const double h0 = H[spad(q - 1)], h1 = H[spad(q)];
             RHS[spad(q)] = 6.0 * (div_rn(M[spad(q + 1)] - M[spad(q)], h1, RP[spad(q)]) - div_rn(M[spad(q)] - M[spad(q - 1)], h0, RP[spad(q - 1)]));
             const int i = wa + q;  // this block's segment-table rows {x, y, -, 1/h}; m follows the solve
-            if (i >= r0 && i < r1) tab[i] = make_double4(DP[spad(q)], M[spad(q)], 0.0, RP[spad(q)]);
+            if (i >= r0 && i < r1) tab.set(i, DP[spad(q)], M[spad(q)], 0.0, RP[spad(q)]);
         }
         if (tid == 0) {
-            if (r0 == 1) tab[0] = make_double4(DP[spad(0 - wa)], M[spad(0 - wa)], 0.0, RP[spad(0 - wa)]);
-            if (r1 == N - 1) tab[N - 1] = make_double4(DP[spad(N - 1 - wa)], M[spad(N - 1 - wa)], 0.0, 0.0);
+            if (r0 == 1) tab.set(0, DP[spad(0 - wa)], M[spad(0 - wa)], 0.0, RP[spad(0 - wa)]);
+            if (r1 == N - 1) tab.set(N - 1, DP[spad(N - 1 - wa)], M[spad(N - 1 - wa)], 0.0, 0.0);
         }
         __syncthreads();
         SOLVE_PROF(1);  // staging + H + RHS
@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
         // --- outputs + cross-block records: [0,1] forward state at r0-1 (from the front halo),
         // [2,3] this block's state at r1-1, [4] m at r0, [5] the m at r1 it used
         // the m column of this block's segment-table rows (x, y, 1/h were written with the rhs)
-        for (int i = r0 + tid; i < r1; i += blockDim.x) reinterpret_cast<double*>(tab + i)[2] = M[spad(i - wa)];
+        for (int i = r0 + tid; i < r1; i += blockDim.x) reinterpret_cast<double*>(tab.b + i)[0] = M[spad(i - wa)];
         if (tid == 0) {
             if (r0 > 1) {
                 rec[0] = DP[spad(r0 - 1 - wa)];
@@ -1031,7 +1031,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveCtasPerSm) k_solve(Arena 
             kv.n = (int)S.n[side];
             kv.e2 = 2.0 * (double)(A.L - 1);
             kv.mom = nullptr;
-            solve_sequential(kv, A.ktab + tab_off(A, side, slot));
+            solve_sequential(kv, tab_planes(A, side, slot));
         };
         for (int it = tid; it < nitems; it += blockDim.x) {
             const int nb = A.solve_off[it + 1] - A.solve_off[it];
