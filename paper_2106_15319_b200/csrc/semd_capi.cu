@@ -133,6 +133,7 @@ struct semd_ctx {
     cudaEvent_t ev[16]{};
     cudaStream_t rng_stream = nullptr;  // noise for the next wave is generated here, overlapping the sift
     cudaEvent_t noise_ready[2]{};
+    cudaEvent_t res_ready{};  // CEEMDAN: the stage residue is final (its std runs on the side stream)
     cudaEvent_t t0 = nullptr, t1 = nullptr;
 
     ~semd_ctx() {
@@ -144,6 +145,7 @@ struct semd_ctx {
         if (t1) cudaEventDestroy(t1);
         for (auto& e : noise_ready)
             if (e) cudaEventDestroy(e);
+        if (res_ready) cudaEventDestroy(res_ready);
         if (rng_stream) cudaStreamDestroy(rng_stream);
         if (own) cudaStreamDestroy(own);
     }
@@ -767,7 +769,14 @@ struct semd_ctx {
             cs_run_tasks(js, &res);
             return;
         }
-        const double beta_i = device_std(cs_residue(), n, cs.ens.nstd);  // emd.cpp:312
+        // beta_i = nstd * std(r_i) (emd.cpp:312): the sequential std (one SM) runs on the side stream
+        // while the noise residues' modes E_i are extracted; the first modes need it afterwards
+        scalar.alloc((2 + 2 * 256 + 8) * 8);
+        ck(cudaEventRecord(res_ready, stream), "residue event");
+        ck(cudaStreamWaitEvent(rng_stream, res_ready, 0), "residue wait");
+        semd::dev::launch_signal_std(cs_residue(), n, scalar.as<double>(), cs.ens.nstd, rng_stream);
+        double* beta_host = reinterpret_cast<double*>(status_host + 8);  // pinned
+        ck(cudaMemcpyAsync(beta_host, scalar.p, 8, cudaMemcpyDeviceToHost, rng_stream), "std");
         {  // E_i(w^(m)) for the living noise residues (emd.cpp:316-325)
             std::vector<JobSpec> js;
             std::vector<int> idx;
@@ -794,6 +803,8 @@ struct semd_ctx {
                 }
             }
         }
+        ck(cudaStreamSynchronize(rng_stream), "std");
+        const double beta_i = *beta_host;
         {  // first modes of r_i + beta_i E_i (emd.cpp:326-329)
             std::vector<JobSpec> js(cnt);
             for (int i = 0; i < cnt; ++i) {
@@ -1108,6 +1119,7 @@ int semd_ctx_create(int device, semd_ctx** out) {
             ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&c->rng_stream, cudaStreamNonBlocking), "stream");
             for (auto& e : c->noise_ready) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&c->res_ready, cudaEventDisableTiming), "event");
             c->stream = c->own;
             for (auto& ev : c->ev) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
             ck(cudaEventCreate(&c->t0), "event");
