@@ -7,15 +7,22 @@ serial-EEMD of 4096 variates x 4096 samples (random 4-sine mixtures + noise,
 fs = 4096 Hz), serialized with D = 64 (L = 17,039,296), NR = 1000
 realizations, NSTD = 0.2, MaxIter 300, sharded over the GPUs (strong scaling,
 total work fixed). One step = one complete decomposition of that input: every
-realization sifted, ensemble sums all-reduced over NCCL, means and residue.
+realization sifted, ensemble sums reduced over NCCL, means and residue.
 
 A "sifted sample" is one serialized sample processed by one sift iteration
 (SURVEY.md §8(d)); the count is the same on CPU and GPU because sift counts
 are bit-exact. value = total sifted samples of all ranks / max-over-ranks
-device time of the K timed steps. Inputs are resident in HBM for `value`;
-`e2e` runs the same decomposition through the public API from pinned host
-memory (H2D of the multi-signal, D2H of the (M, N, K+1) tensor).
-Under torchrun (N > 1) each rank owns one GPU (NCCL over NVLink).
+device time (CUDA events on the engine stream) of the K timed steps. Inputs
+are resident in HBM for `value`; `e2e` runs the same decomposition through the
+public host-pointer C ABI (semd_serial_decompose) from pinned host memory: H2D
+of the (M, N) multi-signal, concatenate, sharded EEMD (+NCCL), deconcatenate,
+D2H of the (M, N, K+1) tensor.
+
+Under torchrun (N > 1) each rank owns one GPU; the ranks' engine contexts are
+joined by an NCCL communicator inside the C ABI (semd_comm_*). No torch on
+any path of this file. The CPU legs (cpu_baseline, --impl reference) run the
+reference compiled from its own sources (oracle/_ref) and count sifted samples
+on the CPU with the reference's own extract_imf.
 """
 from __future__ import annotations
 
@@ -35,15 +42,16 @@ sys.path.insert(0, ROOT)
 
 ALGO_BYTES_PER_SIFTED_SAMPLE = 16  # one f64 read + one f64 write of the candidate
 METRIC = "serial-EEMD/CEEMDAN sifted samples/sec"  # BASELINE.json metric (the % of HBM roofline is `roofline.frac`)
+ALGO_ID = {"emd": 0, "eemd": 1, "ceemdan": 2}
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -99,98 +107,110 @@ def workload(key: str):
     return cfg, x
 
 
-# ------------------------------------------------------------------ our arm
+# ------------------------------------------------------------------ our arm (C ABI only)
+
+class Dev:
+    """A device (or pinned host) buffer owned through the C ABI."""
+
+    def __init__(self, ctx, nbytes: int, pinned_host: bool = False):
+        self.ctx, self.host = ctx, pinned_host
+        p = C.c_void_p()
+        ctx.run("semd_host_alloc" if pinned_host else "semd_device_alloc", int(nbytes), C.byref(p))
+        self.ptr, self.nbytes = p, int(nbytes)
+
+    def free(self):
+        if self.ptr:
+            self.ctx.run("semd_host_free" if self.host else "semd_device_free", self.ptr)
+            self.ptr = None
+
+
+def _stats(ctx) -> dict:
+    return ctx.stats()
+
 
 def run_ours(args, rank, world, local):
-    import torch
-    import torch.distributed as dist
-
     import paper_2106_15319_b200 as se
     from paper_2106_15319_b200 import _native as N
-    from paper_2106_15319_b200.parallel import ceemdan_distributed, eemd_distributed, shard_range
+    from paper_2106_15319_b200.parallel import init_comm
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     cfg, x = workload(args.config)
     if cfg["algo"] not in ("eemd", "ceemdan"):
         raise SystemExit("bench measures the serial-EEMD / serial-CEEMDAN configs (c2, c3, c4, c5)")
+    ctx = se.context(local)
+    init_comm(ctx, rank, world, root=0)  # EEMD sums reduced to rank 0; CEEMDAN stages all-reduced
+    ctx.set_timing(True)
     M, Nch = x.shape
     D = cfg["D"]
-    ctx = se.context(local)
-    ctx.set_timing(True)
-    lib = ctx.lib
-    scfg = {"sd_threshold": 0.2, "max_sift_iters": cfg["max_sift_iters"], "max_imfs": cfg["max_imfs"]}
-    ens = {"nstd": 0.2, "nr": cfg["nr"], "base_seed": 0}
     L = M * Nch + D * (Nch - 1)
-    # serialize once on the device (inputs resident in HBM for `value`)
-    x_cm = torch.from_numpy(np.ascontiguousarray(x.T)).to(dev)
-    s_dev = torch.empty(L, dtype=torch.float64, device=dev)
-
-    def concat(src, dst):
-        rc = lib.semd_set_stream(ctx.ptr, C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
-        ctx.check(rc)
-        # host-pointer-free concatenate: device entry via serial helper kernels
-        ctx.check(_concat_device(lib, ctx, src, dst, M, Nch, D))
-
-    concat(x_cm, s_dev)
-    torch.cuda.synchronize(dev)
+    algo = ALGO_ID[cfg["algo"]]
+    scfg = N.SiftCfg(0.2, cfg["max_sift_iters"], cfg["max_imfs"])
+    ens = N.EnsCfg(0.2, cfg["nr"], 0, 0)
+    xc = np.ascontiguousarray(x.T)  # channel-contiguous MultiSignal (types.hpp:61-62)
+    # inputs resident in HBM for `value`: the multi-signal and its serialization
+    d_x = Dev(ctx, xc.nbytes)
+    ctx.run("semd_memcpy", d_x.ptr, xc.ctypes.data_as(C.c_void_p), xc.nbytes)
+    d_s = Dev(ctx, L * 8)
+    ctx.run("semd_concatenate_device", d_x.ptr, M, Nch, D, d_s.ptr)
+    k_cap = 32
+    d_imfs, d_res = Dev(ctx, k_cap * L * 8), Dev(ctx, L * 8)
+    kout = C.c_size_t()
 
     def step():
-        return decompose_sharded(cfg, s_dev, L, scfg, ens, rank, world, ctx)
+        ctx.run("semd_decompose_device", algo, d_s.ptr, L, C.byref(scfg), C.byref(ens), d_imfs.ptr, k_cap,
+                C.byref(kout), d_res.ptr)
+        return _stats(ctx)
 
-    # warm-up
+    def barrier():
+        ctx.comm_allreduce([0.0])
+
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    stats_tot = {"sifted_samples": 0, "eval_ms": 0.0, "kernel_launches": 0, "solve_hazards": 0, "eval_launches": 0}
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    keys = ("sifted_samples", "eval_ms", "kernel_launches", "solve_hazards", "eval_launches")
+    tot = dict.fromkeys(keys, 0)
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize(dev)
-        ev0.record()
+        barrier()
+        ctx.run("semd_timer_start")
         for _ in range(args.steps):
-            imfs, res, st = step()
-            for k in stats_tot:
-                stats_tot[k] += st.get(k, 0)
-        ev1.record()
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms, float(stats_tot["sifted_samples"]), stats_tot["eval_ms"], float(stats_tot["kernel_launches"])],
-                     dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        ms_max, sifted_all, launches_all = float(tmax[0]), float(tsum[1]), float(tsum[3])
-    else:
-        ms_max, sifted_all, launches_all = ms, float(t[1]), float(t[3])
+            st = step()
+            for k in keys:
+                tot[k] += st[k]
+        ms = C.c_double()
+        ctx.run("semd_timer_stop", C.byref(ms))
+        barrier()
+    ms_max = float(ctx.comm_allreduce([ms.value], "max")[0])
+    sums = ctx.comm_allreduce([float(tot["sifted_samples"]), float(tot["kernel_launches"]),
+                               float(tot["solve_hazards"])], "sum")
+    sifted_all, launches_all, hazards_all = float(sums[0]), int(sums[1]), int(sums[2])
     value = sifted_all / (ms_max / 1e3)
-    K = int(imfs.shape[0])
-    # roofline of the dominant kernel (k_eval, the sift pass) on this rank
-    eval_s = stats_tot["eval_ms"] / 1e3
+    K = int(kout.value)
     peak, peak_kind = peaks()
-    achieved = ALGO_BYTES_PER_SIFTED_SAMPLE * stats_tot["sifted_samples"] / eval_s / 1e9 if eval_s > 0 else None
-    traffic, traffic_note = None, None
-    tf = os.path.join(ROOT, "profiles", "eval_traffic.json")
-    if os.path.exists(tf):  # measured DRAM bytes of one SIFT-mode k_eval launch (ncu --set full capture)
+    # BASELINE.md roofline: 16 B x sifted samples / wall / peak, per GPU, over the whole step
+    achieved = ALGO_BYTES_PER_SIFTED_SAMPLE * sifted_all / world / (ms_max / 1e3) / 1e9
+    eval_s = tot["eval_ms"] / 1e3
+    eval_ach = ALGO_BYTES_PER_SIFTED_SAMPLE * tot["sifted_samples"] / eval_s / 1e9 if eval_s > 0 else None
+    traffic, traffic_src = None, None
+    tf = os.path.join(ROOT, "profiles", "r02", f"traffic_{args.config}.json")
+    if os.path.exists(tf):  # dram bytes of the dominant kernel from an ncu --set full capture of this config
         try:
             t = json.load(open(tf))
-            traffic = t.get("traffic_bytes_per_launch")
-            traffic_note = {"algorithmic_bytes_per_launch": t.get("algorithmic_bytes_per_launch"),
-                            "dram_bytes_per_sifted_sample": t.get("dram_bytes_per_sifted_sample"),
-                            "source": t.get("source")}
+            traffic, traffic_src = t.get("traffic_bytes_per_launch"), t
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_detail": traffic_note,
-            "kernel": "k_eval (sift pass)", "eval_ms_per_step": stats_tot["eval_ms"] / args.steps,
+            "frac": achieved / peak, "traffic": traffic,
+            "scope": "whole step: 16 B x sifted samples / device time of the step / N GPUs (BASELINE.md)",
+            "dominant_kernel": {
+                "kernel": "k_eval (sift pass: envelopes, mean, SD sums, next extrema detection)",
+                "achieved": eval_ach, "frac": (eval_ach / peak) if eval_ach else None,
+                "ms_per_step": tot["eval_ms"] / args.steps,
+                "share_of_step": (tot["eval_ms"] / args.steps) / (ms.value / args.steps) if ms.value else None,
+                "timing": "device time of every k_eval launch (%globaltimer span, first CTA start to last CTA end)",
+                "launches_per_step": tot["eval_launches"] / args.steps},
+            "traffic_detail": traffic_src,
             "algorithmic_bytes": "16 B per sifted sample (SURVEY.md §8(d))"}
-    # end-to-end through the public API, host buffers, copies inside the timed region
-    e2e = run_e2e(args, rank, world, local, ctx, x, cfg, scfg, ens, dev)
+    e2e = run_e2e(args, rank, world, ctx, xc, cfg, algo, scfg, ens)
+    for b in (d_x, d_s, d_imfs, d_res):
+        b.free()
     out = None
     if rank == 0:
         cpu = cpu_baseline(args, x, cfg, ctx) if (world == 1 and not args.no_cpu) else None
@@ -200,93 +220,61 @@ def run_ours(args, rank, world, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "config_key": args.config, "L": L, "M": M, "N": Nch, "D": D,
                        "NR": cfg["nr"], "NSTD": 0.2, "MaxIter": cfg["max_sift_iters"], "max_imfs": cfg["max_imfs"],
-                       "K": K, "parallelism": f"realization-sharded x{world} (NCCL all-reduce of ensemble sums)",
-                       "l2": "working set (>= 3 x 136 MB per slot + knots + 4 GB sums) exceeds the 126 MB L2; no flush",
+                       "K": K, "parallelism": f"realization-sharded x{world} (NCCL reduce of ensemble sums "
+                                              "inside the C ABI)" if world > 1 else "single GPU",
+                       "l2": "working set (>= 3 x 136 MB per slot + knots + 4 GB sums) exceeds the 126 MB L2; "
+                             "no flush" if args.config in ("c4", "c5") else "small signal (L2-resident); "
+                                                                              "latency-bound config",
                        "sifted_samples_per_step": sifted_all / args.steps},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches_all), "clocks": clk.summary(),
-            "solve_hazards": stats_tot["solve_hazards"],
+            "gpu_launches": launches_all, "clocks": clk.summary(), "solve_hazards": hazards_all,
         }
     return out
 
 
-def decompose_sharded(cfg, s_dev, L, scfg, ens, rank, world, ctx):
-    """One whole decomposition with this rank's realization shard: EEMD (one all-reduce at the end)
-    or CEEMDAN (one all-reduce per stage). Returns (imfs, residue, this rank's engine stats)."""
-    from paper_2106_15319_b200.parallel import ceemdan_distributed, eemd_distributed
-    if cfg["algo"] == "ceemdan":
-        imfs, res = ceemdan_distributed(s_dev, L, scfg, ens, rank, world, ctx=ctx)
-        return imfs, res, ctx.stats()
-    return eemd_distributed(s_dev, L, scfg, ens, rank, world, ctx=ctx, k_cap=64)
-
-
-def _concat_device(lib, ctx, src, dst, M, Nch, D):
-    """semd_serial_decompose's first stage on device buffers: transition weights + concatenate kernels."""
-    return lib.semd_concatenate_device(ctx.ptr, C.c_void_p(src.data_ptr()), M, Nch, D, C.c_void_p(dst.data_ptr()))
-
-
-def run_e2e(args, rank, world, local, ctx, x, cfg, scfg, ens, dev):
-    """One decomposition per step through the public API with host buffers."""
-    import torch
-
-    from paper_2106_15319_b200.parallel import eemd_distributed
-
-    lib = ctx.lib
-    M, Nch = x.shape
+def run_e2e(args, rank, world, ctx, xc, cfg, algo, scfg, ens):
+    """The public host-pointer C ABI (semd_serial_decompose): pinned host (N, M) multi-signal in,
+    pinned host (K+1, N, M) ImfTensor out, copies inside the timed region."""
+    N_, M = xc.shape
     D = cfg["D"]
-    L = M * Nch + D * (Nch - 1)
-    host_in = torch.from_numpy(np.ascontiguousarray(x.T)).pin_memory()
+    k_cap = 33
+    h_in = Dev(ctx, xc.nbytes, pinned_host=True)
+    C.memmove(h_in.ptr, xc.ctypes.data, xc.nbytes)
+    h_out = Dev(ctx, k_cap * N_ * M * 8, pinned_host=True)
+    mo = C.c_size_t()
+
+    def one():
+        ctx.run("semd_serial_decompose", algo, C.cast(h_in.ptr, C.POINTER(C.c_double)), M, N_, D, C.byref(scfg),
+                C.byref(ens), C.cast(h_out.ptr, C.POINTER(C.c_double)), k_cap, C.byref(mo), None)
+        return ctx.stats()["sifted_samples"]
+
+    one()  # untimed: first-call allocations
     steps = max(1, args.e2e_steps)
-    out_buf = {}  # pinned host result buffer, allocated once (a caller reuses its buffers)
-
-    def one_step():
-        d_in = host_in.to(dev, non_blocking=True)  # H2D of the (M, N) multi-signal
-        s_dev = torch.empty(L, dtype=torch.float64, device=dev)
-        ctx.check(_concat_device(lib, ctx, d_in, s_dev, M, Nch, D))
-        imfs, res, st = decompose_sharded(cfg, s_dev, L, scfg, ens, rank, world, ctx)
-        nbytes = 0
-        if rank == 0:
-            modes = torch.cat([imfs, res[None, :]], 0).contiguous()
-            tensor = torch.empty((modes.shape[0], Nch, M), dtype=torch.float64, device=dev)
-            ctx.check(lib.semd_deconcatenate_device(ctx.ptr, C.c_void_p(modes.data_ptr()), modes.shape[0], L, M,
-                                                    Nch, D, C.c_void_p(tensor.data_ptr())))
-            host_out = out_buf.get(tuple(tensor.shape))
-            if host_out is None:
-                out_buf.clear()
-                host_out = out_buf[tuple(tensor.shape)] = torch.empty(tensor.shape, dtype=torch.float64,
-                                                                       pin_memory=True)
-            host_out.copy_(tensor)  # D2H of the (K+1, N, M) mode tensor
-            nbytes = host_out.numel() * 8
-        return st.get("sifted_samples", 0), nbytes
-
-    one_step()  # untimed: learns the mode count and allocates the pinned result buffer
-    h2d = d2h = 0
-    torch.cuda.synchronize(dev)
+    ctx.comm_allreduce([0.0])
     t0 = time.perf_counter()
     sifted = 0
     for _ in range(steps):
-        sf, nb = one_step()
-        sifted += sf
-        h2d += host_in.numel() * 8
-        d2h += nb
-    torch.cuda.synchronize(dev)
+        sifted += one()
     wall = time.perf_counter() - t0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([wall, float(sifted)], dtype=torch.float64, device=dev)
-        w = t.clone()
-        dist.all_reduce(w, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        wall, sifted = float(w[0]), float(t[1])
-    return {"value": sifted / wall, "unit": "sifted samples/s", "h2d_bytes_per_step": h2d // steps,
-            "d2h_bytes_per_step": d2h // steps, "steps": steps,
-            "path": f"pinned host (M,N) -> H2D -> concatenate -> sharded {cfg['algo'].upper()} (+NCCL) -> "
-                    "deconcatenate -> D2H (M,N,K+1)"}
+    ctx.comm_allreduce([0.0])
+    wall = float(ctx.comm_allreduce([wall], "max")[0])
+    sifted = float(ctx.comm_allreduce([float(sifted)], "sum")[0])
+    d2h = int(mo.value) * N_ * M * 8  # the ImfTensor, on the rank that holds the result
+    h_in.free()
+    h_out.free()
+    return {"value": sifted / wall, "unit": "sifted samples/s", "h2d_bytes_per_step": xc.nbytes * world,
+            "d2h_bytes_per_step": d2h, "steps": steps, "timing": "host wall clock around the ABI call, max over ranks",
+            "path": "semd_serial_decompose: pinned host (M,N) -> H2D -> concatenate -> "
+                    f"{cfg['algo'].upper()}{' (+NCCL)' if world > 1 else ''} -> deconcatenate -> D2H (M,N,K+1)"}
 
 
-# ------------------------------------------------------------------ CPU baselines
+# ------------------------------------------------------------------ CPU baselines (reference only)
 
-def _ref_or_port():
+def cpu_threads():
+    return max(1, min(os.cpu_count() or 1, 64))
+
+
+def _ref():
     from oracle.ffi import Oracle, Ref, build, ref_available
     if ref_available():
         return Ref(), "reference"
@@ -294,95 +282,111 @@ def _ref_or_port():
     return Oracle(), "port"
 
 
-def cpu_sample(x, cfg, threads, count=None, scale=1):
-    """count realizations (default: one per thread) of the workload on `threads` CPU threads."""
-    from paper_2106_15319_b200 import workloads as W  # noqa: F401
-    impl, kind = _ref_or_port()
-    M, Nch = x.shape
-    D = cfg["D"]
-    xc = np.ascontiguousarray(x.T)
-    s = impl.concatenate(xc, M, Nch, D)
-    count = count or threads
-    t0 = time.perf_counter()
-    if cfg["algo"] == "ceemdan":  # the reference ceemdan() is sequential: one full decomposition, one thread
-        impl.decompose(s, 2, iters=cfg["max_sift_iters"], imfs=cfg["max_imfs"], nstd=0.2, nr=cfg["nr"])
-    elif kind == "reference":
-        impl.emd_realizations(s, 0, count, threads, iters=cfg["max_sift_iters"], imfs=cfg["max_imfs"], nstd=0.2)
-    else:
-        from concurrent.futures import ThreadPoolExecutor
-        with ThreadPoolExecutor(threads) as ex:
-            list(ex.map(lambda m: impl.eemd_partial(s, m, m + 1, iters=cfg["max_sift_iters"], imfs=cfg["max_imfs"],
-                                                    nr=cfg["nr"]), range(count)))
-    return time.perf_counter() - t0, kind, s
+def ceemdan_sifted(trace, n: int) -> int:
+    """n x (find_extrema calls of the CEEMDAN replay that led to a subtraction): the reference's
+    own extract_imf loop (emd.cpp:131-151) subtracts iff both envelopes exist."""
+    ok = (trace["task"] != 3) & (trace["n_max"] >= 2) & (trace["n_min"] >= 2)
+    return int(n) * int(ok.sum())
 
 
-def sifted_for(s, cfg, m_end, ctx):
-    """Sifted samples of realizations [0, m_end) (CEEMDAN: the whole decomposition) from the
-    parity-checked GPU engine."""
-    if cfg["algo"] == "ceemdan":
-        import paper_2106_15319_b200 as se
-        se.decompose(s, "ceemdan", max_sift_iters=cfg["max_sift_iters"], max_imfs=cfg["max_imfs"], nr=cfg["nr"])
-        return ctx.stats()["sifted_samples"]
+class CpuSample:
+    """A bounded sample of the workload on the reference CPU implementation, with its sifted-sample
+    count computed on the CPU (outside any timed region) by the reference's own extract_imf."""
+
+    def __init__(self, x, cfg, threads):
+        self.impl, self.kind = _ref()
+        M, Nch = x.shape
+        self.s = self.impl.concatenate(np.ascontiguousarray(x.T), M, Nch, cfg["D"])
+        self.cfg, self.T = cfg, threads
+        it, im = cfg["max_sift_iters"], cfg["max_imfs"]
+        if cfg["algo"] == "ceemdan":  # the reference ceemdan() is sequential: the whole decomposition, one thread
+            self.T = 1
+            if self.kind == "reference":
+                _, _, tr = self.impl.ceemdan_traced(self.s, iters=it, imfs=im, nr=cfg["nr"])
+                self.sifted = ceemdan_sifted(tr, self.s.size)
+            else:
+                _, _, _, tr = self.impl.decompose(self.s, 2, iters=it, imfs=im, nr=cfg["nr"], trace_cap=1 << 22)
+                self.sifted = ceemdan_sifted(tr, self.s.size)
+            self.per_m = None
+            self.desc = "the whole decomposition by the reference ceemdan() (sequential, one thread)"
+        else:
+            if self.kind == "reference":
+                self.sifted, self.per_m = self.impl.realization_sifts(self.s, 0, self.T, self.T, iters=it, imfs=im)
+            else:
+                raise RuntimeError("oracle/_ref (the reference built from its sources) is required for EEMD baselines")
+            self.desc = (f"{self.T} realizations (m=0..{self.T - 1}) of the same workload, one per host thread, each "
+                         "the reference emd() of x + beta*white_noise(derive_seed(0, m)) (eemd()'s per-realization "
+                         "work without its NR x K x L store)")
+
+    def run(self, x_short=None) -> float:
+        it, im = self.cfg["max_sift_iters"], self.cfg["max_imfs"]
+        s = self.s if x_short is None else x_short
+        t0 = time.perf_counter()
+        if self.cfg["algo"] == "ceemdan":
+            self.impl.decompose(s, 2, iters=it, imfs=im, nr=self.cfg["nr"])
+        else:
+            self.impl.emd_realizations(s, 0, self.T, self.T, iters=it, imfs=im)
+        return time.perf_counter() - t0
+
+
+def gpu_per_realization_sifts(s, cfg, T) -> list[int]:
+    """GPU sift counts of realizations m = 0..T-1 (same beta and seeds as the NR ensemble), from the
+    engine's parity trace: one record per find_extrema call; a call with both envelopes subtracts."""
     import paper_2106_15319_b200 as se
     from paper_2106_15319_b200 import _native as N
-    lib = ctx.lib
-    d_s = None
-    import torch
-    d_s = torch.from_numpy(s).cuda()
-    sums = torch.zeros((64, s.size), dtype=torch.float64, device=d_s.device)
+    c = se.context(0)
+    cap = 400 * T
+    buf = (N.TraceRec * cap)()
+    tr = N.Trace(C.cast(buf, C.c_void_p), cap, 0)
     k = C.c_size_t()
-    ctx.check(lib.semd_eemd_partial_device(ctx.ptr, C.c_void_p(d_s.data_ptr()), s.size,
-                                           C.byref(N.SiftCfg(0.2, cfg["max_sift_iters"], cfg["max_imfs"])),
-                                           C.byref(N.EnsCfg(0.2, cfg["nr"], 0, 0)), 0, m_end,
-                                           C.c_void_p(sums.data_ptr()), 64, C.byref(k)))
-    return ctx.stats()["sifted_samples"]
-
-
-def cpu_threads():
-    return max(1, min(os.cpu_count() or 1, 64))
+    x = np.ascontiguousarray(s, dtype=np.float64)
+    c.run("semd_decompose", ALGO_ID["eemd"], x.ctypes.data_as(N._dp), x.size,
+          C.byref(N.SiftCfg(0.2, cfg["max_sift_iters"], cfg["max_imfs"])), C.byref(N.EnsCfg(0.2, T, 0, 0)),
+          None, 64, C.byref(k), None, None, C.byref(tr))
+    rec = np.frombuffer(C.string_at(buf, min(tr.count, cap) * C.sizeof(N.TraceRec)),
+                        dtype=[("task", "<i4"), ("m", "<i4"), ("k", "<i4"), ("iter", "<i4"), ("n_max", "<u4"),
+                               ("n_min", "<u4"), ("hash", "<u8")])
+    ok = (rec["task"] == 0) & (rec["n_max"] >= 2) & (rec["n_min"] >= 2)
+    return [int((ok & (rec["m"] == m)).sum()) for m in range(T)]
 
 
 def cpu_baseline(args, x, cfg, ctx):
     T = cpu_threads()
-    if cfg["algo"] == "ceemdan":
-        wall, kind, s = cpu_sample(x, cfg, 1)
-        sifted = sifted_for(s, cfg, cfg["nr"], ctx)
-        return {"value": sifted / wall, "unit": "sifted samples/s", "cores": 1, "kind": kind,
-                "sample": f"the whole decomposition by the reference ceemdan() (sequential), wall {wall:.1f} s"}
-    wall, kind, s = cpu_sample(x, cfg, T)
-    sifted = sifted_for(s, cfg, T, ctx)
-    return {"value": sifted / wall, "unit": "sifted samples/s", "cores": T, "kind": kind,
-            "sample": f"{T} realizations (m=0..{T - 1}) of the same workload, one per thread, reference emd() each "
-                      f"(eemd()'s per-realization work without its NR x K x L store); sifted count from the "
-                      f"parity-checked GPU run of the same realizations; wall {wall:.1f} s"}
+    smp = CpuSample(x, cfg, T)
+    wall = smp.run()
+    out = {"value": smp.sifted / wall, "unit": "sifted samples/s", "cores": smp.T, "kind": smp.kind,
+           "sample": f"{smp.desc}; sifted samples {smp.sifted} counted on the CPU by the reference's extract_imf "
+                     f"(outside the timed region); wall {wall:.1f} s"}
+    if smp.per_m is not None:  # free full-size parity: the GPU's per-realization sift counts must equal the CPU's
+        gpu = gpu_per_realization_sifts(smp.s, cfg, smp.T)
+        out["gpu_sift_counts_equal_cpu"] = bool(list(map(int, smp.per_m)) == gpu)
+        out["per_realization_sifts"] = list(map(int, smp.per_m))
+    return out
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU implementation on this box's host cores."""
+    """--impl reference: the reference's CPU implementation (oracle/_ref, built from its sources)
+    on this box's host cores. Never loads the GPU library."""
     if rank != 0:
         return None
     cfg, x = workload(args.config)
     T = cpu_threads()
-    import paper_2106_15319_b200 as se
-    ctx = se.context(0)
-    # warm-up: a short run on 1/16 of the realizations' length (page-in, thread start)
-    for _ in range(args.warmup):
-        cpu_sample(x[: max(64, x.shape[0] // 16)], cfg, T, count=T)
-    total_wall, kind, s = 0.0, None, None
+    smp = CpuSample(x, cfg, T)  # sifted-sample count on the CPU, outside the timed region
+    short = smp.impl.concatenate(np.ascontiguousarray(x[: max(64, x.shape[0] // 16)].T),
+                                 max(64, x.shape[0] // 16), x.shape[1], cfg["D"])
+    for _ in range(args.warmup):  # page-in, thread start: the sample on 1/16 of the rows
+        smp.run(short)
+    total = 0.0
     for _ in range(args.steps):
-        w, kind, s = cpu_sample(x, cfg, T)
-        total_wall += w
-    sifted = sifted_for(s, cfg, T, ctx) * args.steps
-    value = sifted / total_wall
-    if cfg["algo"] == "ceemdan":
-        T = 1  # the reference ceemdan() is sequential
+        total += smp.run()
+    value = smp.sifted * args.steps / total
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "sifted samples/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_wall / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "config_key": args.config,
-                       "sample": f"each step = {T} realizations on {T} host threads"},
-            "cpu_baseline": {"value": value, "unit": "sifted samples/s", "cores": T, "kind": kind,
-                             "sample": f"{T} realizations per step, one per thread (reference emd() per realization)"},
+                       "sample": f"each step = {smp.desc}"},
+            "cpu_baseline": {"value": value, "unit": "sifted samples/s", "cores": smp.T, "kind": smp.kind,
+                             "sample": f"{smp.desc}; {smp.sifted} sifted samples per step, counted on the CPU"},
             "e2e": {"value": value, "unit": "sifted samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -399,23 +403,9 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
-    if args.impl == "reference":
-        out = run_reference(args, rank, world)
-        if out is not None:
-            print(json.dumps(out), flush=True)
-        return
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    out = run_ours(args, rank, world, local)
+    out = run_reference(args, rank, world) if args.impl == "reference" else run_ours(args, rank, world, local)
     if out is not None:
         print(json.dumps(out), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

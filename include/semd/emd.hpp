@@ -183,4 +183,23 @@ inline Decomposition decompose(const Signal& x, Algorithm algo, const SiftConfig
     return detail::run(static_cast<int>(algo), x, cfg, ens);
 }
 
+// ---- multi-GPU (B200 extension; the reference is single-process) ----------------------------
+// One process or thread per GPU (SEMD_DEVICE selects it). Rank 0 calls comm_unique_id() and
+// ships the bytes to the other ranks; every rank then calls comm_init(). From then on eemd,
+// ceemdan, decompose and serial_decompose on this thread are collective: each rank passes the
+// same input, sifts its shard of the realizations, and NCCL combines the ensemble sums
+// (include/semd_b200.h, semd_comm_*). root >= 0 delivers EEMD results to that rank only.
+inline std::vector<unsigned char> comm_unique_id() {
+    std::vector<unsigned char> id(SEMD_COMM_ID_BYTES);
+    detail::check(semd_comm_unique_id(id.data(), id.size()));
+    return id;
+}
+
+inline void comm_init(const std::vector<unsigned char>& id, int rank, int world, int root = -1) {
+    detail::check(semd_comm_init(detail::ctx(), id.data(), id.size(), rank, world));
+    detail::check(semd_comm_set_root(detail::ctx(), root));
+}
+
+inline void comm_destroy() { detail::check(semd_comm_destroy(detail::ctx())); }
+
 }  // namespace semd

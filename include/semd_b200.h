@@ -157,6 +157,11 @@ int semd_decompose_device(semd_ctx* ctx, int algo, const double* d_x, size_t n, 
 int semd_eemd_partial_device(semd_ctx* ctx, const double* d_x, size_t n, const semd_sift_cfg* cfg,
                              const semd_ens_cfg* ens, int32_t m_begin, int32_t m_end, double* d_sums,
                              size_t k_cap, size_t* k_out);
+/* The same, plus the parity trace of the shard's realizations (one record per find_extrema
+ * call, task 0, field m = global realization index; trace may be NULL). */
+int semd_eemd_partial_traced_device(semd_ctx* ctx, const double* d_x, size_t n, const semd_sift_cfg* cfg,
+                                    const semd_ens_cfg* ens, int32_t m_begin, int32_t m_end, double* d_sums,
+                                    size_t k_cap, size_t* k_out, semd_trace* trace);
 /* imfs *= 1/nr; residue = x - sum_k imfs_k (emd.cpp:252-260). */
 int semd_ensemble_finish_device(semd_ctx* ctx, const double* d_x, size_t n, double* d_sums, size_t K, int32_t nr,
                                 double* d_residue);
@@ -198,6 +203,40 @@ int semd_ceemdan_shard_stage(semd_ctx* ctx, double* d_partial);
 int semd_ceemdan_shard_finish_stage(semd_ctx* ctx, const double* d_total, int32_t nr, int32_t check_zero,
                                     double* d_mode_out, int32_t* accepted);
 int semd_ceemdan_shard_residue(semd_ctx* ctx, double* d_res_out);
+
+/* ---- multi-GPU (B200 extension; the reference is single-process) -------------------------
+ * One process (or thread) per GPU, one context each, joined by an NCCL communicator over
+ * NVLink/NVSwitch. Rank 0 makes the id with semd_comm_unique_id and ships its bytes to the
+ * other ranks (any side channel); every rank calls semd_comm_init collectively. After that,
+ * EEMD and CEEMDAN calls on the context (semd_decompose, semd_serial_decompose and their
+ * *_device forms) are collective: every rank passes the same input, rank r sifts realizations
+ * shard_range(nr, r, W) (contiguous; seeds from the global index, emd.cpp:238), and
+ *   EEMD:    ncclAllReduce(max) of K, one ncclReduce/ncclAllReduce(sum) of the K x n sums,
+ *            then the finish (emd.cpp:246-261);
+ *   CEEMDAN: one ncclAllReduce(sum) of n doubles per stage (emd.cpp:301-306, :331-339).
+ * Across ranks the ensemble sum is not realization-ordered, so N > 1 results equal the
+ * single-GPU ones to rounding (not bit-for-bit); a 1-rank communicator is bit-identical.
+ * EMD calls are replicated (every rank computes the same result). */
+#define SEMD_COMM_ID_BYTES 128
+int semd_comm_unique_id(void* id_out, size_t bytes);
+int semd_comm_init(semd_ctx* ctx, const void* id, size_t bytes, int rank, int world);
+/* root >= 0: the EEMD sums are reduced to that rank only (others get K and no outputs);
+ * root < 0 (default): every rank receives the full result. */
+int semd_comm_set_root(semd_ctx* ctx, int root);
+int semd_comm_info(semd_ctx* ctx, int* rank, int* world);
+/* Small host-side reductions over the communicator (op 0 sum, 1 max); no-op without one. */
+int semd_comm_allreduce_host(semd_ctx* ctx, double* vals, size_t n, int op);
+int semd_comm_destroy(semd_ctx* ctx);
+
+/* ---- device memory and timing on the context's stream (driver / benchmark plumbing) ------ */
+int semd_device_alloc(semd_ctx* ctx, size_t bytes, void** d_out);
+int semd_device_free(semd_ctx* ctx, void* d);
+int semd_host_alloc(semd_ctx* ctx, size_t bytes, void** h_out); /* pinned host memory */
+int semd_host_free(semd_ctx* ctx, void* h);
+int semd_memcpy(semd_ctx* ctx, void* dst, const void* src, size_t bytes); /* any direction, synchronous */
+/* CUDA events on the context stream: device milliseconds between start and stop. */
+int semd_timer_start(semd_ctx* ctx);
+int semd_timer_stop(semd_ctx* ctx, double* ms);
 
 #ifdef __cplusplus
 }

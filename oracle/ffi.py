@@ -259,6 +259,12 @@ class Ref:
                                            C.c_int, C.c_int, C.c_int, _dp]
         L.ref_serial_decompose.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, C.c_double, C.c_int,
                                            C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_void_p]
+        L.ref_realization_summary.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                              C.c_int, C.c_int, _u64p, C.c_size_t, C.c_void_p]
+        L.ref_eemd_stream.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
+                                      C.c_uint64, C.c_int, C.c_void_p]
+        L.ref_realization_sifts.argtypes = [_dp, C.c_size_t, C.c_double, C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                            C.c_int, C.c_int, C.c_int, _u64p, _i32p]
 
     def _chk(self, rc):
         if rc != 0:
@@ -369,6 +375,51 @@ class Ref:
         self._chk(self.lib.ref_emd_realizations(_d(x), x.size, sd, iters, imfs, nstd, seed, m_begin, count, threads,
                                                 C.byref(chk)))
         return chk.value
+
+    def realization_summary(self, x, m, sample_idx, check=False, sd=0.2, iters=300, imfs=0, nstd=0.2, seed=0):
+        """EEMD realization m (emd.cpp:237-244) through the replayer: (sift counts per IMF, trace,
+        per-IMF L2 norms, IMF values at sample_idx (K x ns)). check: also bit-compare with semd::emd."""
+        x = _f64(x)
+        idx = np.ascontiguousarray(sample_idx, dtype=np.uint64)
+        o = self.lib.ref_out_new()
+        try:
+            self._chk(self.lib.ref_realization_summary(_d(x), x.size, sd, iters, imfs, nstd, seed, int(m), int(check),
+                                                       idx.ctypes.data_as(_u64p), idx.size, o))
+            L = self.lib
+            K = L.ref_out_K(o)
+            ns = idx.size
+            samples = np.ctypeslib.as_array(L.ref_out_imfs(o), shape=(K * ns,)).copy().reshape(K, ns) if K * ns \
+                else np.zeros((K, ns))
+            norms = np.ctypeslib.as_array(L.ref_out_residue(o), shape=(K,)).copy() if K else np.zeros(0)
+            nc = L.ref_out_ncounts(o)
+            counts = np.ctypeslib.as_array(L.ref_out_counts(o), shape=(nc,)).copy() if nc else np.zeros(0, np.int32)
+            nt = L.ref_out_ntrace(o)
+            trace = np.frombuffer(C.string_at(L.ref_out_trace(o), nt * TRACE_DTYPE.itemsize), dtype=TRACE_DTYPE).copy()
+            return counts, trace, norms, samples
+        finally:
+            self.lib.ref_out_free(o)
+
+    def eemd_stream(self, x, threads, sd=0.2, iters=300, imfs=0, nstd=0.2, nr=100, seed=0):
+        """semd::eemd (bit-identical) with realizations streamed in order over `threads` workers.
+        Returns (imfs KxL, residue L, per-realization K)."""
+        x = _f64(x)
+        o = self.lib.ref_out_new()
+        try:
+            self._chk(self.lib.ref_eemd_stream(_d(x), x.size, sd, iters, imfs, nstd, nr, seed, threads, o))
+            imfs_, res, counts, _ = self._out(o, x.size)
+            return imfs_, res, counts
+        finally:
+            self.lib.ref_out_free(o)
+
+    def realization_sifts(self, x, m_begin, count, threads, sd=0.2, iters=300, imfs=0, nstd=0.2, seed=0):
+        """(n x total sift iterations, per-realization sift totals) of EEMD realizations
+        [m_begin, m_begin+count), computed on the CPU by the reference's extract_imf."""
+        x = _f64(x)
+        tot = C.c_uint64()
+        per = np.zeros(max(count, 1), np.int32)
+        self._chk(self.lib.ref_realization_sifts(_d(x), x.size, sd, iters, imfs, nstd, seed, m_begin, count, threads,
+                                                 C.byref(tot), per.ctypes.data_as(_i32p)))
+        return int(tot.value), per[:count]
 
     def concatenate(self, x_cm, M, N, D, naive=False):
         x = _f64(x_cm).ravel()

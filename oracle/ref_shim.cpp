@@ -8,8 +8,14 @@
 // re-driven through the reference's public find_extrema / envelope so that
 // every find_extrema call's extrema lists can be hashed; ref_emd_traced checks
 // its own output against semd::emd bit-for-bit and reports any divergence.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <random>
 #include <string>
 #include <thread>
@@ -373,6 +379,181 @@ int ref_ceemdan_traced(const double* x, std::size_t n, double sd, int iters, int
         return 3;
     }
     return rc;
+}
+
+
+// ---- full-size ensemble goldens (tests/golden/make_golden_ensembles.py) ------------------
+
+// One EEMD realization m of x (emd.cpp:237-244: w = white_noise(n, derive_seed(seed, m)),
+// xm = x + beta*w, emd(xm)) through the replayer: per-IMF sift counts, the trace, and a
+// compact summary of the IMFs (per-IMF sequential L2 norm, values at `ns` fixed indices).
+// check != 0 also runs semd::emd and fails (3) unless the replay is bit-identical.
+// Out: K, counts = sift counts, trace, imfs = K x ns sampled values, residue = K norms.
+int ref_realization_summary(const double* x, std::size_t n, double sd, int iters, int imfs, double nstd,
+                            uint64_t seed, int m, int check, const uint64_t* sidx, std::size_t ns, void* out) {
+    int mismatch = 0;
+    int rc = guard([&] {
+        Out* o = static_cast<Out*>(out);
+        const semd::Signal s(x, x + n);
+        const semd::SiftConfig cfg{sd, iters, imfs};
+        const double beta = nstd * semd::signal_std(s);
+        semd::Signal xm(n);
+        {
+            const semd::Signal w = semd::white_noise(n, semd::derive_seed(seed, std::uint64_t(m)));
+            for (std::size_t i = 0; i < n; ++i) xm[i] = s[i] + beta * w[i];
+        }
+        const semd::Decomposition d = replay_emd(xm, cfg, &o->trace, &o->counts, m);
+        if (check && !same(d, semd::emd(xm, cfg))) mismatch = 1;
+        o->K = d.imfs.size();
+        o->imfs.assign(o->K * ns, 0.0);
+        o->residue.assign(o->K, 0.0);
+        for (std::size_t k = 0; k < o->K; ++k) {
+            double acc = 0.0;
+            for (double v : d.imfs[k]) acc += v * v;
+            o->residue[k] = std::sqrt(acc);
+            for (std::size_t j = 0; j < ns; ++j) o->imfs[k * ns + j] = d.imfs[k][sidx[j]];
+        }
+    });
+    if (rc == 0 && mismatch) {
+        g_err = "replay diverged from semd::emd";
+        return 3;
+    }
+    return rc;
+}
+
+// The reference eemd() (emd.cpp:228-262) with its NR x K x L realization store replaced by
+// in-order streaming: realizations are decomposed by the UNMODIFIED semd::emd on `threads`
+// workers and added to the sums strictly in realization order, so the result is bit-identical
+// to semd::eemd (skipping a missing IMF equals adding eemd()'s zero padding). Needed where
+// eemd() itself cannot run (C5 would store 2.2 TB). Out: K, imfs (means), residue,
+// counts = per-realization K.
+int ref_eemd_stream(const double* x, std::size_t n, double sd, int iters, int imfs, double nstd, int nr,
+                    uint64_t seed, int threads, void* out) {
+    return guard([&] {
+        Out* o = static_cast<Out*>(out);
+        const semd::Signal s(x, x + n);
+        const semd::SiftConfig cfg{sd, iters, imfs};
+        if (nr < 1) throw semd::InvalidInput("ensemble: nr must be at least 1");
+        if (nstd == 0.0) {
+            store(o, semd::emd(s, cfg));
+            return;
+        }
+        const double beta = nstd * semd::signal_std(s);
+        const int T = std::max(1, threads);
+        std::mutex mu;
+        std::condition_variable cv;
+        std::map<int, std::vector<semd::Signal>> ready;
+        int next_add = 0;
+        std::atomic<int> next_m{0};
+        std::string err;
+        auto work = [&] {
+            for (;;) {
+                const int m = next_m.fetch_add(1);
+                if (m >= nr) return;
+                {
+                    std::unique_lock<std::mutex> lk(mu);  // bound the realizations held in memory
+                    cv.wait(lk, [&] { return m < next_add + T + 1 || !err.empty(); });
+                    if (!err.empty()) return;
+                }
+                try {
+                    const semd::Signal w = semd::white_noise(n, semd::derive_seed(seed, std::uint64_t(m)));
+                    semd::Signal xm(n);
+                    for (std::size_t i = 0; i < n; ++i) xm[i] = s[i] + beta * w[i];
+                    semd::Decomposition d = semd::emd(xm, cfg);
+                    std::lock_guard<std::mutex> lk(mu);
+                    ready[m] = std::move(d.imfs);
+                } catch (const std::exception& e) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    err = e.what();
+                }
+                cv.notify_all();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t) pool.emplace_back(work);
+        std::vector<semd::Signal> sums;
+        o->counts.clear();
+        for (int m = 0; m < nr; ++m) {
+            std::vector<semd::Signal> r;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return ready.count(m) || !err.empty(); });
+                if (!err.empty()) break;
+                r = std::move(ready[m]);
+                ready.erase(m);
+            }
+            o->counts.push_back(int32_t(r.size()));
+            while (sums.size() < r.size()) sums.emplace_back(n, 0.0);
+            for (std::size_t k = 0; k < r.size(); ++k)
+                for (std::size_t i = 0; i < n; ++i) sums[k][i] += r[k][i];
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                next_add = m + 1;
+            }
+            cv.notify_all();
+        }
+        for (auto& t : pool) t.join();
+        if (!err.empty()) throw std::runtime_error(err);
+        const double inv = 1.0 / static_cast<double>(nr);
+        for (auto& imf : sums)
+            for (double& v : imf) v *= inv;
+        semd::Decomposition d;
+        d.residue = s;
+        for (const auto& imf : sums)
+            for (std::size_t i = 0; i < n; ++i) d.residue[i] -= imf[i];
+        d.imfs = std::move(sums);
+        store(o, d);
+    });
+}
+
+// Sift counts of EEMD realizations [m_begin, m_begin+count) on `threads` threads: emd()'s
+// loop (emd.cpp:155-172) over the reference's public extract_imf (emd.hpp:62), which
+// returns the sift count emd() discards. *sifted = n * total sift iterations. The CPU
+// baseline times semd::emd and takes its sifted-sample count from here (computed on the CPU).
+int ref_realization_sifts(const double* x, std::size_t n, double sd, int iters, int imfs, double nstd,
+                          uint64_t seed, int m_begin, int count, int threads, uint64_t* sifted, int32_t* per_m) {
+    return guard([&] {
+        const semd::Signal s(x, x + n);
+        const semd::SiftConfig cfg{sd, iters, imfs};
+        const double beta = nstd * semd::signal_std(s);
+        const int T = std::max(1, threads);
+        std::vector<uint64_t> part(std::size_t(T), 0);
+        std::vector<std::string> errs(static_cast<std::size_t>(T));
+        auto work = [&](int tid) {
+            try {
+                for (int q = tid; q < count; q += T) {
+                    const int m = m_begin + q;
+                    const semd::Signal w = semd::white_noise(n, semd::derive_seed(seed, std::uint64_t(m)));
+                    semd::Signal residue(n);
+                    for (std::size_t i = 0; i < n; ++i) residue[i] = s[i] + beta * w[i];
+                    int32_t sifts = 0, k = 0;
+                    while (cfg.max_imfs == 0 || k < cfg.max_imfs) {
+                        semd::SiftResult r;
+                        try {
+                            r = semd::extract_imf(residue, cfg);
+                        } catch (const semd::InsufficientExtrema&) {
+                            break;
+                        }
+                        for (std::size_t i = 0; i < n; ++i) residue[i] -= r.imf[i];
+                        sifts += r.sift_count;
+                        ++k;
+                    }
+                    if (per_m) per_m[q] = sifts;
+                    part[std::size_t(tid)] += uint64_t(sifts) * n;
+                }
+            } catch (const std::exception& e) {
+                errs[std::size_t(tid)] = e.what();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t) pool.emplace_back(work, t);
+        for (auto& t : pool) t.join();
+        for (const auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
+        uint64_t tot = 0;
+        for (uint64_t v : part) tot += v;
+        *sifted = tot;
+    });
 }
 
 int ref_concatenate(const double* x, std::size_t M, std::size_t N, std::size_t D, int naive, double* out) {

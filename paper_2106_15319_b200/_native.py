@@ -20,6 +20,7 @@ SEMD_INSUFFICIENT_EXTREMA = 2
 SEMD_CAPACITY = 3
 SEMD_CUDA_ERROR = 4
 SEMD_NO_MEMORY = 5
+SEMD_COMM_ID_BYTES = 128
 
 ALGOS = {"emd": 0, "eemd": 1, "ceemdan": 2}
 
@@ -85,6 +86,9 @@ SIGNATURES = {
                                         C.POINTER(EnsCfg), C.c_void_p, C.c_size_t, _szp, C.c_void_p]),
     "semd_eemd_partial_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(SiftCfg), C.POINTER(EnsCfg),
                                            C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, _szp]),
+    "semd_eemd_partial_traced_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(SiftCfg),
+                                                  C.POINTER(EnsCfg), C.c_int32, C.c_int32, C.c_void_p, C.c_size_t,
+                                                  _szp, C.POINTER(Trace)]),
     "semd_ensemble_finish_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int32,
                                               C.c_void_p]),
     "semd_concatenate_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p]),
@@ -105,6 +109,19 @@ SIGNATURES = {
     "semd_ceemdan_shard_finish_stage": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                                   C.POINTER(C.c_int32)]),
     "semd_ceemdan_shard_residue": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "semd_comm_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
+    "semd_comm_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int]),
+    "semd_comm_set_root": (C.c_int, [C.c_void_p, C.c_int]),
+    "semd_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "semd_comm_allreduce_host": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_int]),
+    "semd_comm_destroy": (C.c_int, [C.c_void_p]),
+    "semd_device_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "semd_device_free": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "semd_host_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "semd_host_free": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "semd_memcpy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
+    "semd_timer_start": (C.c_int, [C.c_void_p]),
+    "semd_timer_stop": (C.c_int, [C.c_void_p, _dp]),
 }
 # test-only hook (not part of the reference API)
 EXTRA = {"semd_set_noise_override": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t]),

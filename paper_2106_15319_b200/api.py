@@ -68,6 +68,10 @@ class Context:
 
     def __init__(self, device: int = 0):
         self.lib = N.load()
+        # ctypes releases the GIL during foreign calls; one context's arena, pinned staging and
+        # streams must not be entered by two threads at once (semd_b200.h: one context per host
+        # thread, or external locking). Every call on this context holds this lock.
+        self.lock = threading.RLock()
         p = C.c_void_p()
         _check(self.lib, self.lib.semd_ctx_create(device, C.byref(p)))
         self.ptr = p
@@ -87,34 +91,68 @@ class Context:
     def check(self, rc: int):
         _check(self.lib, rc)
 
+    def call(self, name: str, *args) -> int:
+        """lib.<name>(ctx, *args) under the context lock; returns the status code."""
+        with self.lock:
+            return getattr(self.lib, name)(self.ptr, *args)
+
+    def run(self, name: str, *args) -> None:
+        self.check(self.call(name, *args))
+
+    # ---- multi-GPU (semd_comm_*): one context per rank, NCCL communicator ----
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        lib = N.load()
+        buf = C.create_string_buffer(N.SEMD_COMM_ID_BYTES)
+        _check(lib, lib.semd_comm_unique_id(buf, N.SEMD_COMM_ID_BYTES))
+        return buf.raw
+
+    def comm_init(self, uid: bytes, rank: int, world: int, root: int = -1) -> None:
+        buf = C.create_string_buffer(bytes(uid), N.SEMD_COMM_ID_BYTES)
+        self.run("semd_comm_init", buf, N.SEMD_COMM_ID_BYTES, int(rank), int(world))
+        self.run("semd_comm_set_root", int(root))
+
+    def comm_info(self) -> tuple[int, int]:
+        r, w = C.c_int(), C.c_int()
+        self.run("semd_comm_info", C.byref(r), C.byref(w))
+        return r.value, w.value
+
+    def comm_allreduce(self, vals, op: str = "sum") -> np.ndarray:
+        a = np.array(vals, dtype=np.float64).ravel().copy()
+        self.run("semd_comm_allreduce_host", _dp(a), a.size, 0 if op == "sum" else 1)
+        return a
+
+    def comm_destroy(self) -> None:
+        self.run("semd_comm_destroy")
+
     def stats(self) -> dict:
         s = N.Stats()
-        self.check(self.lib.semd_get_stats(self.ptr, C.byref(s)))
+        self.run("semd_get_stats", C.byref(s))
         return {f: getattr(s, f) for f, _ in N.Stats._fields_}
 
     def set_timing(self, on: bool):
-        self.check(self.lib.semd_set_timing(self.ptr, int(on)))
+        self.run("semd_set_timing", int(on))
 
     def set_max_slots(self, g: int):
-        self.check(self.lib.semd_set_max_slots(self.ptr, int(g)))
+        self.run("semd_set_max_slots", int(g))
 
     def set_stream(self, stream_ptr: int | None):
-        self.check(self.lib.semd_set_stream(self.ptr, C.c_void_p(stream_ptr or 0)))
+        self.run("semd_set_stream", C.c_void_p(stream_ptr or 0))
 
     def mt19937_64(self, seed: int, n: int) -> np.ndarray:
         """TEST HOOK: raw device std::mt19937_64 draws."""
         out = np.zeros(max(n, 1), dtype=np.uint64)
-        self.check(self.lib.semd_mt19937_64_device_test(self.ptr, C.c_uint64(seed), n,
-                                                        out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        self.run("semd_mt19937_64_device_test", C.c_uint64(seed), n,
+                                                        out.ctypes.data_as(C.POINTER(C.c_uint64)))
         return out[:n]
 
     def set_noise_override(self, noise: np.ndarray | None):
         """TEST HOOK: use the given (nr, n) noise instead of the device RNG."""
         if noise is None:
-            self.check(self.lib.semd_set_noise_override(self.ptr, None, 0, 0))
+            self.run("semd_set_noise_override", None, 0, 0)
             return
         w = _f64(noise, 2)
-        self.check(self.lib.semd_set_noise_override(self.ptr, _dp(w), w.shape[0], w.shape[1]))
+        self.run("semd_set_noise_override", _dp(w), w.shape[0], w.shape[1])
 
 
 def context(device: int = 0) -> Context:
@@ -156,8 +194,8 @@ def find_extrema(x, device: int = 0):
     mi, ni = np.zeros(max(n, 1), np.uint64), np.zeros(max(n, 1), np.uint64)
     mv, nv = np.zeros(max(n, 1)), np.zeros(max(n, 1))
     a, b = C.c_size_t(), C.c_size_t()
-    c.check(c.lib.semd_find_extrema(c.ptr, _dp(x), n, mi.ctypes.data_as(N._szp), _dp(mv), C.byref(a),
-                                    ni.ctypes.data_as(N._szp), _dp(nv), C.byref(b)))
+    c.run("semd_find_extrema", _dp(x), n, mi.ctypes.data_as(N._szp), _dp(mv), C.byref(a),
+                                    ni.ctypes.data_as(N._szp), _dp(nv), C.byref(b))
     return (mi[:a.value].astype(np.int64), mv[:a.value], ni[:b.value].astype(np.int64), nv[:b.value])
 
 
@@ -169,7 +207,7 @@ def envelope(idx, val, length: int, device: int = 0) -> np.ndarray:
     if i.size != v.size:
         raise InvalidInput("envelope: index/value size mismatch")
     out = np.zeros(length)
-    c.check(c.lib.semd_envelope(c.ptr, i.ctypes.data_as(N._szp), _dp(v), i.size, length, _dp(out)))
+    c.run("semd_envelope", i.ctypes.data_as(N._szp), _dp(v), i.size, length, _dp(out))
     return out
 
 
@@ -180,7 +218,7 @@ def extract_imf(x, sd_threshold=0.2, max_sift_iters=300, max_imfs=0, device: int
     out = np.zeros(x.size)
     cnt = C.c_int32()
     cfg = N.SiftCfg(sd_threshold, max_sift_iters, max_imfs)
-    c.check(c.lib.semd_extract_imf(c.ptr, _dp(x), x.size, C.byref(cfg), _dp(out), C.byref(cnt)))
+    c.run("semd_extract_imf", _dp(x), x.size, C.byref(cfg), _dp(out), C.byref(cnt))
     return out, cnt.value
 
 
@@ -200,7 +238,7 @@ def decompose_full(x, algo="emd", sd_threshold=0.2, max_sift_iters=300, max_imfs
         kout = C.c_size_t()
         trace_buf = (N.TraceRec * trace_cap)() if trace_cap else None
         tr = N.Trace(C.cast(trace_buf, C.c_void_p) if trace_cap else None, trace_cap, 0)
-        rc = c.lib.semd_decompose(c.ptr, a, _dp(x), n, C.byref(cfg), C.byref(ens), _dp(imfs), k_cap, C.byref(kout),
+        rc = c.call("semd_decompose", a, _dp(x), n, C.byref(cfg), C.byref(ens), _dp(imfs), k_cap, C.byref(kout),
                                   _dp(res), counts.ctypes.data_as(N._i32p), C.byref(tr) if trace_cap else None)
         if rc == N.SEMD_CAPACITY and kout.value > k_cap:
             k_cap = int(kout.value)
@@ -242,7 +280,7 @@ def white_noise(n: int, seed: int, std: float = 1.0, device: int = 0) -> np.ndar
     """emd.cpp:181-200 (mt19937_64 + Box-Muller on the GPU)."""
     c = context(device)
     out = np.zeros(max(n, 1))
-    c.check(c.lib.semd_white_noise(c.ptr, n, C.c_uint64(seed), std, _dp(out)))
+    c.run("semd_white_noise", n, C.c_uint64(seed), std, _dp(out))
     return out[:n]
 
 
@@ -252,7 +290,7 @@ def noise_mode(w, i: int, sd_threshold=0.2, max_sift_iters=300, max_imfs=0, devi
     w = _f64(w, 1)
     out = np.zeros(w.size)
     cfg = N.SiftCfg(sd_threshold, max_sift_iters, max_imfs)
-    c.check(c.lib.semd_noise_mode(c.ptr, _dp(w), w.size, i, C.byref(cfg), _dp(out)))
+    c.run("semd_noise_mode", _dp(w), w.size, i, C.byref(cfg), _dp(out))
     return out
 
 
@@ -261,7 +299,7 @@ def signal_std(x, device: int = 0) -> float:
     c = context(device)
     x = _f64(x, 1)
     out = C.c_double()
-    c.check(c.lib.semd_signal_std(c.ptr, _dp(x), x.size, C.byref(out)))
+    c.run("semd_signal_std", _dp(x), x.size, C.byref(out))
     return out.value
 
 
@@ -270,7 +308,7 @@ def signal_std(x, device: int = 0) -> float:
 def transition_weights(d: int, device: int = 0) -> np.ndarray:
     c = context(device)
     out = np.zeros(max(d, 1))
-    c.check(c.lib.semd_transition_weights(c.ptr, d, _dp(out)))
+    c.run("semd_transition_weights", d, _dp(out))
     return out[:d]
 
 
@@ -290,8 +328,7 @@ def concatenate(x, d: int, naive: bool = False, device: int = 0) -> np.ndarray:
     cm, M, Nc = _channel_major(x)
     L = M * Nc + d * (Nc - 1) if M and Nc else 0
     out = np.zeros(max(L, 1))
-    fn = c.lib.semd_concatenate_naive if naive else c.lib.semd_concatenate
-    c.check(fn(c.ptr, _dp(cm), M, Nc, d, _dp(out)))
+    c.run("semd_concatenate_naive" if naive else "semd_concatenate", _dp(cm), M, Nc, d, _dp(out))
     return out[:L]
 
 
@@ -306,7 +343,7 @@ def deconcatenate(modes, rows: int, channels: int, d: int, device: int = 0) -> n
     L, K = m.shape
     km = np.ascontiguousarray(m.T)
     out = np.zeros(max(K * rows * channels, 1))
-    c.check(c.lib.semd_deconcatenate(c.ptr, _dp(km), K, L, rows, channels, d, _dp(out)))
+    c.run("semd_deconcatenate", _dp(km), K, L, rows, channels, d, _dp(out))
     return out[:K * rows * channels].reshape(K, channels, rows).transpose(2, 1, 0).copy()
 
 
@@ -322,7 +359,7 @@ def serial_decompose_full(x, d: int, algo="emd", sd_threshold=0.2, max_sift_iter
         mo = C.c_size_t()
         trace_buf = (N.TraceRec * trace_cap)() if trace_cap else None
         tr = N.Trace(C.cast(trace_buf, C.c_void_p) if trace_cap else None, trace_cap, 0)
-        rc = c.lib.semd_serial_decompose(c.ptr, a, _dp(cm), M, Nc, d, C.byref(cfg), C.byref(ens), _dp(t), k_cap,
+        rc = c.call("semd_serial_decompose", a, _dp(cm), M, Nc, d, C.byref(cfg), C.byref(ens), _dp(t), k_cap,
                                          C.byref(mo), C.byref(tr) if trace_cap else None)
         if rc == N.SEMD_CAPACITY and mo.value > k_cap:
             k_cap = int(mo.value)
@@ -355,7 +392,7 @@ def slicewise_decompose(x, algo="emd", sd_threshold=0.2, max_sift_iters=300, max
     while True:
         t = np.zeros(max(k_cap * M * Nc, 1))
         mo = C.c_size_t()
-        rc = c.lib.semd_slicewise_decompose(c.ptr, a, _dp(cm), M, Nc, C.byref(cfg), C.byref(ens), _dp(t), k_cap,
+        rc = c.call("semd_slicewise_decompose", a, _dp(cm), M, Nc, C.byref(cfg), C.byref(ens), _dp(t), k_cap,
                                             C.byref(mo))
         if rc == N.SEMD_CAPACITY and mo.value > k_cap:
             k_cap = int(mo.value)

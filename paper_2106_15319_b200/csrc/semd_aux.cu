@@ -10,6 +10,7 @@
 
 #include "semd_device.cuh"
 #include "semd_launch.h"
+#include "semd_libm.cuh"
 #include "semd_types.cuh"
 
 namespace semd {
@@ -102,19 +103,28 @@ __global__ void __launch_bounds__(320) k_mt19937_64_ens(uint64_t base, long long
 }
 
 // In place: draws (u64 pairs) -> Gaussian samples (f64), emd.cpp:189-198.
-__global__ void k_box_muller(uint64_t* draws, long long n, double stdv) {
+// white_noise's Box-Muller (emd.cpp:189-198) with glibc's own log and sincos restated
+// (semd_libm.cuh), so every noise sample equals the reference's bit-for-bit. The two glibc
+// tables (2 KB log, 3.5 KB sin/cos) are served from shared memory.
+__global__ void __launch_bounds__(256) k_box_muller(uint64_t* draws, long long n, double stdv) {
+    __shared__ double logtab[256];
+    __shared__ double sctab[440];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) logtab[i] = libm::kLogTab[i];
+    for (int i = threadIdx.x; i < 440; i += blockDim.x) sctab[i] = libm::kSinCosTab[i];
+    __syncthreads();
     const long long pairs = (n + 1) / 2;
     const double two_pi = 6.283185307179586476925286766559;
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < pairs;
          p += (long long)gridDim.x * blockDim.x) {
         const uint64_t d1 = draws[2 * p], d2 = draws[2 * p + 1];
         const double u1 = (double)((d1 >> 11) + 1) * 0x1.0p-53;
-        const double r = stdv * sqrt(-2.0 * log(u1));
+        const double r = stdv * __dsqrt_rn(-2.0 * libm::log(u1, logtab));
         const double u2 = (double)((d2 >> 11) + 1) * 0x1.0p-53;
-        const double theta = two_pi * u2;
+        double sn, cs;
+        libm::sincos(two_pi * u2, sctab, &sn, &cs);
         double* out = reinterpret_cast<double*>(draws);
-        out[2 * p] = r * cos(theta);
-        if (2 * p + 1 < n) out[2 * p + 1] = r * sin(theta);
+        out[2 * p] = r * cs;
+        if (2 * p + 1 < n) out[2 * p + 1] = r * sn;
     }
 }
 

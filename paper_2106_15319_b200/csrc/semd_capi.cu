@@ -7,6 +7,8 @@
 // the epilogues of k_eval / k_final; the host only polls a mapped pinned word
 // a few steps behind to learn when every slot is done.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -67,6 +69,64 @@ uint64_t derive_seed(uint64_t base, uint64_t index) {  // emd.cpp:174-179
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
     return z ^ (z >> 31);
+}
+
+// ---- NCCL, loaded on first use (single-GPU contexts never touch it) ----------------------
+// The library is resolved by soname, so a process that already loaded one (e.g. torch's
+// bundled copy) shares it. SEMD_NCCL_LIB overrides the path.
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                           cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = nullptr;
+        const char* names[] = {std::getenv("SEMD_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+        for (const char* nm : names)
+            if (nm && (h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL)) != nullptr) break;
+        if (!h) {
+            const char* e = dlerror();
+            a.err = e ? e : "libnccl.so.2 not found";
+            return a;
+        }
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+        a.Reduce = reinterpret_cast<decltype(a.Reduce)>(dlsym(h, "ncclReduce"));
+        a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.Reduce && a.GetErrorString;
+        if (!a.ok) a.err = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+
+const NcclApi& nccl() {
+    const NcclApi& a = nccl_api();
+    if (!a.ok) raise(SEMD_CUDA_ERROR, "NCCL unavailable: %s", a.err.c_str());
+    return a;
+}
+
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) raise(SEMD_CUDA_ERROR, "%s: %s", what, nccl_api().GetErrorString(r));
+}
+
+// Contiguous realization shard of rank r of W (the same split as paper_2106_15319_b200/parallel.py).
+void shard_range(int nr, int rank, int world, int* mb, int* me) {
+    const int per = (nr + world - 1) / world;
+    *mb = std::min(nr, rank * per);
+    *me = std::min(nr, *mb + per);
 }
 
 // Device allocation helper that frees on scope exit.
@@ -135,8 +195,16 @@ struct semd_ctx {
     cudaEvent_t noise_ready[2]{};
     cudaEvent_t res_ready{};  // CEEMDAN: the stage residue is final (its std runs on the side stream)
     cudaEvent_t t0 = nullptr, t1 = nullptr;
+    cudaEvent_t tm0 = nullptr, tm1 = nullptr;  // semd_timer_start / semd_timer_stop
+    // multi-GPU: an NCCL communicator over one context per rank (semd_comm_init)
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1, root = -1;  // root < 0: every rank receives the ensemble result
+    DBuf comm_buf, comm_red;
 
     ~semd_ctx() {
+        if (comm) nccl_api().CommDestroy(comm);
+        if (tm0) cudaEventDestroy(tm0);
+        if (tm1) cudaEventDestroy(tm1);
         if (status_host) cudaFreeHost(status_host);
         if (pin_jobs) cudaFreeHost(pin_jobs);
         for (auto& e : ev)
@@ -480,6 +548,49 @@ struct semd_ctx {
         else semd::dev::launch_fill(A.sums, n, value, stream);
     }
 
+    // ---- multi-GPU collectives (NCCL on the engine stream: stream-ordered with the kernels) ----
+    long long comm_max(long long v) {
+        if (!comm) return v;
+        comm_buf.alloc(64);
+        long long* d = comm_buf.as<long long>();
+        ck(cudaMemcpyAsync(d, &v, 8, cudaMemcpyHostToDevice, stream), "comm max");
+        nck(nccl().AllReduce(d, d, 1, ncclInt64, ncclMax, comm, stream), "ncclAllReduce(max)");
+        ck(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, stream), "comm max");
+        ck(cudaStreamSynchronize(stream), "comm max");
+        return v;
+    }
+    // in-place sum over ranks: to the root only when root >= 0 and root_only, else to every rank
+    void comm_sum(double* d, size_t count, bool root_only) {
+        if (!comm || count == 0) return;
+        if (root_only && root >= 0)
+            nck(nccl().Reduce(d, d, count, ncclDouble, ncclSum, root, comm, stream), "ncclReduce(sum)");
+        else
+            nck(nccl().AllReduce(d, d, count, ncclDouble, ncclSum, comm, stream), "ncclAllReduce(sum)");
+    }
+    bool has_result() const { return !comm || root < 0 || rank == root; }
+
+    // more IMF rows for the configured engine, keeping rows [0, kcap) (CEEMDAN stages past the
+    // initial estimate; the reference's IMF list is unbounded when max_imfs == 0)
+    void grow_sums(int newk) {
+        if (newk <= A.kcap) return;
+        const size_t n = (size_t)A.L, old = (size_t)A.kcap;
+        DBuf t((size_t)newk * n * 8);
+        ck(cudaMemsetAsync(t.p, 0, t.bytes, stream), "grow sums");
+        ck(cudaMemcpyAsync(t.p, sums.p, old * n * 8, cudaMemcpyDeviceToDevice, stream), "grow sums");
+        DBuf c((size_t)newk * 4);
+        ck(cudaMemsetAsync(c.p, 0, c.bytes, stream), "grow counts");
+        ck(cudaMemcpyAsync(c.p, imf_sifts.p, old * 4, cudaMemcpyDeviceToDevice, stream), "grow counts");
+        ck(cudaStreamSynchronize(stream), "grow sums");
+        std::swap(sums.p, t.p);
+        std::swap(sums.bytes, t.bytes);
+        std::swap(imf_sifts.p, c.p);
+        std::swap(imf_sifts.bytes, c.bytes);
+        A.sums = sums.as<double>();
+        A.imf_sifts = imf_sifts.as<int>();
+        A.kcap = newk;
+        cfg_kcap = newk;
+    }
+
     // ---- drivers ---------------------------------------------------------------
     // emd.cpp:155-172 on a device signal; returns K. IMFs in sums rows, residue in buffer.
     int emd_device(const double* d_x, long long n, const semd_sift_cfg& cfg, semd_trace* tr, int m = 0) {
@@ -749,7 +860,10 @@ struct semd_ctx {
     // the shard's unscaled first-mode sum of stage K into sums row K
     void ceemdan_stage() {
         if (!cs.active) raise(SEMD_INVALID_INPUT, "ceemdan: no active shard (call begin)");
-        if (cs.K >= cs.kcap) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", cs.kcap);
+        if (cs.K >= cs.kcap) {
+            grow_sums(2 * cs.kcap);
+            cs.kcap = A.kcap;
+        }
         const int cnt = cs.m1 - cs.m0;
         const long long n = cs.n;
         if (cs.K == 0) {  // mode 1 (emd.cpp:292-307): first modes of x + beta0 w^(m)
@@ -843,16 +957,24 @@ struct semd_ctx {
         return true;
     }
 
-    // emd.cpp:264-344 on one GPU. Returns K; IMFs in `out_imfs` (device, k_cap rows), residue in out_res.
+    // emd.cpp:264-344. Returns K; IMFs in `out_imfs` (device, k_cap rows), residue in out_res.
+    // With a communicator the realizations are sharded over the ranks and every stage's first-mode
+    // sum is all-reduced (NCCL, in place on the engine stream) before the identical finish on each
+    // rank (emd.cpp:301-306, :331-339): residues, beta_i and the stop decisions agree everywhere.
     int ceemdan_device(const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens,
                        double* out_imfs, int k_cap, double* out_res, semd_trace* tr, int* k_needed) {
-        ceemdan_begin(d_x, n, cfg, ens, 0, ens.nr, tr);
-        ceemdan_stage();
+        int mb = 0, me = ens.nr;
+        if (comm) shard_range(ens.nr, rank, world, &mb, &me);
+        ceemdan_begin(d_x, n, cfg, ens, mb, me, tr);
+        auto stage_total = [&] {
+            ceemdan_stage();
+            comm_sum(A.sums + (size_t)cs.K * n, (size_t)n, false);
+        };
+        stage_total();
         ceemdan_finish(nullptr, ens.nr, false, nullptr);
         while (cfg.max_imfs == 0 || cs.K < cfg.max_imfs) {  // emd.cpp:310
-            if (cs.K >= cs.kcap) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", cs.kcap);
-            if (ceemdan_residue_extrema() < 3) break;
-            ceemdan_stage();
+            if (ceemdan_residue_extrema() < 3) break;        // emd.cpp:311
+            stage_total();                                   // grows the IMF rows when needed
             if (!ceemdan_finish(nullptr, ens.nr, true, nullptr)) break;
         }
         const int K = cs.K;
@@ -1018,14 +1140,44 @@ struct semd_ctx {
         }
         if (algo == SEMD_ALGO_EEMD) {
             if (n < 4) raise(SEMD_INVALID_INPUT, "emd: signal too short (need at least 4 samples)");
-            const int K = eemd_partial_device(d_x, n, cfg, ens, 0, ens.nr, tr);
+            // realization shard of this rank (all of [0, nr) without a communicator)
+            int mb = 0, me = ens.nr;
+            if (comm) shard_range(ens.nr, rank, world, &mb, &me);
+            int K = 0;
+            if (me > mb) {
+                K = eemd_partial_device(d_x, n, cfg, ens, mb, me, tr);
+            } else {  // more ranks than realizations: this rank contributes zeros
+                configure(n, 1, default_kcap(n, cfg.max_imfs), tr ? trace_cap_for(tr) : 0);
+                fill_sums(A.kcap, 0.0);
+                h_trace.clear();
+                trace_total = 0;
+            }
+            double* sums_d = A.sums;
+            if (comm) {  // emd.cpp:246-251 across ranks: K = max K_m, then the ensemble sum
+                const int k_local = K;
+                K = (int)comm_max(K);
+                if (K > A.kcap) {  // another rank needed more IMF rows than this one holds
+                    comm_red.alloc((size_t)K * n * 8);
+                    ck(cudaMemsetAsync(comm_red.p, 0, (size_t)K * n * 8, stream), "reduce rows");
+                    if (k_local)
+                        ck(cudaMemcpyAsync(comm_red.p, A.sums, (size_t)k_local * n * 8, cudaMemcpyDeviceToDevice,
+                                           stream),
+                           "reduce rows");
+                    sums_d = comm_red.as<double>();
+                }
+                comm_sum(sums_d, (size_t)K * n, true);
+            }
             *k_out = (size_t)K;
             export_trace(tr);
+            if (!has_result()) {  // root-only reduction: the ensemble lives on the root rank
+                ck(cudaStreamSynchronize(stream), "eemd");
+                return;
+            }
             if ((size_t)K > k_cap) raise(SEMD_CAPACITY, "output holds %zu IMFs, decomposition has %d", k_cap, K);
-            semd::dev::launch_ensemble_finish(A.sums, K, n, d_x, d_res ? d_res : buf(0, 1), 1.0 / (double)ens.nr,
+            semd::dev::launch_ensemble_finish(sums_d, K, n, d_x, d_res ? d_res : buf(0, 1), 1.0 / (double)ens.nr,
                                               stream);
             if (K && d_imfs)
-                ck(cudaMemcpyAsync(d_imfs, A.sums, (size_t)K * n * 8, cudaMemcpyDeviceToDevice, stream), "imfs");
+                ck(cudaMemcpyAsync(d_imfs, sums_d, (size_t)K * n * 8, cudaMemcpyDeviceToDevice, stream), "imfs");
             if (sift_counts_host)
                 for (int k = 0; k < K; ++k) sift_counts_host[k] = 0;
             ck(cudaStreamSynchronize(stream), "eemd");
@@ -1435,6 +1587,7 @@ int semd_decompose(semd_ctx* ctx, int algo, const double* x, size_t n, const sem
         }
         if (k_out) *k_out = K;
         if (rc) raise(rc, "%s", msg.c_str());
+        if (!ctx->has_result()) return;  // root-only ensemble reduction on another rank
         if (imfs && K) ctx->download(imfs, d_imfs, K * n);
         if (residue) ctx->download(residue, d_res, n);
     });
@@ -1459,6 +1612,12 @@ int semd_decompose_device(semd_ctx* ctx, int algo, const double* d_x, size_t n, 
 int semd_eemd_partial_device(semd_ctx* ctx, const double* d_x, size_t n, const semd_sift_cfg* cfg_,
                              const semd_ens_cfg* ens_, int32_t m_begin, int32_t m_end, double* d_sums, size_t k_cap,
                              size_t* k_out) {
+    return semd_eemd_partial_traced_device(ctx, d_x, n, cfg_, ens_, m_begin, m_end, d_sums, k_cap, k_out, nullptr);
+}
+
+int semd_eemd_partial_traced_device(semd_ctx* ctx, const double* d_x, size_t n, const semd_sift_cfg* cfg_,
+                                    const semd_ens_cfg* ens_, int32_t m_begin, int32_t m_end, double* d_sums,
+                                    size_t k_cap, size_t* k_out, semd_trace* trace) {
     return guard([&] {
         need_ctx(ctx);
         const semd_sift_cfg cfg = sift_or_default(cfg_);
@@ -1466,8 +1625,14 @@ int semd_eemd_partial_device(semd_ctx* ctx, const double* d_x, size_t n, const s
         if (ens.nr < 1) raise(SEMD_INVALID_INPUT, "ensemble: nr must be at least 1");
         if (ens.nstd < 0.0) raise(SEMD_INVALID_INPUT, "ensemble: nstd must be non-negative");
         if (m_begin < 0 || m_end < m_begin) raise(SEMD_INVALID_INPUT, "invalid realization range");
+        // emd.cpp:230: a zero-noise ensemble is plain EMD, which ensemble sums cannot reproduce
+        // bit-for-bit (sum of nr copies x 1/nr); the caller runs semd_decompose(SEMD_ALGO_EMD).
+        if (ens.nstd == 0.0) raise(SEMD_INVALID_INPUT, "eemd shard: nstd == 0 is plain EMD (use semd_decompose)");
         ctx->reset_stats(1);
-        const int K = m_end > m_begin ? ctx->eemd_partial_device(d_x, (long long)n, cfg, ens, m_begin, m_end, nullptr) : 0;
+        const int K =
+            m_end > m_begin ? ctx->eemd_partial_device(d_x, (long long)n, cfg, ens, m_begin, m_end, trace) : 0;
+        if (m_end > m_begin) ctx->export_trace(trace);
+        else if (trace) trace->count = 0;
         if (k_out) *k_out = (size_t)K;
         if ((size_t)K > k_cap) raise(SEMD_CAPACITY, "output holds %zu IMFs, shard has %d", k_cap, K);
         if (k_cap) ck(cudaMemsetAsync(d_sums, 0, k_cap * n * 8, ctx->stream), "zero sums");
@@ -1602,16 +1767,20 @@ static void serial_device(semd_ctx* ctx, int algo, const double* d_x, size_t M, 
     size_t kc = std::max<size_t>(k_cap, 1);
     DBuf modes;
     size_t K = 0;
-    for (int attempt = 0; attempt < 4; ++attempt) {
+    for (int attempt = 0;; ++attempt) {
         modes.alloc((kc + 1) * L * 8);
         try {
             ctx->decompose_device(algo, sig.as<double>(), (long long)L, sift_or_default(cfg), ens_or_default(ens),
                                   modes.as<double>(), kc, &K, modes.as<double>() + kc * L, nullptr, trace);
             break;
         } catch (const Error& e) {
-            if (e.code != SEMD_CAPACITY) throw;
+            if (e.code != SEMD_CAPACITY || attempt == 3 || K <= kc) throw;  // only an output-capacity miss retries
             kc = std::max(kc * 2, K);
         }
+    }
+    if (!ctx->has_result()) {  // root-only ensemble reduction: the tensor is produced on the root rank
+        *modes_out = K + 1;
+        return;
     }
     if (K != kc)  // move the residue right after the K IMFs
         ck(cudaMemcpyAsync(modes.as<double>() + K * L, modes.as<double>() + kc * L, L * 8, cudaMemcpyDeviceToDevice,
@@ -1642,7 +1811,7 @@ int semd_serial_decompose(semd_ctx* ctx, int algo, const double* x, size_t M, si
             throw;
         }
         if (modes_out) *modes_out = mo;
-        ctx->download(tensor, t.as<double>(), mo * M * N);
+        if (ctx->has_result()) ctx->download(tensor, t.as<double>(), mo * M * N);
     });
 }
 
@@ -1702,6 +1871,149 @@ int semd_slicewise_decompose_device(semd_ctx* ctx, int algo, const double* d_x, 
             throw;
         }
         if (modes_out) *modes_out = mo;
+    });
+}
+
+// ---- device memory and timing on the context stream (bench / driver plumbing) -----------------
+int semd_device_alloc(semd_ctx* ctx, size_t bytes, void** d_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!d_out) raise(SEMD_INVALID_INPUT, "null output pointer");
+        *d_out = nullptr;
+        const cudaError_t e = cudaMalloc(d_out, std::max<size_t>(bytes, 8));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            raise(SEMD_NO_MEMORY, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+        }
+    });
+}
+
+int semd_device_free(semd_ctx* ctx, void* d) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (d) ck(cudaFree(d), "cudaFree");
+    });
+}
+
+int semd_memcpy(semd_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (bytes) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream), "memcpy");
+        ck(cudaStreamSynchronize(ctx->stream), "memcpy");
+    });
+}
+
+int semd_host_alloc(semd_ctx* ctx, size_t bytes, void** h_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!h_out) raise(SEMD_INVALID_INPUT, "null output pointer");
+        ck(cudaHostAlloc(h_out, std::max<size_t>(bytes, 8), cudaHostAllocDefault), "cudaHostAlloc");
+    });
+}
+
+int semd_host_free(semd_ctx* ctx, void* h) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (h) ck(cudaFreeHost(h), "cudaFreeHost");
+    });
+}
+
+int semd_timer_start(semd_ctx* ctx) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!ctx->tm0) ck(cudaEventCreate(&ctx->tm0), "event");
+        if (!ctx->tm1) ck(cudaEventCreate(&ctx->tm1), "event");
+        ck(cudaStreamSynchronize(ctx->stream), "timer");
+        ck(cudaEventRecord(ctx->tm0, ctx->stream), "timer");
+    });
+}
+
+int semd_timer_stop(semd_ctx* ctx, double* ms) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!ctx->tm0 || !ctx->tm1) raise(SEMD_INVALID_INPUT, "semd_timer_stop without semd_timer_start");
+        ck(cudaEventRecord(ctx->tm1, ctx->stream), "timer");
+        ck(cudaEventSynchronize(ctx->tm1), "timer");
+        float f = 0.f;
+        ck(cudaEventElapsedTime(&f, ctx->tm0, ctx->tm1), "timer");
+        if (ms) *ms = (double)f;
+    });
+}
+
+// ---- multi-GPU: one context per rank joined by an NCCL communicator ---------------------------
+int semd_comm_unique_id(void* id_out, size_t bytes) {
+    return guard([&] {
+        if (!id_out || bytes < sizeof(ncclUniqueId)) raise(SEMD_INVALID_INPUT, "unique id buffer needs %zu bytes",
+                                                           sizeof(ncclUniqueId));
+        ncclUniqueId id;
+        nck(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(id_out, &id, sizeof id);
+    });
+}
+
+int semd_comm_init(semd_ctx* ctx, const void* id, size_t bytes, int rank, int world) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!id || bytes < sizeof(ncclUniqueId)) raise(SEMD_INVALID_INPUT, "unique id needs %zu bytes",
+                                                       sizeof(ncclUniqueId));
+        if (world < 1 || rank < 0 || rank >= world) raise(SEMD_INVALID_INPUT, "rank %d out of range (world %d)", rank,
+                                                          world);
+        if (ctx->comm) {
+            nccl_api().CommDestroy(ctx->comm);
+            ctx->comm = nullptr;
+        }
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof uid);
+        ncclComm_t c = nullptr;
+        nck(nccl().CommInitRank(&c, world, uid, rank), "ncclCommInitRank");
+        ctx->comm = c;
+        ctx->rank = rank;
+        ctx->world = world;
+        ctx->root = -1;
+    });
+}
+
+int semd_comm_set_root(semd_ctx* ctx, int root) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (root >= ctx->world) raise(SEMD_INVALID_INPUT, "root %d out of range (world %d)", root, ctx->world);
+        ctx->root = root < 0 ? -1 : root;
+    });
+}
+
+int semd_comm_info(semd_ctx* ctx, int* rank, int* world) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (rank) *rank = ctx->comm ? ctx->rank : 0;
+        if (world) *world = ctx->comm ? ctx->world : 1;
+    });
+}
+
+int semd_comm_allreduce_host(semd_ctx* ctx, double* vals, size_t n, int op) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (!ctx->comm || n == 0) return;
+        if (op != 0 && op != 1) raise(SEMD_INVALID_INPUT, "op must be 0 (sum) or 1 (max)");
+        ctx->comm_buf.alloc(std::max<size_t>(64, n * 8));
+        double* d = ctx->comm_buf.as<double>();
+        ck(cudaMemcpyAsync(d, vals, n * 8, cudaMemcpyHostToDevice, ctx->stream), "allreduce");
+        nck(nccl().AllReduce(d, d, n, ncclDouble, op ? ncclMax : ncclSum, ctx->comm, ctx->stream), "ncclAllReduce");
+        ck(cudaMemcpyAsync(vals, d, n * 8, cudaMemcpyDeviceToHost, ctx->stream), "allreduce");
+        ck(cudaStreamSynchronize(ctx->stream), "allreduce");
+    });
+}
+
+int semd_comm_destroy(semd_ctx* ctx) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (ctx->comm) {
+            ck(cudaStreamSynchronize(ctx->stream), "comm");
+            nck(nccl_api().CommDestroy(ctx->comm), "ncclCommDestroy");
+        }
+        ctx->comm = nullptr;
+        ctx->rank = 0;
+        ctx->world = 1;
+        ctx->root = -1;
     });
 }
 

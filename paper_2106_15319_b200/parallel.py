@@ -9,9 +9,15 @@ EEMD realizations are independent units: rank r of W owns the contiguous
 range shard_range(nr, r, W) and runs them on its own GPU (seeds derive from
 the GLOBAL realization index, emd.cpp:238, so the work of realization m is
 identical on any rank). The only exchange is the ensemble mean: an
-all-reduce(max) of the IMF count and one all-reduce(sum) of the K x L partial
-sums (NCCL over NVLink on GPUs; gloo in the CPU tests), followed by the same
-finish on every rank (emd.cpp:252-260). No collective inside the sift loop.
+all-reduce(max) of the IMF count and one reduce/all-reduce(sum) of the K x L
+partial sums, followed by the finish (emd.cpp:252-260). No collective inside
+the sift loop.
+
+sharded_ensemble / sharded_ceemdan below are the host logic, written against
+abstract collectives so the CPU tests can drive them with gloo (world size 2)
+and the oracle. The GPU product runs the same logic inside the C engine
+(semd_capi.cu, semd_comm_* in include/semd_b200.h) with NCCL on the engine
+stream; init_comm joins a context to its communicator.
 """
 from __future__ import annotations
 
@@ -58,138 +64,56 @@ def sharded_ceemdan(nr: int, rank: int, world: int, engine, allreduce_sum: Calla
     return engine.result()
 
 
-# ------------------------------------------------------------- torch / GPU driver
+# ------------------------------------------------------------- GPU: NCCL inside the C ABI
+#
+# On GPUs the drivers above run inside the engine (semd_capi.cu decompose_device /
+# ceemdan_device) once a context is joined to an NCCL communicator: the collectives are
+# enqueued on the engine's own stream, so they are ordered with the kernels that produce and
+# consume the sums. Python only ships the 128-byte NCCL unique id from rank 0 to the others.
 
-def eemd_distributed(x_dev, n: int, cfg: dict, ens: dict, rank: int, world: int, ctx=None, k_cap: int = 64,
-                     group=None):
-    """EEMD on this rank's GPU shard + NCCL all-reduce; returns (imfs (K, n), residue) torch tensors.
-
-    x_dev: torch.float64 CUDA tensor of the serialized signal (resident in HBM).
-    """
-    import ctypes as C
-
-    import torch
-    import torch.distributed as dist
-
-    from . import _native as N
-    from .api import context
-
-    c = ctx or context(x_dev.device.index or 0)
-    scfg = N.SiftCfg(cfg.get("sd_threshold", 0.2), cfg.get("max_sift_iters", 300), cfg.get("max_imfs", 0))
-    ecfg = N.EnsCfg(ens.get("nstd", 0.2), ens.get("nr", 100), 0, ens.get("base_seed", 0))
-    nr = ecfg.nr
-    state = {}
-
-    def partial(mb, me):
-        sums = torch.zeros((k_cap, n), dtype=torch.float64, device=x_dev.device)
-        kout = C.c_size_t()
-        c.check(c.lib.semd_eemd_partial_device(c.ptr, C.c_void_p(x_dev.data_ptr()), n, C.byref(scfg), C.byref(ecfg),
-                                               mb, me, C.c_void_p(sums.data_ptr()), k_cap, C.byref(kout)))
-        state["stats"] = c.stats()
-        return sums, int(kout.value)
-
-    def amax(k):
-        if world == 1:
-            return k
-        t = torch.tensor([k], dtype=torch.int64, device=x_dev.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        return int(t.item())
-
-    def asum(sums, K):
-        s = sums[:K].contiguous()
-        if world > 1 and K:
-            dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
-        return s
-
-    def finish(total, K):
-        residue = torch.empty(n, dtype=torch.float64, device=x_dev.device)
-        c.check(c.lib.semd_ensemble_finish_device(c.ptr, C.c_void_p(x_dev.data_ptr()), n,
-                                                  C.c_void_p(total.data_ptr()), K, nr, C.c_void_p(residue.data_ptr())))
-        return total, residue
-
-    imfs, residue = sharded_ensemble(nr, rank, world, partial, amax, asum, finish)
-    return imfs, residue, state.get("stats", {})
+def _rdzv_path() -> str:
+    import os
+    d = os.environ.get("SEMD_RDZV_DIR", "/tmp")
+    # the launcher's ranks share a parent process (torchrun's agent): its pid keeps launches apart
+    tag = os.environ.get("SEMD_RDZV_TAG") or f"{os.environ.get('TORCHELASTIC_RUN_ID', 'semd')}.{os.getppid()}"
+    return os.path.join(d, f"semd_nccl_id.{tag}.{os.environ.get('MASTER_PORT', '0')}")
 
 
-class GpuCeemdanShard:
-    """sharded_ceemdan engine over the C ABI (semd_ceemdan_shard_*) on one GPU."""
-
-    def __init__(self, ctx, x_dev, n: int, cfg: dict, ens: dict):
-        import ctypes as C
-
-        from . import _native as N
-        self.C, self.c, self.x, self.n = C, ctx, x_dev, n
-        self.scfg = N.SiftCfg(cfg.get("sd_threshold", 0.2), cfg.get("max_sift_iters", 300), cfg.get("max_imfs", 0))
-        self.ecfg = N.EnsCfg(ens.get("nstd", 0.2), ens.get("nr", 100), 0, ens.get("base_seed", 0))
-        self.modes = []
-
-    def begin(self, mb, me):
-        C, c = self.C, self.c
-        c.check(c.lib.semd_ceemdan_shard_begin(c.ptr, C.c_void_p(self.x.data_ptr()), self.n, C.byref(self.scfg),
-                                               C.byref(self.ecfg), mb, me))
-
-    def stage(self):
-        import torch
-        part = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
-        self.c.check(self.c.lib.semd_ceemdan_shard_stage(self.c.ptr, self.C.c_void_p(part.data_ptr())))
-        return part
-
-    def finish(self, total, check_zero):
-        import torch
-        C, c = self.C, self.c
-        mode = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
-        ok = C.c_int32()
-        c.check(c.lib.semd_ceemdan_shard_finish_stage(c.ptr, C.c_void_p(total.data_ptr()), self.ecfg.nr,
-                                                      int(check_zero), C.c_void_p(mode.data_ptr()), C.byref(ok)))
-        if ok.value:
-            self.modes.append(mode)
-        return bool(ok.value)
-
-    def residue_extrema(self):
-        t = self.C.c_size_t()
-        self.c.check(self.c.lib.semd_ceemdan_shard_residue_extrema(self.c.ptr, self.C.byref(t)))
-        return int(t.value)
-
-    def result(self):
-        import torch
-        res = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
-        self.c.check(self.c.lib.semd_ceemdan_shard_residue(self.c.ptr, self.C.c_void_p(res.data_ptr())))
-        imfs = torch.stack(self.modes) if self.modes else torch.empty((0, self.n), dtype=torch.float64,
-                                                                        device=self.x.device)
-        return imfs, res
-
-
-def ceemdan_distributed(x_dev, n: int, cfg: dict, ens: dict, rank: int, world: int, ctx=None, group=None):
-    """CEEMDAN with realizations sharded over the ranks' GPUs and one NCCL all-reduce per stage;
-    returns (imfs (K, n), residue) torch tensors (identical on every rank)."""
-    import torch.distributed as dist
-
-    from .api import context
-    c = ctx or context(x_dev.device.index or 0)
-    if float(ens.get("nstd", 0.2)) == 0.0:  # degenerate ensemble is plain EMD (emd.cpp:267), same on every rank
-        import ctypes as C
-
-        import torch
-
-        from . import _native as N
-        k_cap = 64
-        imfs = torch.empty((k_cap, n), dtype=torch.float64, device=x_dev.device)
-        res = torch.empty(n, dtype=torch.float64, device=x_dev.device)
-        k = C.c_size_t()
-        c.check(c.lib.semd_decompose_device(c.ptr, 0, C.c_void_p(x_dev.data_ptr()), n,
-                                            C.byref(N.SiftCfg(cfg.get("sd_threshold", 0.2),
-                                                              cfg.get("max_sift_iters", 300), cfg.get("max_imfs", 0))),
-                                            None, C.c_void_p(imfs.data_ptr()), k_cap, C.byref(k),
-                                            C.c_void_p(res.data_ptr())))
-        return imfs[:k.value], res
-    eng = GpuCeemdanShard(c, x_dev, n, cfg, ens)
-
-    def asum(part):
-        if world > 1:
-            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
-        return part
-
-    return sharded_ceemdan(int(ens.get("nr", 100)), rank, world, eng, asum, int(cfg.get("max_imfs", 0)))
+def init_comm(ctx, rank: int, world: int, root: int = -1, timeout: float = 300.0) -> None:
+    """Join this rank's context to an NCCL communicator of `world` ranks (one process per GPU,
+    one node). Rank 0 makes the unique id and publishes it through a file named after the
+    launcher (run id, agent pid, master port); the others read it. No-op for world == 1."""
+    import os
+    import time
+    if world <= 1:
+        return
+    path = _rdzv_path()
+    if rank == 0:
+        uid = ctx.comm_unique_id()
+        tmp = f"{path}.{os.getpid()}.tmp"
+        with open(tmp, "wb") as f:
+            f.write(uid)
+        os.replace(tmp, path)
+    else:
+        t0 = time.time()
+        while True:
+            try:
+                with open(path, "rb") as f:
+                    uid = f.read()
+                if len(uid) == 128:
+                    break
+            except FileNotFoundError:
+                pass
+            if time.time() - t0 > timeout:
+                raise TimeoutError(f"no NCCL unique id at {path}")
+            time.sleep(0.02)
+    ctx.comm_init(uid, rank, world, root)
+    ctx.comm_allreduce([0.0])  # every rank has read the id
+    if rank == 0:
+        try:
+            os.remove(path)
+        except OSError:
+            pass
 
 
 # ------------------------------------------------------------- numpy reference driver (tests)

@@ -122,6 +122,18 @@ int main() {
         CHECK(throws_with<InvalidInput>([] { slicewise_decompose(MultiSignal(), Algorithm::Emd); },
                                         "slicewise_decompose: empty input"));
     }
+    {  // multi-GPU API on a 1-rank NCCL communicator: bit-identical to the single-GPU engine
+        Signal x(900);
+        for (std::size_t i = 0; i < x.size(); ++i) x[i] = std::sin(0.21 * i) + 0.4 * std::cos(0.047 * i);
+        const Decomposition e1 = eemd(x, {}, {0.2, 7, 3});
+        const Decomposition c1 = ceemdan(x, {}, {0.2, 5, 2});
+        comm_init(comm_unique_id(), 0, 1);
+        const Decomposition e2 = eemd(x, {}, {0.2, 7, 3});
+        const Decomposition c2 = ceemdan(x, {}, {0.2, 5, 2});
+        CHECK(e1.imfs == e2.imfs && e1.residue == e2.residue);
+        CHECK(c1.imfs == c2.imfs && c1.residue == c2.residue);
+        comm_destroy();
+    }
     std::printf("%s %d/%d\n", fails ? "FAILED" : "OK", checks - fails, checks);
     return fails ? 1 : 0;
 }
