@@ -460,7 +460,7 @@ def test_cpp_mirror_runs(se):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.startswith("OK")
+    assert r.stdout.strip().splitlines()[-1].startswith("OK"), r.stdout
 
 
 def test_ceemdan_stage_api_matches_monolithic(se, oracle):
