@@ -122,18 +122,24 @@ constexpr int kStripTiles = 16;  // longest strip (A.strip tiles): consecutive t
 // Per-strip constants of one warp.
 struct Strip {
     int slot, j0, nt, mode, par;
-    const double* src;     // the samples this pass reads (SIFT, DETECT)
     double* dst;           // where new values go (INIT: X, SIFT: the candidate; DETECT: none)
-    const double2* tab0;   // side-0 segment table, {x, y} plane ({m, 1/h} plane at + cap + 8)
-    const double2* tab1;   // side-1 segment table
-    const unsigned* ow;    // SIFT: tflags words of tile j0 (current knot parity)
     unsigned* nw;          // tflags words of tile j0 (parity of the new detection)
     unsigned* cnt0;        // scnt of tile j0, side 0 (side 1 at + A.G * tiles4)
     int to[2];             // lane l <= nt: knot offset (toff) of tile j0 + l, per side (SIFT)
 };
 
+// The global sources of a strip's bulk copies, only ever read by the lane that issues them.
+// They live in the warp's shared memory, not in registers: held across the strip in registers
+// they were spilled, and every group's copies then waited on local-memory reloads from L2.
+struct alignas(16) CopySrc {
+    const double* src;     // the samples this pass reads (SIFT, DETECT)
+    const unsigned* ow;    // SIFT: tflags words of tile j0 (current knot parity)
+    const double2* tab0;   // side-0 segment table, {x, y} plane ({m, 1/h} plane at + cap + 8)
+    const double2* tab1;   // side-1 segment table
+};
+
 template <int ST>
-__device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsigned strips) {
+__device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsigned strips, CopySrc& cs) {
     const int lane = threadIdx.x & 31;
     Strip S;
     const unsigned sx = item % strips;
@@ -145,12 +151,14 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
     S.mode = state == ST_INIT ? EM_INIT : (state == ST_DETECT ? EM_DETECT : EM_SIFT);
     const int cb = sl.cb, xb = sl.xb;
     S.par = sl.par;
-    S.src = A.bufs + buf_off(A, S.slot, (S.mode == EM_SIFT && cb >= 0) ? cb : xb);
     S.dst = S.mode == EM_INIT ? A.bufs + buf_off(A, S.slot, xb)
                               : (S.mode == EM_SIFT ? A.bufs + buf_off(A, S.slot, sl.db) : nullptr);
-    S.tab0 = tab_planes(A, 0, S.slot).a;
-    S.tab1 = tab_planes(A, 1, S.slot).a;
-    S.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
+    if (lane == 0) {
+        cs.src = A.bufs + buf_off(A, S.slot, (S.mode == EM_SIFT && cb >= 0) ? cb : xb);
+        cs.tab0 = tab_planes(A, 0, S.slot).a;
+        cs.tab1 = tab_planes(A, 1, S.slot).a;
+        cs.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
+    }
     S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
     S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
     S.to[0] = S.to[1] = 0;
@@ -166,7 +174,7 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
 // the free stage), parked in shared memory so it does not hold registers meanwhile.
 struct alignas(16) StripStash {
     int to[2][32];
-    int slot, mode, par, srcb, dstb, g, pad[2];
+    int slot, mode, par, dstb, g, pad[3];
 };
 template <int ST>
 __device__ __forceinline__ void stash_strip(const Arena& A, const Strip& S, int g, StripStash& st) {
@@ -178,7 +186,6 @@ __device__ __forceinline__ void stash_strip(const Arena& A, const Strip& S, int 
         st.slot = S.slot;
         st.mode = S.mode;
         st.par = S.par;
-        st.srcb = (S.mode == EM_SIFT && sl.cb >= 0) ? sl.cb : sl.xb;
         st.dstb = S.mode == EM_INIT ? sl.xb : sl.db;
         st.g = g;
     }
@@ -193,11 +200,7 @@ __device__ __forceinline__ Strip strip_from(const Arena& A, unsigned item, unsig
     S.nt = min(ST, A.tiles - S.j0);
     S.mode = st.mode;
     S.par = st.par;
-    S.src = A.bufs + buf_off(A, S.slot, st.srcb);
     S.dst = S.mode == EM_DETECT ? nullptr : A.bufs + buf_off(A, S.slot, st.dstb);
-    S.tab0 = tab_planes(A, 0, S.slot).a;
-    S.tab1 = tab_planes(A, 1, S.slot).a;
-    S.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
     S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
     S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
     S.to[0] = st.to[0][lane];
@@ -221,7 +224,8 @@ __device__ __forceinline__ int group_tiles(const Strip& S, int i) {
 }
 
 // Issue group (i, g)'s copies: samples, detection words, both sides' rows (lane 0 arms the barrier).
-__device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpStage& st, int bofs) {
+__device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpStage& st, int bofs,
+                                            const CopySrc& cs) {
     const int lo0 = __shfl_sync(0xffffffffu, S.to[0], i), lo1 = __shfl_sync(0xffffffffu, S.to[1], i);
     const int n0 = __shfl_sync(0xffffffffu, S.to[0], i + g) + 3 - lo0;
     const int n1 = __shfl_sync(0xffffffffu, S.to[1], i + g) + 3 - lo1;
@@ -233,13 +237,14 @@ __device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpSt
     double* f = st.flat;
     unsigned* ow = reinterpret_cast<unsigned*>(f + g * kEvalTile + 2);
     double2* r0 = reinterpret_cast<double2*>(ow + g * 32);  // {x,y} side 0 | side 1, then {m,1/h} side 0 | side 1
+    const CopySrc c = cs;
     bar_arrive_tx(&st.bar, sb + (unsigned)g * 128u + (unsigned)(n0 + n1) * 32u);
-    bulk_g2s(f + (e0 - (base - 2)), S.src + e0, sb, &st.bar);
-    bulk_g2s(ow, S.ow + i * 32, (unsigned)g * 128u, &st.bar);
-    bulk_g2s(r0, S.tab0 + lo0, (unsigned)n0 * 16u, &st.bar);
-    bulk_g2s(r0 + n0, S.tab1 + lo1, (unsigned)n1 * 16u, &st.bar);
-    bulk_g2s(r0 + n0 + n1, S.tab0 + bofs + lo0, (unsigned)n0 * 16u, &st.bar);
-    bulk_g2s(r0 + 2 * n0 + n1, S.tab1 + bofs + lo1, (unsigned)n1 * 16u, &st.bar);
+    bulk_g2s(f + (e0 - (base - 2)), c.src + e0, sb, &st.bar);
+    bulk_g2s(ow, c.ow + i * 32, (unsigned)g * 128u, &st.bar);
+    bulk_g2s(r0, c.tab0 + lo0, (unsigned)n0 * 16u, &st.bar);
+    bulk_g2s(r0 + n0, c.tab1 + lo1, (unsigned)n1 * 16u, &st.bar);
+    bulk_g2s(r0 + n0 + n1, c.tab0 + bofs + lo0, (unsigned)n0 * 16u, &st.bar);
+    bulk_g2s(r0 + 2 * n0 + n1, c.tab1 + bofs + lo1, (unsigned)n1 * 16u, &st.bar);
 }
 
 // DETECT passes stream samples only: the stage's row area holds kDetChunk tiles, so one bulk
@@ -248,7 +253,7 @@ __device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpSt
 constexpr int kDetChunk = 6;
 static_assert((kDetChunk * kEvalTile + 2) * 8 <= kStageBytes, "a DETECT chunk fits one stage");
 __device__ __forceinline__ double* stage_flat(WarpStage& st) { return st.flat; }
-__device__ __forceinline__ void issue_chunk(const Strip& S, int c, WarpStage& st) {
+__device__ __forceinline__ void issue_chunk(const Strip& S, int c, WarpStage& st, const CopySrc& cs) {
     if ((threadIdx.x & 31) != 0) return;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
     const int base = (S.j0 + c * kDetChunk) * kEvalTile;
@@ -256,7 +261,7 @@ __device__ __forceinline__ void issue_chunk(const Strip& S, int c, WarpStage& st
     const int e0 = base > 0 ? base - 2 : 0;                                 // 16-byte aligned
     const unsigned sb = (unsigned)(end - e0) * 8u;
     bar_arrive_tx(&st.bar, sb);
-    bulk_g2s(stage_flat(st) + (e0 - (base - 2)), S.src + e0, sb, &st.bar);
+    bulk_g2s(stage_flat(st) + (e0 - (base - 2)), cs.src + e0, sb, &st.bar);
 }
 
 __device__ __forceinline__ int smem_search(const double2* R, int hi, double t) {  // last q <= hi with x_q < t
@@ -478,10 +483,16 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     item = __shfl_sync(0xffffffffu, item, 0);
     StripStash& stash = reinterpret_cast<StripStash*>(reinterpret_cast<WarpStage*>(eval_smem) +
                                                       2 * (kEvalThreads / 32))[threadIdx.x >> 5];
+    CopySrc* csrc = reinterpret_cast<CopySrc*>(reinterpret_cast<StripStash*>(reinterpret_cast<WarpStage*>(eval_smem) +
+                                                                            2 * (kEvalThreads / 32)) +
+                                               kEvalThreads / 32) +
+                    2 * (threadIdx.x >> 5);  // [2] per warp: this strip's and the prefetched one's
+    int ci = 0;
     bool pre = false;  // this strip was set up (and its first copy issued) by the previous one
     while (item < nstrips) {
         if (lane == 0) next = atomicAdd(tk, 1u);
-        const Strip S = pre ? strip_from<ST>(A, item, strips, stash) : strip_setup<ST>(A, item, strips);
+        const Strip S = pre ? strip_from<ST>(A, item, strips, stash) : strip_setup<ST>(A, item, strips, csrc[ci]);
+        __syncwarp();  // csrc[ci] written by lane 0
         const int g_pre = pre ? stash.g : 0;
         bool pre_next = false;
         // during this strip's last group: set up the next strip and issue its first copy into
@@ -489,14 +500,15 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
         auto prefetch_next = [&](int fb) {
             const unsigned nx = __shfl_sync(0xffffffffu, next, 0);
             if (nx >= nstrips) return;
-            const Strip S2 = strip_setup<ST>(A, nx, strips);
+            const Strip S2 = strip_setup<ST>(A, nx, strips, csrc[ci ^ 1]);
             if (S2.mode == EM_INIT) return;
+            __syncwarp();
             int g2 = 0;
             if (S2.mode == EM_SIFT) {
                 g2 = group_tiles(S2, 0);
-                issue_group(S2, 0, g2, stage[fb], A.cap + 8);
+                issue_group(S2, 0, g2, stage[fb], A.cap + 8, csrc[ci ^ 1]);
             } else {
-                issue_chunk(S2, 0, stage[fb]);
+                issue_chunk(S2, 0, stage[fb], csrc[ci ^ 1]);
             }
             stash_strip<ST>(A, S2, g2, stash);
             pre_next = true;
@@ -505,9 +517,9 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
         double c2 = 0.0, c1 = 0.0, snum = 0.0, sden = 0.0;
         if (S.mode == EM_DETECT) {
             const int nch = (S.nt + kDetChunk - 1) / kDetChunk;
-            if (!pre) issue_chunk(S, 0, stage[b]);
+            if (!pre) issue_chunk(S, 0, stage[b], csrc[ci]);
             for (int c = 0; c < nch; ++c) {
-                if (c + 1 < nch) issue_chunk(S, c + 1, stage[b ^ 1]);
+                if (c + 1 < nch) issue_chunk(S, c + 1, stage[b ^ 1], csrc[ci]);
                 else prefetch_next(b ^ 1);
                 bar_wait(&stage[b].bar, (phase >> b) & 1u);
                 phase ^= 1u << b;
@@ -526,10 +538,10 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
             }
         } else if (S.mode == EM_SIFT) {
             int g = pre ? g_pre : group_tiles(S, 0);
-            if (!pre) issue_group(S, 0, g, stage[b], A.cap + 8);
+            if (!pre) issue_group(S, 0, g, stage[b], A.cap + 8, csrc[ci]);
             for (int i = 0; i < S.nt;) {
                 const int gn = i + g < S.nt ? group_tiles(S, i + g) : 0;
-                if (gn) issue_group(S, i + g, gn, stage[b ^ 1], A.cap + 8);
+                if (gn) issue_group(S, i + g, gn, stage[b ^ 1], A.cap + 8, csrc[ci]);
                 else prefetch_next(b ^ 1);
                 bar_wait(&stage[b].bar, (phase >> b) & 1u);
                 phase ^= 1u << b;
@@ -574,6 +586,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
         }
         item = __shfl_sync(0xffffffffu, next, 0);
         pre = pre_next;
+        if (pre_next) ci ^= 1;  // the prefetched strip's copy sources are in the other slot
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -582,7 +595,9 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     }
 }
 
-size_t eval_smem_bytes() { return (sizeof(WarpStage) * 2 + sizeof(StripStash)) * (kEvalThreads / 32); }
+size_t eval_smem_bytes() {
+    return (sizeof(WarpStage) * 2 + sizeof(StripStash) + 2 * sizeof(CopySrc)) * (kEvalThreads / 32);
+}
 cudaError_t eval_setup() {
     const cudaError_t e = cudaFuncSetAttribute(k_eval<kStripTiles>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)eval_smem_bytes());

@@ -463,23 +463,65 @@ def test_cpp_mirror_runs(se):
     assert r.stdout.strip().splitlines()[-1].startswith("OK"), r.stdout
 
 
+class _GpuCeemdanShard:
+    """parallel.sharded_ceemdan's engine contract over the C ABI stage entry points
+    (semd_ceemdan_shard_*), with torch CUDA tensors as the device buffers (test harness)."""
+
+    def __init__(self, ctx, x_dev, n, nr):
+        import ctypes as C
+
+        from paper_2106_15319_b200 import _native as N
+        self.C, self.c, self.x, self.n, self.nr = C, ctx, x_dev, n, nr
+        self.scfg, self.ecfg = N.SiftCfg(0.2, 300, 0), N.EnsCfg(0.2, nr, 0, 0)
+        self.modes = []
+
+    def begin(self, mb, me):
+        C = self.C
+        self.c.run("semd_ceemdan_shard_begin", C.c_void_p(self.x.data_ptr()), self.n, C.byref(self.scfg),
+                   C.byref(self.ecfg), mb, me)
+
+    def stage(self):
+        import torch
+        part = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
+        self.c.run("semd_ceemdan_shard_stage", self.C.c_void_p(part.data_ptr()))
+        return part
+
+    def finish(self, total, check_zero):
+        import torch
+        C = self.C
+        mode = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
+        ok = C.c_int32()
+        self.c.run("semd_ceemdan_shard_finish_stage", C.c_void_p(total.data_ptr()), self.nr, int(check_zero),
+                   C.c_void_p(mode.data_ptr()), C.byref(ok))
+        if ok.value:
+            self.modes.append(mode)
+        return bool(ok.value)
+
+    def residue_extrema(self):
+        t = self.C.c_size_t()
+        self.c.run("semd_ceemdan_shard_residue_extrema", self.C.byref(t))
+        return int(t.value)
+
+    def result(self):
+        import torch
+        res = torch.empty(self.n, dtype=torch.float64, device=self.x.device)
+        self.c.run("semd_ceemdan_shard_residue", self.C.c_void_p(res.data_ptr()))
+        return torch.stack(self.modes), res
+
+
 def test_ceemdan_stage_api_matches_monolithic(se, oracle):
-    """The per-stage CEEMDAN API (multi-GPU driver, world 1) is the monolithic CEEMDAN bit-for-bit,
-    and with the oracle's noise injected both are the oracle's CEEMDAN bit-for-bit."""
+    """The per-stage CEEMDAN API driven by parallel.sharded_ceemdan (world 1) is the monolithic
+    CEEMDAN bit-for-bit, and both are the oracle's CEEMDAN bit-for-bit (same noise: the device's
+    Box-Muller reproduces glibc's)."""
     import torch
 
-    from paper_2106_15319_b200.parallel import ceemdan_distributed
+    from paper_2106_15319_b200.parallel import sharded_ceemdan
     x = pickup_serialized(se, 50)[:3000].copy()
     nr = 24
     ctx = se.context()
-    w = np.stack([oracle.white_noise(x.size, oracle.derive_seed(0, m)) for m in range(nr)])
-    ctx.set_noise_override(w)
-    try:
-        mono = se.decompose(x, "ceemdan", nr=nr)
-        xd = torch.from_numpy(x).cuda()
-        imfs, res = ceemdan_distributed(xd, x.size, {}, {"nr": nr}, 0, 1, ctx=ctx)
-    finally:
-        ctx.set_noise_override(None)
+    mono = se.decompose(x, "ceemdan", nr=nr)
+    xd = torch.from_numpy(x).cuda()
+    imfs, res = sharded_ceemdan(nr, 0, 1, _GpuCeemdanShard(ctx, xd, x.size, nr), lambda p: p)
     o = oracle.decompose(x, 2, nr=nr)
     assert np.array_equal(imfs.cpu().numpy(), mono["imfs"]) and np.array_equal(res.cpu().numpy(), mono["residue"])
     assert np.array_equal(mono["imfs"], o[0]) and np.array_equal(mono["residue"], o[1])
@@ -541,7 +583,6 @@ def test_ceemdan_residue_extrema_count(se, oracle):
     when untraced: equal to the oracle's find_extrema on plateau-rich and smooth signals."""
     import torch
 
-    from paper_2106_15319_b200.parallel import GpuCeemdanShard
     ctx = se.context()
     rng = np.random.default_rng(7)
     cases = [rng.integers(-2, 3, size=int(rng.integers(4, 9000))).astype(float) for _ in range(6)]
@@ -549,7 +590,7 @@ def test_ceemdan_residue_extrema_count(se, oracle):
     cases += [np.concatenate([np.zeros(10), np.ones(5000), np.zeros(3000), -np.ones(7001), np.zeros(3)]),
               np.array([1.0, 1.0, 1.0, 1.0]), np.array([0.0, 1.0, 1.0, 0.0, 2.0, 2.0, 2.0])]
     for x in cases:
-        eng = GpuCeemdanShard(ctx, torch.from_numpy(x).cuda(), x.size, {}, {"nr": 2})
+        eng = _GpuCeemdanShard(ctx, torch.from_numpy(x).cuda(), x.size, 2)
         eng.begin(0, 2)  # the shard's residue starts as x
         max_idx, _, min_idx, _ = oracle.find_extrema(x)
         assert eng.residue_extrema() == len(max_idx) + len(min_idx)
