@@ -85,6 +85,8 @@ typedef struct semd_stats {
     int32_t waves;
     double eval_ms;          /* optional: device time of the sift (eval) kernel, if timing enabled */
     uint64_t eval_launches;
+    uint64_t sd_rechecks;    /* SD stop tests whose tree-summed ratio was too close to sd_threshold to certify
+                                and were redone with the reference's sequential sums */
 } semd_stats;
 
 typedef struct semd_ctx semd_ctx;

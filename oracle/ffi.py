@@ -182,6 +182,18 @@ class Oracle:
         sums, _, _ = self._take(d, rc)
         return sums, buf[:tr.count].copy()
 
+    def sd_ratios(self, x, sd=0.2, iters=300):
+        """extract_imf -> (imf, sift_count, the reference's num/den of every sift)."""
+        x = _f64(x)
+        out = np.zeros(x.size)
+        cnt = C.c_int32()
+        r = np.zeros(max(iters, 1) + 1)
+        k = C.c_size_t()
+        cfg = _SiftCfg(sd, iters, 0)
+        self._chk(self.lib.so_sd_ratios(_d(x), C.c_size_t(x.size), C.byref(cfg), _d(out), C.byref(cnt), _d(r),
+                                        C.c_size_t(r.size), C.byref(k)))
+        return out, cnt.value, r[:k.value].copy()
+
     # --- serializer ---------------------------------------------------------------
     def concatenate(self, x_cm: np.ndarray, M: int, N: int, D: int, naive: bool = False) -> np.ndarray:
         x = _f64(x_cm).ravel()

@@ -195,6 +195,10 @@ static void scratch_free(scratch* s) {
     free(s->max_idx); free(s->min_idx); free(s->max_val); free(s->min_val); free(s->upper); free(s->lower);
 }
 
+/* Test hook: num/den of every sift of the next extract_imf (so_sd_ratios). */
+static double* g_ratio_out = NULL;
+static size_t g_ratio_cap = 0, g_ratio_n = 0;
+
 /* emd.cpp:127-153 */
 static int extract_imf_t(const double* x, size_t n, const so_sift_cfg* cfg, double* cur, int32_t* count,
                          const tctx* tc) {
@@ -225,6 +229,7 @@ static int extract_imf_t(const double* x, size_t n, const so_sift_cfg* cfg, doub
             cur[i] -= mean;
         }
         ++*count;
+        if (g_ratio_out && g_ratio_n < g_ratio_cap) g_ratio_out[g_ratio_n++] = num / den;
         if (den == 0.0 || num / den < cfg->sd_threshold) break; /* :150 */
     }
     scratch_free(&s);
@@ -235,6 +240,19 @@ int so_extract_imf(const double* x, size_t n, const so_sift_cfg* cfg, double* im
                    so_trace* tr) {
     tctx tc = {tr, 0, 0, 0};
     return extract_imf_t(x, n, cfg, imf, sift_count, &tc);
+}
+
+/* extract_imf (emd.cpp:127-153) recording the reference's SD ratio num/den of every sift
+ * (emd.cpp:150, sequential sums) -- the adversarial-threshold tests of the GPU's certified stop test. */
+int so_sd_ratios(const double* x, size_t n, const so_sift_cfg* cfg, double* imf, int32_t* sift_count, double* ratios,
+                 size_t cap, size_t* count) {
+    g_ratio_out = ratios;
+    g_ratio_cap = cap;
+    g_ratio_n = 0;
+    const int rc = extract_imf_t(x, n, cfg, imf, sift_count, NULL);
+    *count = g_ratio_n;
+    g_ratio_out = NULL;
+    return rc;
 }
 
 /* -------------------------------------------------------------------- emd */

@@ -51,7 +51,8 @@ class Trace(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("sifted_samples", C.c_uint64), ("sift_iterations", C.c_uint64), ("steps", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("solve_hazards", C.c_uint64), ("slots", C.c_int32),
-                ("waves", C.c_int32), ("eval_ms", C.c_double), ("eval_launches", C.c_uint64)]
+                ("waves", C.c_int32), ("eval_ms", C.c_double), ("eval_launches", C.c_uint64),
+                ("sd_rechecks", C.c_uint64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/semd_b200.h

@@ -478,6 +478,7 @@ struct semd_ctx {
             stats.sift_iterations += (uint64_t)(S.sifted / std::max(1, A.L));
         }
         stats.solve_hazards += (uint64_t)c.hazards;
+        stats.sd_rechecks += (uint64_t)c.sd_rechecks;
         if (timing) stats.eval_ms += (double)c.ev_ns * 1e-6;
         for (int id = 0; id < 5; ++id) {  // the spans the last two steps left unfolded
             unsigned long long ns = c.kns[id];

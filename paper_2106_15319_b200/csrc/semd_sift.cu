@@ -116,6 +116,51 @@ __device__ void build_lists(const Arena& A, bool allow_final) {
 // Chunked per-slot tile prefix of the new extrema (see k_scan) + SD sums in a
 // fixed reduction order; the last CTA applies extract_imf's control flow.
 
+// ---- the SD stop test (emd.cpp:142-150), certified ----------------------------------------
+// The engine forms num = sum mean^2 and den = sum cur^2 in a fixed tree (per-lane runs, warp
+// sums, strip and chunk partials); the reference adds left to right. The terms are bit-identical,
+// non-negative and n in number, so both sums lie within g = n u / (1 - n u) of the exact sum S,
+// and each within 2g/(1-g) (relative) of the other. The decision num/den < sd_threshold is
+// certified when the threshold lies outside the interval those bounds allow for the reference's
+// ratio; otherwise the slot's sums are redone in the reference's order before deciding.
+__device__ bool sd_decision_uncertain(double num, double den, long long n, double thr) {
+    if (!(den > 0.0)) return false;  // den == 0 exactly when every cur^2 term is 0: the same in any order
+    const double u = 0x1p-53;
+    const double g = (double)n * u / (1.0 - (double)n * u);
+    const double e = 2.0 * g / (1.0 - g) * 1.0001;
+    const double lo = (num * (1.0 - e)) / (den * (1.0 + e)) * (1.0 - 8.0 * u);
+    const double hi = (num * (1.0 + e)) / (den * (1.0 - e)) * (1.0 + 8.0 * u);
+    return lo <= thr && thr <= hi;
+}
+
+// The reference's own loop, emd.cpp:142-148 (num += mean*mean, den += cur*cur, t = 0..L-1), over
+// this iteration's envelopes (the segment tables of the step's solve, the reference's segment
+// march, emd.cpp:79) and the candidate it sifted. One thread: only reached for uncertified tests.
+__device__ __noinline__ void sd_sums_sequential(const Arena& A, int s, int cur_buf, double* num, double* den) {
+    const Slot& S = A.slots[s];
+    const double* cur = A.bufs + buf_off(A, s, cur_buf);
+    const TabPlanes tp[2] = {tab_planes(A, 0, s), tab_planes(A, 1, s)};
+    const int N[2] = {(int)S.n[0] + 4, (int)S.n[1] + 4};
+    int seg[2] = {0, 0};
+    double x = 0.0, y = 0.0;
+    for (int t = 0; t < A.L; ++t) {
+        const double tt = (double)t;
+        double e[2];
+        for (int k = 0; k < 2; ++k) {
+            while (seg[k] + 2 < N[k] && tt > tp[k].a[seg[k] + 1].x) ++seg[k];
+            const double2 a0 = tp[k].a[seg[k]], b0 = tp[k].b[seg[k]], a1 = tp[k].a[seg[k] + 1];
+            const double m1 = tp[k].b[seg[k] + 1].x;
+            const double h = a1.x - a0.x;
+            e[k] = spline_eval_fast(a0.x, a1.x, a0.y, a1.y, b0.x, m1, h, b0.y, h * h, tt);
+        }
+        const double mean = 0.5 * (e[0] + e[1]);
+        x += mean * mean;
+        y += cur[t] * cur[t];
+    }
+    *num = x;
+    *den = y;
+}
+
 // extract_imf's control flow (emd.cpp:131-151) for one slot after its eval
 // pass; returns 1 when this step's extrema must be compacted.
 __device__ int decide_slot(const Arena& A, int s) {
@@ -162,8 +207,13 @@ __device__ int decide_slot(const Arena& A, int s) {
     if (state == ST_SIFT) {
         S.iter += 1;
         S.sifted += A.L;
+        const int cur_buf = S.cb >= 0 ? S.cb : S.xb;  // the candidate this step sifted
         S.cb = S.db;
-        const double num = S.num, den = S.den;
+        double num = S.num, den = S.den;
+        if ((A.debug & 4) || sd_decision_uncertain(num, den, A.L, A.sd_threshold)) {
+            sd_sums_sequential(A, s, cur_buf, &num, &den);
+            atomicAdd(&A.ctrl->sd_rechecks, 1);
+        }
         bool stop = (den == 0.0 || num / den < A.sd_threshold) || S.iter >= A.max_sift_iters;
         if (!stop) {
             S.trace_iter = S.iter;
@@ -240,7 +290,7 @@ __host__ __device__ inline int scan_grid(const Arena& A) {
     return scan_by_warp(A) ? (2 * A.G + kScanThreads / 32 - 1) / (kScanThreads / 32) : 2 * A.G * A.chunks;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
+__global__ void __launch_bounds__(kScanThreads, 5) k_scan(Arena A) {
     pdl_begin();
     if (A.ctrl->finished) return;  // a step launched past the run's end
     const int kstep_ = A.ctrl->step;

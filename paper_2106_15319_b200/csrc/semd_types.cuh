@@ -116,7 +116,8 @@ struct Ctrl {
     int step;
     int hz_count;  // hazard log records produced
     int finished;  // the run's last step has published active == 0: later steps return at once
-    int pad[4];
+    int sd_rechecks;  // SD stop tests redone with the reference's sequential sums (uncertified decisions)
+    int pad[3];
     unsigned long long ev_t0;  // k_eval span of this step (globaltimer): min CTA start, max CTA end
     unsigned long long ev_t1;
     unsigned long long ev_ns;  // accumulated k_eval spans of this run (timing mode)
@@ -199,7 +200,8 @@ struct Arena {
     TraceRec* trace;
     int* hzlog;       // [hzlog_cap][8] solve-hazard records {m, k, iter, side, n, block, blocks, 0}
     int hzlog_cap;
-    int debug;        // test hook bit 0: treat every solve block boundary as a hazard (exercise the repair)
+    int debug;        // test hooks: bit 0 treat every solve block boundary as a hazard (exercise the repair);
+                      // bit 2 redo every SD stop test with the sequential sums
                       // bit 1: accumulate k_solve per-phase clock cycles into prof[]
     unsigned long long* prof;  // [16]
     int* status_host; // mapped pinned: [0] active slots after this step, [1] step counter

@@ -11,8 +11,12 @@ top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
-start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
-rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+which = int(__import__("os").environ.get("RESULT", "0"))  # which kernel result of a multi-result report
+starts = [i for i, l in enumerate(lines) if l.startswith('"Address"')]
+start = starts[which]
+end = next((i for i in range(start + 1, len(lines)) if lines[i].startswith('"Kernel Name"') or lines[i].startswith('"Address"')),
+           len(lines))
+rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:end]))))
 agg = collections.Counter()
 tot = 0
 for r in rows:

@@ -622,3 +622,41 @@ def test_eemd_shards_sum_to_whole(se):
     b, kb = part(5, nr)
     assert kw == max(ka, kb)
     assert np.max(np.abs((a + b) - whole)) <= 1e-12 * np.max(np.abs(whole))
+
+
+def test_sd_stop_adversarial_thresholds(se, oracle):
+    """The SD stop test (emd.cpp:150) at thresholds equal to, and one ulp above, the reference's
+    own num/den of a sift: the engine's tree-summed ratio can differ from the reference's
+    sequential one in the last bits, so these decisions are uncertifiable and must be redone with
+    the reference's sequential sums (semd_stats.sd_rechecks counts them). Sift counts and IMFs
+    must equal the oracle's at every such threshold."""
+    rng = np.random.default_rng(150)
+    c = se.context()
+    rechecks = 0
+    for n in (700, 3001, 200_003):
+        t = np.arange(n)
+        x = np.sin(0.07 * t) + 0.5 * np.sin(0.011 * t + 1.0) + 0.3 * rng.standard_normal(n)
+        _, cnt, ratios = oracle.sd_ratios(x)
+        thresholds = sorted({float(r) for r in ratios} | {float(np.nextafter(r, np.inf)) for r in ratios})
+        for thr in thresholds:
+            gi, gc = se.extract_imf(x, sd_threshold=thr)
+            rechecks += c.stats()["sd_rechecks"]
+            oi, oc = oracle.extract_imf(x, sd=thr)
+            assert gc == oc, (n, thr, gc, oc)
+            assert np.array_equal(gi, oi), (n, thr)
+    assert rechecks > 0  # the uncertain branch ran
+
+
+def test_sd_forced_sequential_sums_identical(se):
+    """Debug bit 2 redoes every SD test with the sequential sums: results are unchanged."""
+    from tests.golden.inputs import rng_signal
+    x = rng_signal(31, 2500)
+    c = se.context()
+    a = se.decompose_full(x, "eemd", nr=6)
+    c.run("semd_set_debug", 4)
+    try:
+        b = se.decompose_full(x, "eemd", nr=6)
+    finally:
+        c.run("semd_set_debug", 0)
+    assert b["stats"]["sd_rechecks"] == b["stats"]["sift_iterations"] > 0
+    assert np.array_equal(a["imfs"], b["imfs"]) and np.array_equal(a["residue"], b["residue"])
