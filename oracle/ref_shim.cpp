@@ -21,9 +21,16 @@
 #include <thread>
 #include <vector>
 
+#include <filesystem>
+#include <fstream>
+
 #include "semd/emd.hpp"
+#include "semd/io.hpp"
 #include "semd/serialize.hpp"
 #include "semd/synth.hpp"
+#ifdef REF_HAVE_JSON
+#include "nlohmann/json.hpp"
+#endif
 
 namespace {
 
@@ -598,5 +605,89 @@ int ref_multivariate_sinusoids(std::size_t n, double fs, double* out) {
 }
 
 std::size_t ref_default_transition_length(std::size_t rows) { return semd::default_transition_length(rows); }
+
+// The reference CLI's `decompose` (cli.cpp:93-134) restated over the reference's own library
+// functions (read_csv / read_pgm / image_to_multisignal, serial_decompose, write_csv / write_pgm)
+// and nlohmann::json for the sidecar (cli.cpp:51-64): the golden outputs for semd-cli. cli.cpp
+// itself needs CLI11, which is not in this image.
+int ref_cli_decompose(const char* input, const char* algo_name, const char* d_flag, double nstd, int nr,
+                      uint64_t seed, double sd, int iters, int imfs, const char* out_dir) {
+    return guard([&] {
+        namespace fs = std::filesystem;
+        const semd::Algorithm algo = semd::parse_algorithm(algo_name);
+        const semd::SiftConfig cfg{sd, iters, imfs};
+        const semd::EnsembleConfig ens{nstd, nr, seed};
+        fs::create_directories(out_dir);
+        std::string ext = fs::path(input).extension().string();
+        for (char& c : ext) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+        const bool is_pgm = ext == ".pgm";
+        const std::string stem = fs::path(input).stem().string();
+        semd::MultiSignal data;
+        std::vector<std::string> header;
+        if (is_pgm) {
+            data = semd::image_to_multisignal(semd::read_pgm(input));
+            for (std::size_t j = 0; j < data.channels(); ++j) header.push_back("c" + std::to_string(j + 1));
+        } else {
+            semd::CsvData csv = semd::read_csv(input);
+            data = std::move(csv.data);
+            header = std::move(csv.header);
+        }
+        const std::string dfl(d_flag);
+        const std::size_t d = dfl == "auto" ? semd::default_transition_length(data.rows()) : std::stoul(dfl);
+        const semd::ImfTensor t = semd::serial_decompose(data, d, algo, cfg, ens);
+        for (std::size_t k = 0; k < t.modes(); ++k) {
+            char nb[16];
+            std::snprintf(nb, sizeof nb, "imf_%02zu", k + 1);
+            const std::string name = stem + "_" + (k + 1 == t.modes() ? std::string("residue") : std::string(nb));
+            semd::MultiSignal mode(t.rows(), t.channels());
+            for (std::size_t j = 0; j < t.channels(); ++j)
+                for (std::size_t i = 0; i < t.rows(); ++i) mode(i, j) = t(i, j, k);
+            semd::write_csv((fs::path(out_dir) / (name + ".csv")).string(), mode, header);
+            if (is_pgm) {
+                semd::Image img(t.rows(), t.channels());
+                for (std::size_t c = 0; c < t.channels(); ++c)
+                    for (std::size_t r = 0; r < t.rows(); ++r) img(r, c) = t(r, c, k);
+                semd::write_pgm((fs::path(out_dir) / (name + ".pgm")).string(), img, true);
+            }
+        }
+#ifdef REF_HAVE_JSON
+        nlohmann::json j{{"M", data.rows()}, {"N", data.channels()}, {"D", d}, {"K", t.modes()},
+                         {"algorithm", semd::algorithm_name(algo)}, {"seed", ens.base_seed},
+                         {"nstd", ens.nstd}, {"nr", ens.nr}};
+        std::ofstream(fs::path(out_dir) / (stem + "_decomposition.json")) << j.dump(2) << '\n';
+#else
+        throw std::runtime_error("built without nlohmann::json");
+#endif
+    });
+}
+
+// nlohmann::json's text for one double (the sidecar's nstd), for the formatter test.
+int ref_json_double(double v, char* out, std::size_t cap) {
+#ifdef REF_HAVE_JSON
+    const std::string s = nlohmann::json(v).dump();
+    std::snprintf(out, cap, "%s", s.c_str());
+    return 0;
+#else
+    return 4;
+#endif
+}
+
+int ref_synth_signals_csv(std::size_t n, double fs, const char* path) {
+    return guard([&] {
+        const semd::MultiSignal s = semd::multivariate_sinusoids(semd::PickupMask::standard(), n, fs);
+        std::vector<std::string> header;
+        for (const char* name : semd::PickupMask::names()) header.push_back(name);
+        semd::write_csv(path, s, header);
+    });
+}
+
+int ref_write_pgm(const double* px, std::size_t rows, std::size_t cols, int rescale, const char* path) {
+    return guard([&] {
+        semd::Image img(rows, cols);
+        for (std::size_t p = 0; p < rows * cols; ++p) img.data()[p] = px[p];
+        semd::write_pgm(path, img, rescale != 0);
+    });
+}
+
 
 }  // extern "C"

@@ -18,10 +18,10 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fma
 
 
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(os.path.join(PKG, "semd-cli")):
         return True
     t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(os.path.join(HERE, f)) > t for f in SRCS + HDRS)
+    return any(os.path.getmtime(os.path.join(HERE, f)) > t for f in SRCS + HDRS + ["semd_cli.cpp"])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -42,7 +42,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(LIB + ".tmp", LIB)
+    build_cli(verbose)
     return LIB
+
+
+CLI = os.path.join(PKG, "semd-cli")
+INC = os.path.join(PKG, "..", "include")
+
+
+def build_cli(verbose: bool = False) -> str:
+    """The reference's `decompose` front-end (semd_cli.cpp) linked against libsemd_b200.so."""
+    cmd = ["g++", "-std=c++20", "-O2", "-I" + INC, os.path.join(HERE, "semd_cli.cpp"), "-o", CLI + ".tmp",
+           "-L" + PKG, "-lsemd_b200", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd))
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"semd-cli build failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
 
 
 if __name__ == "__main__":
