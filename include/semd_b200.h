@@ -186,6 +186,15 @@ int semd_slicewise_decompose_device(semd_ctx* ctx, int algo, const double* d_x, 
                                     const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* d_tensor,
                                     size_t k_cap, size_t* modes_out);
 
+/* recognition.cpp:281-298's decompositions batched: B independent serial_decompose calls
+ * (serialize.cpp:97-105) on same-shape multi-signals (e.g. images as channels) in one engine pass.
+ * x: B blocks of M x N (channel-contiguous); tensor: B blocks of k_cap x N x M in the ImfTensor
+ * layout, item b holding K_b IMFs then its residue (zero modes after); modes_out[b] = K_b + 1.
+ * SEMD_CAPACITY when some K_b + 1 > k_cap. */
+int semd_serial_decompose_batch(semd_ctx* ctx, int algo, const double* x, size_t B, size_t M, size_t N, size_t D,
+                                const semd_sift_cfg* cfg, const semd_ens_cfg* ens, double* tensor, size_t k_cap,
+                                size_t* modes_out);
+
 /* ---- CEEMDAN across GPUs: stages over a realization shard (emd.cpp:264-344) ----------
  * Rank r owns realizations [m_begin, m_end) (seeds from the global index). Driver loop:
  *   begin; stage(partial); all-reduce(partial) -> total; finish_stage(total, nr, 0, ...);

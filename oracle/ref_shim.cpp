@@ -26,6 +26,7 @@
 
 #include "semd/emd.hpp"
 #include "semd/io.hpp"
+#include "semd/recognition.hpp"
 #include "semd/serialize.hpp"
 #include "semd/synth.hpp"
 #ifdef REF_HAVE_JSON
@@ -678,6 +679,30 @@ int ref_synth_signals_csv(std::size_t n, double fs, const char* path) {
         std::vector<std::string> header;
         for (const char* name : semd::PickupMask::names()) header.push_back(name);
         semd::write_csv(path, s, header);
+    });
+}
+
+// recognition.cpp:281-298 build_feature_bank on B images (row-major rows x cols each); out gets
+// bank.features(1, k) for k = 1..target: B x target x (rows*cols) doubles.
+int ref_feature_bank(const double* imgs, std::size_t B, std::size_t rows, std::size_t cols, int algo, std::size_t d,
+                     double nstd, int nr, uint64_t seed, double snr_db, uint64_t speckle_seed, std::size_t target,
+                     double* out) {
+    return guard([&] {
+        semd::FaceDataset ds;
+        for (std::size_t b = 0; b < B; ++b) {
+            semd::Image img(rows, cols);
+            for (std::size_t p = 0; p < rows * cols; ++p) img.data()[p] = imgs[b * rows * cols + p];
+            ds.images.push_back(std::move(img));
+            ds.labels.push_back(int(b) + 1);
+        }
+        const semd::FaceFeatureBank bank = semd::build_feature_bank(
+            ds, static_cast<semd::Algorithm>(algo), d, semd::SiftConfig{}, {nstd, nr, seed}, snr_db, speckle_seed, target);
+        const std::size_t dim = rows * cols;
+        for (std::size_t k = 1; k <= target; ++k) {
+            const auto f = bank.features(1, k);
+            for (std::size_t b = 0; b < B; ++b)
+                std::memcpy(out + (b * target + (k - 1)) * dim, f[b].data(), dim * 8);
+        }
     });
 }
 

@@ -103,6 +103,9 @@ SIGNATURES = {
     "semd_slicewise_decompose_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_size_t,
                                                   C.POINTER(SiftCfg), C.POINTER(EnsCfg), C.c_void_p, C.c_size_t,
                                                   _szp]),
+    "semd_serial_decompose_batch": (C.c_int, [C.c_void_p, C.c_int, _dp, C.c_size_t, C.c_size_t, C.c_size_t,
+                                              C.c_size_t, C.POINTER(SiftCfg), C.POINTER(EnsCfg), _dp, C.c_size_t,
+                                              _szp]),
     "semd_ceemdan_shard_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(SiftCfg), C.POINTER(EnsCfg),
                                            C.c_int32, C.c_int32]),
     "semd_ceemdan_shard_residue_extrema": (C.c_int, [C.c_void_p, _szp]),

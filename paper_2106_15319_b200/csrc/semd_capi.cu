@@ -995,6 +995,7 @@ struct semd_ctx {
     // EMD / EEMD: every channel (EEMD: channel x realization, channel-major) is a job of ONE
     // batched engine run; job j owns IMF rows [j*kc, (j+1)*kc). CEEMDAN: channel by channel.
     DBuf sl_imfs, sl_res, sl_kj, sl_beta;
+    std::vector<int> sl_kj_host;  // IMF count of every channel of the last slicewise run
     void slicewise_device(int algo, const double* d_x, long long M, int N, const semd_sift_cfg& cfg,
                           const semd_ens_cfg& ens, double* d_tensor, size_t cap_modes, size_t* modes_out) {
         if (M == 0 || N == 0) raise(SEMD_INVALID_INPUT, "slicewise_decompose: empty input");
@@ -1096,6 +1097,7 @@ struct semd_ctx {
         }
         int common = 1;
         for (int j = 0; j < N; ++j) common = std::max(common, kj[j] + 1);
+        sl_kj_host = kj;
         *modes_out = (size_t)common;
         if ((size_t)common > cap_modes) raise(SEMD_CAPACITY, "output holds %zu modes, decomposition has %d", cap_modes, common);
         sl_kj.alloc((size_t)N * 4);
@@ -1104,6 +1106,67 @@ struct semd_ctx {
                                            scaled ? 1.0 / (double)ens.nr : 1.0, scaled ? 1 : 0, d_tensor, stream);
         ck(cudaGetLastError(), "slicewise");
         ck(cudaStreamSynchronize(stream), "slicewise");
+    }
+
+    // B independent serial_decompose calls (serialize.cpp:97-105) on same-shape multi-signals, as
+    // one batched engine pass: every multi-signal is serialized (x_b -> s_b of length L), the B
+    // signals are decomposed like slicewise channels (EMD: one job each; EEMD: B x nr jobs sharing
+    // the realizations' noise w_m, beta_b from s_b; CEEMDAN: one after another), and each result is
+    // deconcatenated into its own ImfTensor: K_b IMFs then the residue, zero modes after.
+    DBuf sb_ser, sb_tens;
+    void serial_batch_device(int algo, const double* d_x, long long B, long long M, long long N, long long D,
+                             const semd_sift_cfg& cfg, const semd_ens_cfg& ens, double* d_out, size_t k_cap,
+                             size_t* modes_out) {
+        if (B < 1) raise(SEMD_INVALID_INPUT, "serial_decompose_batch: empty batch");
+        if (M == 0 || N == 0) raise(SEMD_INVALID_INPUT, "concatenate: empty input");
+        if (D < 1) raise(SEMD_INVALID_INPUT, "concatenate: D must be at least 1");
+        if (D > M) raise(SEMD_INVALID_INPUT, "concatenate: transition longer than channel");
+        const long long L = M * N + D * (N - 1);
+        sb_ser.alloc((size_t)B * L * 8);
+        scratch2.alloc((size_t)D * 8);
+        semd::dev::launch_transition_weights(D, scratch2.as<double>(), stream);
+        for (long long b = 0; b < B; ++b)
+            semd::dev::launch_concatenate(d_x + (size_t)b * M * N, M, N, D, scratch2.as<double>(),
+                                          sb_ser.as<double>() + (size_t)b * L, 0, stream);
+        ck(cudaGetLastError(), "concatenate");
+        size_t cap = std::max<size_t>(k_cap, 2), common = 0;
+        for (;;) {  // the slicewise tensor holds the common mode count; grow to fit it
+            sb_tens.alloc(cap * (size_t)B * L * 8);
+            try {
+                slicewise_device(algo, sb_ser.as<double>(), L, (int)B, cfg, ens, sb_tens.as<double>(), cap, &common);
+                break;
+            } catch (const Error& e) {
+                if (e.code != SEMD_CAPACITY || common <= cap) throw;
+                cap = common;
+            }
+        }
+        bool fits = true;
+        for (long long b = 0; b < B; ++b) {
+            modes_out[b] = (size_t)sl_kj_host[b] + 1;
+            fits = fits && modes_out[b] <= k_cap;
+        }
+        if (!fits) raise(SEMD_CAPACITY, "output holds %zu modes per item, a decomposition has more", k_cap);
+        // slicewise layout (k*B + b)*L + i, residue at k = common-1 -> per item K_b IMFs + residue
+        DBuf modes((size_t)(common + 1) * L * 8);
+        for (long long b = 0; b < B; ++b) {
+            const int Kb = sl_kj_host[b];
+            double* mrow = modes.as<double>();
+            const double* t = sb_tens.as<double>();
+            if (Kb)
+                ck(cudaMemcpy2DAsync(mrow, (size_t)L * 8, t + (size_t)b * L, (size_t)B * L * 8, (size_t)L * 8, (size_t)Kb,
+                                     cudaMemcpyDeviceToDevice, stream),
+                   "modes");
+            ck(cudaMemcpyAsync(mrow + (size_t)Kb * L, t + ((size_t)(common - 1) * B + b) * L, (size_t)L * 8,
+                               cudaMemcpyDeviceToDevice, stream),
+               "residue");
+            double* dst = d_out + (size_t)b * k_cap * N * M;
+            if ((size_t)Kb + 1 < k_cap)
+                ck(cudaMemsetAsync(dst + (size_t)(Kb + 1) * N * M, 0, (k_cap - Kb - 1) * (size_t)N * M * 8, stream),
+                   "zero modes");
+            semd::dev::launch_deconcatenate(mrow, Kb + 1, L, M, N, D, dst, stream);
+        }
+        ck(cudaGetLastError(), "deconcatenate");
+        ck(cudaStreamSynchronize(stream), "serial batch");
     }
 
     // Full decomposition with device buffers. Returns K via *k_out; SEMD_CAPACITY if K > k_cap.
@@ -2015,6 +2078,25 @@ int semd_comm_destroy(semd_ctx* ctx) {
         ctx->rank = 0;
         ctx->world = 1;
         ctx->root = -1;
+    });
+}
+
+// ---- recognition.cpp:281-298: the feature bank's decompositions, batched ---------------------
+int semd_serial_decompose_batch(semd_ctx* ctx, int algo, const double* x, size_t B, size_t M, size_t N, size_t D,
+                                const semd_sift_cfg* cfg_, const semd_ens_cfg* ens_, double* tensor, size_t k_cap,
+                                size_t* modes_out) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (algo < 0 || algo > 2) raise(SEMD_INVALID_INPUT, "unknown algorithm");
+        if (!modes_out) raise(SEMD_INVALID_INPUT, "null modes_out");
+        const semd_sift_cfg cfg = sift_or_default(cfg_);
+        const semd_ens_cfg ens = ens_or_default(ens_);
+        const double* d_x = ctx->upload(ctx->in_x, x, B * M * N);
+        ctx->reset_stats(1);
+        DBuf t(std::max<size_t>(k_cap, 1) * B * M * N * 8);
+        ctx->serial_batch_device(algo, d_x, (long long)B, (long long)M, (long long)N, (long long)D, cfg, ens,
+                                 t.as<double>(), k_cap, modes_out);
+        ctx->download(tensor, t.as<double>(), k_cap * B * M * N);
     });
 }
 
