@@ -41,9 +41,9 @@ def test_feature_bank_bit_identical_to_reference(se, tmp_path):
         fin, fout = tmp_path / "in.bin", tmp_path / "out.bin"
         imgs.tofile(fin)
         snr = "inf" if case["snr_db"] is None else repr(case["snr_db"])
-        r = subprocess.run([exe, fin, fout, B, rows, cols, case["algo"], case["d"], repr(case["nstd"]), case["nr"],
-                            case["seed"], snr, case["speckle_seed"], case["target"]], capture_output=True, text=True,
-                           timeout=600)
+        argv = [exe, fin, fout, B, rows, cols, case["algo"], case["d"], repr(case["nstd"]), case["nr"], case["seed"],
+                snr, case["speckle_seed"], case["target"]]
+        r = subprocess.run(list(map(str, argv)), capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout + r.stderr
         feats = np.fromfile(fout, dtype="<f8")
         assert [float(v).hex() for v in feats.reshape(B, case["target"], -1)[0, -1, :8]] == case["features_head"]
