@@ -408,16 +408,28 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
 
     // extrema flags branch-free (find_extrema, emd.cpp:16-33); samples equal to a neighbour
     // take the reference's plateau rule in a warp-uniform slow path
-    unsigned fmax = 0, fmin = 0, plat = 0;
+    // Each neighbour pair (w[j], w[j+1]) is compared once (up: w[j+1] > w[j], dn: w[j+1] < w[j])
+    // and shared by the two samples it borders: v > r of sample k is dn of pair k+1. Equality is
+    // "neither up nor dn"; a NaN neighbour lands in the plateau path, which compares exactly.
+    unsigned up = 0, dn = 0;
 #pragma unroll
-    for (int k = 0; k < kSpt; ++k) {
-        const int t = t0 - 1 + k;
-        const bool in = Interior || (t >= 1 && t <= L - 2);
-        const double l = w[k], v = w[k + 1], r = w[k + 2];
-        fmax |= (unsigned)(in && v > l && v > r) << k;
-        fmin |= (unsigned)(in && v < l && v < r) << k;
-        plat |= (unsigned)(in && (v == l || v == r)) << k;
+    for (int j = 0; j <= kSpt; ++j) {
+        up |= (unsigned)(w[j + 1] > w[j]) << j;
+        dn |= (unsigned)(w[j + 1] < w[j]) << j;
     }
+    unsigned inm = (1u << kSpt) - 1u;
+    if (!Interior) {
+        inm = 0;
+#pragma unroll
+        for (int k = 0; k < kSpt; ++k) {
+            const int t = t0 - 1 + k;
+            inm |= (unsigned)(t >= 1 && t <= L - 2) << k;
+        }
+    }
+    const unsigned eq = ~(up | dn);  // bit j: w[j+1] == w[j] (or unordered)
+    unsigned fmax = up & (dn >> 1) & inm;  // v > l (up_k) and v > r (dn_{k+1})
+    unsigned fmin = dn & (up >> 1) & inm;  // v < l (dn_k) and v < r (up_{k+1})
+    const unsigned plat = (eq | (eq >> 1)) & inm;  // v == l or v == r
     if (__any_sync(0xffffffffu, plat != 0u)) {
         for (int k = 0; k < kSpt; ++k) {
             if (!(plat & (1u << k))) continue;
