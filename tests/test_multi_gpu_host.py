@@ -193,3 +193,41 @@ def test_sharded_ceemdan_gloo_world2(oracle):
         assert np.array_equal(imfs, got[0][0]) and np.array_equal(res, got[0][1])  # every rank identical
         assert imfs.shape == o[0].shape
         assert np.max(np.abs(imfs - o[0])) <= 1e-11 * np.max(np.abs(x))  # stage sums in a different tree
+
+
+# ------------------------------------------------------------------ NCCL id rendezvous (bench / drivers)
+
+def test_init_comm_rendezvous_world2(tmp_path, monkeypatch):
+    """parallel.init_comm: rank 0 publishes the 128-byte NCCL id, the other ranks read the same
+    bytes and every rank joins with its own rank (the C ABI is stood in for by a recorder)."""
+    import threading
+
+    from paper_2106_15319_b200.parallel import init_comm
+    monkeypatch.setenv("SEMD_RDZV_DIR", str(tmp_path))
+    monkeypatch.setenv("SEMD_RDZV_TAG", "t")
+    monkeypatch.setenv("MASTER_PORT", "29555")
+    uid = bytes(range(128))
+    got = {}
+    barrier = threading.Barrier(3)
+
+    class FakeCtx:
+        def __init__(self, rank):
+            self.rank = rank
+
+        @staticmethod
+        def comm_unique_id():
+            return uid
+
+        def comm_init(self, u, rank, world, root):
+            got[self.rank] = (u, rank, world, root)
+
+        def comm_allreduce(self, vals, op="sum"):
+            barrier.wait(timeout=30)
+
+    ts = [threading.Thread(target=init_comm, args=(FakeCtx(r), r, 3, 0)) for r in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=60)
+    assert got == {r: (uid, r, 3, 0) for r in range(3)}
+    assert not list(tmp_path.iterdir())  # rank 0 removed the id file after everyone joined
