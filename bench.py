@@ -67,6 +67,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("SEMD_BENCH_NO_SMI"):  # diagnosis: no sampler process during the timed region
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
                                           "--format=csv,noheader,nounits", "-lms", "200"],

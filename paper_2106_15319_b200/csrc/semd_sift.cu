@@ -161,6 +161,19 @@ __device__ __noinline__ void sd_sums_sequential(const Arena& A, int s, int cur_b
     *den = y;
 }
 
+__device__ __noinline__ void sd_fix_uncertain(const Arena& A, int ne) {
+    for (int li = 0; li < ne; ++li) {
+        Slot& S = A.slots[A.eval_list[li]];
+        if (S.state != ST_SIFT) continue;
+        if (!(A.debug & 4) && !sd_decision_uncertain(S.num, S.den, A.L, A.sd_threshold)) continue;
+        double num, den;
+        sd_sums_sequential(A, A.eval_list[li], S.cb >= 0 ? S.cb : S.xb, &num, &den);  // cb: the candidate sifted
+        S.num = num;
+        S.den = den;
+        atomicAdd(&A.ctrl->sd_rechecks, 1);
+    }
+}
+
 // extract_imf's control flow (emd.cpp:131-151) for one slot after its eval
 // pass; returns 1 when this step's extrema must be compacted.
 __device__ int decide_slot(const Arena& A, int s) {
@@ -207,13 +220,8 @@ __device__ int decide_slot(const Arena& A, int s) {
     if (state == ST_SIFT) {
         S.iter += 1;
         S.sifted += A.L;
-        const int cur_buf = S.cb >= 0 ? S.cb : S.xb;  // the candidate this step sifted
         S.cb = S.db;
-        double num = S.num, den = S.den;
-        if ((A.debug & 4) || sd_decision_uncertain(num, den, A.L, A.sd_threshold)) {
-            sd_sums_sequential(A, s, cur_buf, &num, &den);
-            atomicAdd(&A.ctrl->sd_rechecks, 1);
-        }
+        const double num = S.num, den = S.den;  // reference-order sums when uncertified (sd_fix_uncertain)
         bool stop = (den == 0.0 || num / den < A.sd_threshold) || S.iter >= A.max_sift_iters;
         if (!stop) {
             S.trace_iter = S.iter;
@@ -264,6 +272,17 @@ __device__ void decide_after_eval(const Arena& A) {
         }
     }
     __syncthreads();
+    // SD tests too close to the threshold to certify get the reference's sequential sums first
+    // (cold path: one thread, out of line, so the decision loop below keeps its registers)
+    int unc = 0;
+    for (int li = threadIdx.x; li < ne; li += blockDim.x) {
+        const Slot& S = A.slots[A.eval_list[li]];
+        if (S.state == ST_SIFT && ((A.debug & 4) || sd_decision_uncertain(S.num, S.den, A.L, A.sd_threshold))) unc = 1;
+    }
+    if (__syncthreads_or(unc)) {
+        if (threadIdx.x == 0) sd_fix_uncertain(A, ne);
+        __syncthreads();
+    }
     const int per = (ne + blockDim.x - 1) / blockDim.x;
     const int l0 = min(ne, (int)threadIdx.x * per), l1 = min(ne, l0 + per);
     int flags = 0, cnt = 0;  // per <= 32 when G <= 8192
@@ -290,7 +309,7 @@ __host__ __device__ inline int scan_grid(const Arena& A) {
     return scan_by_warp(A) ? (2 * A.G + kScanThreads / 32 - 1) / (kScanThreads / 32) : 2 * A.G * A.chunks;
 }
 
-__global__ void __launch_bounds__(kScanThreads, 5) k_scan(Arena A) {
+__global__ void __launch_bounds__(kScanThreads) k_scan(Arena A) {
     pdl_begin();
     if (A.ctrl->finished) return;  // a step launched past the run's end
     const int kstep_ = A.ctrl->step;
