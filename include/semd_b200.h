@@ -87,6 +87,7 @@ typedef struct semd_stats {
     uint64_t eval_launches;
     uint64_t sd_rechecks;    /* SD stop tests whose tree-summed ratio was too close to sd_threshold to certify
                                 and were redone with the reference's sequential sums */
+    uint64_t resident_jobs;  /* jobs run by the resident (one CTA per job, shared-memory) engine */
 } semd_stats;
 
 typedef struct semd_ctx semd_ctx;
@@ -102,6 +103,16 @@ int semd_set_stream(semd_ctx* ctx, void* cuda_stream);
 int semd_set_timing(semd_ctx* ctx, int enable);
 /* Maximum concurrent sift jobs (0 = automatic from L and memory). */
 int semd_set_max_slots(semd_ctx* ctx, int slots);
+/* Sift engine: SEMD_ENGINE_AUTO (default; the SEMD_ENGINE environment variable "lockstep" /
+ * "resident" overrides it) runs signals of at most SEMD_RESIDENT_MAX_L samples on the resident
+ * engine (one persistent CTA per job, candidate and segment tables in shared memory) and longer
+ * ones on the lockstep engine (G jobs per five-kernel step, state in HBM). Both are bit-identical
+ * to the reference; RESIDENT still falls back to LOCKSTEP for signals it cannot hold. */
+#define SEMD_ENGINE_AUTO 0
+#define SEMD_ENGINE_LOCKSTEP 1
+#define SEMD_ENGINE_RESIDENT 2
+#define SEMD_RESIDENT_MAX_L 8188
+int semd_set_engine(semd_ctx* ctx, int engine);
 
 /* ---- emd.hpp ---------------------------------------------------------- */
 /* emd.hpp:41 find_extrema (emd.cpp:10-35). Arrays hold up to n entries. */

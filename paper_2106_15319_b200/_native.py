@@ -52,7 +52,7 @@ class Stats(C.Structure):
     _fields_ = [("sifted_samples", C.c_uint64), ("sift_iterations", C.c_uint64), ("steps", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("solve_hazards", C.c_uint64), ("slots", C.c_int32),
                 ("waves", C.c_int32), ("eval_ms", C.c_double), ("eval_launches", C.c_uint64),
-                ("sd_rechecks", C.c_uint64)]
+                ("sd_rechecks", C.c_uint64), ("resident_jobs", C.c_uint64)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/semd_b200.h
@@ -64,6 +64,7 @@ SIGNATURES = {
     "semd_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "semd_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "semd_set_max_slots": (C.c_int, [C.c_void_p, C.c_int]),
+    "semd_set_engine": (C.c_int, [C.c_void_p, C.c_int]),
     "semd_find_extrema": (C.c_int, [C.c_void_p, _dp, C.c_size_t, _szp, _dp, _szp, _szp, _dp, _szp]),
     "semd_envelope": (C.c_int, [C.c_void_p, _szp, _dp, C.c_size_t, C.c_size_t, _dp]),
     "semd_extract_imf": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.POINTER(SiftCfg), _dp, _i32p]),
@@ -131,6 +132,7 @@ SIGNATURES = {
 EXTRA = {"semd_set_noise_override": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_size_t]),
          "semd_set_debug": (C.c_int, [C.c_void_p, C.c_int]),
          "semd_solve_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+         "semd_resident_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
          "semd_kernel_spans": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
          "semd_hazard_log": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
          "semd_mt19937_64_device_test": (C.c_int, [C.c_void_p, C.c_uint64, C.c_size_t, C.POINTER(C.c_uint64)])}

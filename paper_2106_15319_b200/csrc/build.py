@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 LIB = os.path.join(PKG, "libsemd_b200.so")
-SRCS = ["semd_eval.cu", "semd_sift.cu", "semd_aux.cu", "semd_capi.cu"]
+SRCS = ["semd_eval.cu", "semd_sift.cu", "semd_aux.cu", "semd_resident.cu", "semd_capi.cu"]
 HDRS = ["semd_types.cuh", "semd_device.cuh", "semd_launch.h", "semd_libm.cuh", "semd_libm_tables.h", "semd_libm.cuh", "semd_libm_tables.h", os.path.join("..", "..", "include", "semd_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # -fmad=false: the sift arithmetic must round exactly like the reference's

@@ -522,6 +522,186 @@ struct semd_ctx {
         return (int)std::min<long long>((long long)(A.kcap + 2) * it + 64, 1LL << 30);
     }
 
+    // ---- the resident engine (semd_resident.cu): short signals, one persistent CTA per job ----
+    int engine = SEMD_ENGINE_AUTO;
+    DBuf r_jobs, r_res, r_store, r_sifts, r_scratch, r_ticket, r_noise, r_prof;
+    bool r_prof_init = false;
+    cudaEvent_t r_t0 = nullptr, r_t1 = nullptr;  // SEMD_RES_LOG timing
+    std::vector<semd::dev::RResult> r_out;
+    static int env_engine() {
+        static const int v = [] {
+            const char* e = std::getenv("SEMD_ENGINE");
+            if (e && std::strcmp(e, "lockstep") == 0) return (int)SEMD_ENGINE_LOCKSTEP;
+            if (e && std::strcmp(e, "resident") == 0) return (int)SEMD_ENGINE_RESIDENT;
+            return (int)SEMD_ENGINE_AUTO;
+        }();
+        return v;
+    }
+    // segment-table rows (16 B) the resident kernel's shared memory holds next to a length-L candidate
+    static int res_tab_rows(long long L) {
+        const long long fixed = (long long)semd::dev::resident_smem_bytes((int)L, 0);
+        return (int)std::max(0LL, ((long long)semd::dev::resident_max_smem() - fixed) / 16);
+    }
+    bool resident_for(long long L) const {
+        const int mode = engine != SEMD_ENGINE_AUTO ? engine : env_engine();
+        if (mode == SEMD_ENGINE_LOCKSTEP) return false;
+        if (L < 4 || L > semd::dev::kResMaxL) return false;
+        return res_tab_rows(L) >= 64;
+    }
+    static Slot slot_from(const semd::dev::RResult& r) {
+        Slot S{};
+        S.k = r.k;
+        S.ended_insufficient = r.ended_insufficient;
+        S.n[0] = r.n0;
+        S.n[1] = r.n1;
+        S.sifted = r.sifted;
+        S.state = semd::dev::ST_DONE;
+        return S;
+    }
+    // All jobs in one launch of the resident engine (the arena must be configured for L: its sums,
+    // trace and control block are used). write_imf jobs keep up to kc IMFs each, accumulated into
+    // A.sums in job order afterwards (k_res_accum); job 0's sift counts go to A.imf_sifts and its
+    // final residue to res_final0. Results per job in r_out. Jobs whose segment tables outgrow the
+    // shared memory are listed in *failed; when one of them accumulates IMFs nothing is accumulated
+    // and false is returned (the caller reruns the whole call on the lockstep engine, keeping the
+    // realization order of the sums).
+    bool run_resident(const std::vector<JobSpec>& js, int kc, std::vector<int>* failed, double* res_final0 = nullptr) {
+        using namespace semd::dev;
+        failed->clear();
+        ensure_pin(A.G);
+        const int nj = (int)js.size();
+        const int L = A.L;
+        const long long Lp = (L + 3) & ~3;
+        std::vector<RJob> h(nj);
+        bool any_write = false;
+        for (int i = 0; i < nj; ++i) {
+            const JobSpec& J = js[i];
+            RJob R{};
+            R.m = J.m;
+            R.task = J.task;
+            R.k = J.k;
+            R.kmax = J.kmax;
+            R.k0 = J.k0;
+            R.init_kind = J.init_kind;
+            R.write_imf = J.write_imf;
+            R.detect_only = J.detect_only;
+            R.beta = J.beta;
+            R.a = J.a;
+            R.b = J.b;
+            R.imf_out = J.imf_out;
+            R.res_out = J.res_out;
+            R.res_final = i == 0 ? res_final0 : nullptr;
+            h[i] = R;
+            any_write = any_write || (J.write_imf && !J.detect_only);
+        }
+        kc = std::max(1, kc);
+        const int grid = std::max(1, std::min(nj, sms));
+        r_jobs.alloc((size_t)nj * sizeof(RJob));
+        r_res.alloc((size_t)nj * sizeof(RResult));
+        r_sifts.alloc((size_t)nj * kc * 4);
+        if (any_write) r_store.alloc((size_t)nj * kc * Lp * 8);
+        r_scratch.alloc((size_t)grid * 2 * Lp * 8);
+        r_ticket.alloc(16);
+        ck(cudaMemcpyAsync(r_jobs.p, h.data(), (size_t)nj * sizeof(RJob), cudaMemcpyHostToDevice, stream), "jobs");
+        ck(cudaMemsetAsync(r_ticket.p, 0, 16, stream), "ticket");
+        ResArgs P{};
+        P.jobs = r_jobs.as<RJob>();
+        P.res = r_res.as<RResult>();
+        P.njobs = nj;
+        P.L = L;
+        P.store = any_write ? r_store.as<double>() : nullptr;
+        P.kc = kc;
+        P.sifts = r_sifts.as<int>();
+        P.scratch = r_scratch.as<double>();
+        P.ticket = r_ticket.as<unsigned>();
+        P.max_iters = A.max_sift_iters;
+        P.sd_thr = A.sd_threshold;
+        P.tab_rows = res_tab_rows(L);
+        P.trace = A.trace_cap > 0 ? A.trace : nullptr;
+        P.trace_cap = A.trace_cap;
+        P.trace_count = &A.ctrl->trace_count;
+        P.sd_rechecks = &A.ctrl->sd_rechecks;
+        P.debug = debug_flags;
+        if (debug_flags & 2) {
+            r_prof.alloc(64);
+            if (!r_prof_init) {
+                ck(cudaMemsetAsync(r_prof.p, 0, 64, stream), "prof");
+                r_prof_init = true;
+            }
+            P.prof = r_prof.as<unsigned long long>();
+        }
+        static const bool res_log = std::getenv("SEMD_RES_LOG") != nullptr;
+        if (res_log && !r_t0) {
+            ck(cudaEventCreate(&r_t0), "event");
+            ck(cudaEventCreate(&r_t1), "event");
+        }
+        if (res_log) ck(cudaEventRecord(r_t0, stream), "ev");
+        launch_resident(P, grid, stream);
+        ck(cudaGetLastError(), "resident launch");
+        if (res_log) ck(cudaEventRecord(r_t1, stream), "ev");
+        r_out.resize(nj);
+        ck(cudaMemcpyAsync(r_out.data(), r_res.p, (size_t)nj * sizeof(RResult), cudaMemcpyDeviceToHost, stream),
+           "resident results");
+        ck(cudaStreamSynchronize(stream), "resident run");  // also keeps h alive for the upload
+        if (res_log) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r_t0, r_t1);
+            long long sifts = 0;
+            int maxs = 0;
+            for (int i = 0; i < nj; ++i) {
+                sifts += r_out[i].sifted / std::max(1, L);
+                maxs = std::max(maxs, (int)(r_out[i].sifted / std::max(1, L)));
+            }
+            std::fprintf(stderr, "[resident] jobs %d task %d L %d: %.3f ms, sifts %lld (max per job %d)\n", nj,
+                         js[0].task, L, ms, sifts, maxs);
+        }
+        bool fail_write = false, overflow = false;
+        for (int i = 0; i < nj; ++i) {
+            if (r_out[i].smem_overflow) {
+                failed->push_back(i);
+                fail_write = fail_write || (h[i].write_imf && !h[i].detect_only);
+            }
+            overflow = overflow || r_out[i].k_overflow;
+        }
+        if (fail_write || overflow) {  // nothing of this run is kept (its traces neither)
+            ck(cudaMemcpyAsync(A.ctrl, pin_reset_ctrl(), sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
+            ck(cudaStreamSynchronize(stream), "ctrl reset");
+            if (overflow && !fail_write) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", kc);
+            return false;
+        }
+        if (any_write)
+            launch_res_accum(P.jobs, P.res, nj, P.store, kc, Lp, L, A.sums, A.kcap, stream);
+        if (A.imf_sifts && js[0].write_imf && !js[0].detect_only) {
+            const int base = js[0].k0 + js[0].k;
+            const int cnt = std::min(r_out[0].produced, std::max(0, A.kcap - base));
+            if (cnt > 0)
+                ck(cudaMemcpyAsync(A.imf_sifts + base, r_sifts.p, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, stream),
+                   "sift counts");
+        }
+        ck(cudaGetLastError(), "resident accumulate");
+        Ctrl c;
+        ck(cudaMemcpyAsync(pin_jobs, A.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream), "ctrl");
+        ck(cudaStreamSynchronize(stream), "resident");
+        std::memcpy(&c, pin_jobs, sizeof(Ctrl));
+        for (int i = 0; i < nj; ++i) {
+            stats.sifted_samples += (uint64_t)r_out[i].sifted;
+            stats.sift_iterations += (uint64_t)(r_out[i].sifted / std::max(1, L));
+            stats.solve_hazards += (uint64_t)r_out[i].hazards;
+        }
+        stats.resident_jobs += (uint64_t)nj;
+        stats.sd_rechecks += (uint64_t)c.sd_rechecks;
+        if (A.trace) {
+            const int n = std::min(c.trace_count, A.trace_cap);
+            const size_t old = h_trace.size();
+            h_trace.resize(old + n);
+            if (n) ck(cudaMemcpy(h_trace.data() + old, A.trace, (size_t)n * sizeof(TraceRec), cudaMemcpyDeviceToHost),
+                      "trace");
+            trace_total += c.trace_count;
+        }
+        ck(cudaMemcpyAsync(A.ctrl, pin_reset_ctrl(), sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
+        return true;
+    }
+
     unsigned long long launches_at_reset = 0;
     void reset_stats(int slots_used) {
         stats = semd_stats{};
@@ -609,8 +789,17 @@ struct semd_ctx {
             J.a = d_x;
             h_trace.clear();
             trace_total = 0;
-            set_jobs({J});
             try {
+                if (resident_for(n)) {
+                    std::vector<int> failed;
+                    if (run_resident({J}, kcap, &failed, buf(0, 0))) {
+                        h_slots[0] = slot_from(r_out[0]);
+                        h_slots[0].xb = 0;
+                        return h_slots[0].k;
+                    }
+                    fill_sums(kcap, -0.0);  // the tables outgrew the resident engine: lockstep below
+                }
+                set_jobs({J});
                 run(max_steps_for(cfg));
             } catch (const Error& e) {
                 if (e.code == SEMD_CAPACITY && attempt < 3 && cfg.max_imfs == 0) {
@@ -676,9 +865,10 @@ struct semd_ctx {
         };
         int kcap = default_kcap(n, cfg.max_imfs);
         const long long Ls = (n + 1) / 2 * 2;
+        const bool res = jobs > 0 && resident_for(n);
         // the first wave's noise (side stream) overlaps the sequential std on the main stream
         bool first_noise_ready = false;
-        if (!noise_override && jobs > 0) {
+        if (!noise_override && jobs > 0 && !res) {
             int fw0, fg;
             wave(0, fw0, fg);
             noise.alloc((size_t)2 * G * Ls * 8);
@@ -713,6 +903,38 @@ struct semd_ctx {
                 ck(cudaEventRecord(noise_ready[b], rng_stream), "rng event");
             };
             try {
+                if (res) {  // every realization in one resident-engine launch, summed in m order
+                    if (!noise_override) {
+                        r_noise.alloc((size_t)jobs * Ls * 8);
+                        semd::dev::launch_rng_ensemble(ens.base_seed, m_begin, jobs,
+                                                       reinterpret_cast<uint64_t*>(r_noise.as<double>()), Ls, n,
+                                                       stream);
+                        semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(r_noise.as<double>()),
+                                                     (long long)jobs * Ls, 1.0, stream);
+                        ck(cudaGetLastError(), "rng");
+                    }
+                    std::vector<JobSpec> js(jobs);
+                    for (int i = 0; i < jobs; ++i) {
+                        JobSpec& J = js[i];
+                        J.m = m_begin + i;
+                        J.task = 0;
+                        J.kmax = cfg.max_imfs;
+                        J.init_kind = 1;
+                        J.beta = beta;
+                        J.a = d_x;
+                        J.b = noise_override ? noise_override + (size_t)(m_begin + i) * n
+                                             : r_noise.as<double>() + (size_t)i * Ls;
+                    }
+                    std::vector<int> failed;
+                    if (run_resident(js, kcap, &failed)) {
+                        for (int i = 0; i < jobs; ++i) kmax_seen = std::max(kmax_seen, r_out[i].k);
+                        stats.waves += 1;
+                        stats.slots = std::min(jobs, sms);
+                        return kmax_seen;
+                    }
+                    fill_sums(kcap, 0.0);  // the tables outgrew the resident engine: lockstep waves below
+                    if (!noise_override) make_noise(0, 0), first_noise_ready = true;
+                }
                 if (!noise_override && !first_noise_ready && W > 0) make_noise(0, 0);
                 first_noise_ready = false;  // a capacity retry regenerates it
                 for (int wi = 0; wi < W; ++wi) {
@@ -820,6 +1042,25 @@ struct semd_ctx {
     }
 
     void cs_run_tasks(std::vector<JobSpec>& all, std::vector<Slot>* results) {
+        results->resize(all.size());
+        if (!all.empty() && resident_for(cs.n)) {
+            std::vector<int> failed;
+            if (run_resident(all, 1, &failed)) {
+                for (size_t i = 0; i < all.size(); ++i) (*results)[i] = slot_from(r_out[i]);
+                cs.waves += 1;
+                if (failed.empty()) return;
+                // jobs whose tables outgrew the shared memory (none of them accumulates): lockstep
+                std::vector<JobSpec> rest;
+                for (int i : failed) rest.push_back(all[i]);
+                std::vector<Slot> rr;
+                cs_run_lockstep(rest, &rr);
+                for (size_t q = 0; q < failed.size(); ++q) (*results)[failed[q]] = rr[q];
+                return;
+            }
+        }
+        cs_run_lockstep(all, results);
+    }
+    void cs_run_lockstep(std::vector<JobSpec>& all, std::vector<Slot>* results) {
         results->resize(all.size());
         for (size_t w0 = 0; w0 < all.size(); w0 += cs.G) {
             const size_t g = std::min<size_t>(cs.G, all.size() - w0);
@@ -1387,6 +1628,14 @@ int semd_set_max_slots(semd_ctx* ctx, int slots) {
     });
 }
 
+int semd_set_engine(semd_ctx* ctx, int engine) {
+    return guard([&] {
+        need_ctx(ctx);
+        if (engine < SEMD_ENGINE_AUTO || engine > SEMD_ENGINE_RESIDENT) raise(SEMD_INVALID_INPUT, "unknown engine %d", engine);
+        ctx->engine = engine;
+    });
+}
+
 // Test hook: nr x n host noise used instead of the device RNG (NULL clears).
 int semd_set_noise_override(semd_ctx* ctx, const double* noise, size_t nr, size_t n) {
     return guard([&] {
@@ -1457,6 +1706,17 @@ int semd_set_debug(semd_ctx* ctx, int flags) {
         need_ctx(ctx);
         ctx->debug_flags = flags;
         ctx->A.debug = flags;
+    });
+}
+
+// Dev hook: the resident engine's per-phase SM cycles (debug bit 1), 8 u64; reset after reading.
+int semd_resident_profile(semd_ctx* ctx, uint64_t* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        for (int i = 0; i < 8; ++i) out[i] = 0;
+        if (!ctx->r_prof_init) return;
+        ck(cudaMemcpy(out, ctx->r_prof.p, 64, cudaMemcpyDeviceToHost), "prof");
+        ck(cudaMemset(ctx->r_prof.p, 0, 64), "prof");
     });
 }
 

@@ -43,6 +43,19 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+// The SD stop test's certification (emd.cpp:142-150): the engines sum num/den in a fixed tree,
+// the reference left to right; true when the threshold lies inside the interval the rounding
+// bounds allow for the reference's ratio (see semd_sift.cu).
+__device__ __forceinline__ bool sd_decision_uncertain(double num, double den, long long n, double thr) {
+    if (!(den > 0.0)) return false;  // den == 0 exactly when every cur^2 term is 0: the same in any order
+    const double u = 0x1p-53;
+    const double g = (double)n * u / (1.0 - (double)n * u);
+    const double e = 2.0 * g / (1.0 - g) * 1.0001;
+    const double lo = (num * (1.0 - e)) / (den * (1.0 + e)) * (1.0 - 8.0 * u);
+    const double hi = (num * (1.0 + e)) / (den * (1.0 - e)) * (1.0 + 8.0 * u);
+    return lo <= thr && thr <= hi;
+}
+
 // Mirrored knot v of a sift envelope (emd.cpp:107-122; both mirrors present in
 // sifting because extrema never sit on an end): v=0,1 left mirrors, 2..n+1
 // the extrema, n+2 and n+3 the (non-monotone) right mirrors.

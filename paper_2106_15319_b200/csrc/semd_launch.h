@@ -54,5 +54,48 @@ void launch_slicewise_finish(const double* x, const double* sums, int kc, long l
                              cudaStream_t st);
 void launch_axpy(const double* a, const double* b, double beta, double* out, long long n, cudaStream_t st);
 
+
+// ---- the resident engine (semd_resident.cu): one CTA per job for short signals
+constexpr int kResThreads = 512;
+constexpr int kResMaxL = 8188;  // longest signal (samples) the resident engine takes
+struct RJob {  // one job = JobSpec of the host driver (emd / EEMD realization / CEEMDAN task)
+    int m, task, k, kmax, k0, init_kind, write_imf, detect_only;
+    double beta;
+    const double* a;
+    const double* b;
+    double* imf_out;    // every IMF also written here (single-IMF CEEMDAN noise tasks)
+    double* res_out;    // every residue also written here
+    double* res_final;  // the job's final residue
+};
+struct RResult {
+    int k, produced, ended_insufficient, smem_overflow, k_overflow, hazards;
+    unsigned n0, n1;
+    long long sifted;
+};
+struct ResArgs {
+    const RJob* jobs;
+    RResult* res;
+    int njobs, L;
+    double* store;     // [njobs][kc][Lp] IMFs of write_imf jobs (accumulated in job order afterwards)
+    int kc;            // IMF rows per job
+    int* sifts;        // [njobs][kc] sift count of every produced IMF
+    double* scratch;   // [grid][2][Lp] per-CTA residue and pre-sift candidate
+    unsigned* ticket;  // job queue
+    int max_iters;
+    double sd_thr;
+    int tab_rows;      // shared-memory segment-table capacity (16-byte rows)
+    TraceRec* trace;
+    int trace_cap;
+    int* trace_count;
+    int* sd_rechecks;
+    int debug;         // bit 2: every SD decision by the sequential sums; bit 1: phase cycle profile
+    unsigned long long* prof;  // [8] SM cycles per phase (debug bit 1): detect, tables, solve, eval, sums, final, init
+};
+size_t resident_smem_bytes(int L, int rows);
+int resident_max_smem();
+void launch_resident(const ResArgs& P, int grid, cudaStream_t st);
+void launch_res_accum(const RJob* jobs, const RResult* res, int njobs, const double* store, int kc, long long Lp,
+                      int L, double* sums, int rows, cudaStream_t st);
+
 }  // namespace dev
 }  // namespace semd

@@ -123,15 +123,6 @@ __device__ void build_lists(const Arena& A, bool allow_final) {
 // and each within 2g/(1-g) (relative) of the other. The decision num/den < sd_threshold is
 // certified when the threshold lies outside the interval those bounds allow for the reference's
 // ratio; otherwise the slot's sums are redone in the reference's order before deciding.
-__device__ bool sd_decision_uncertain(double num, double den, long long n, double thr) {
-    if (!(den > 0.0)) return false;  // den == 0 exactly when every cur^2 term is 0: the same in any order
-    const double u = 0x1p-53;
-    const double g = (double)n * u / (1.0 - (double)n * u);
-    const double e = 2.0 * g / (1.0 - g) * 1.0001;
-    const double lo = (num * (1.0 - e)) / (den * (1.0 + e)) * (1.0 - 8.0 * u);
-    const double hi = (num * (1.0 + e)) / (den * (1.0 - e)) * (1.0 + 8.0 * u);
-    return lo <= thr && thr <= hi;
-}
 
 // The reference's own loop, emd.cpp:142-148 (num += mean*mean, den += cur*cur, t = 0..L-1), over
 // this iteration's envelopes (the segment tables of the step's solve, the reference's segment

@@ -1,0 +1,122 @@
+"""The resident engine (semd_resident.cu: one persistent CTA per job, candidate and segment tables
+in shared memory) against the lockstep engine, the oracle and the reference's golden data.
+
+The default engine choice sends signals of at most SEMD_RESIDENT_MAX_L samples to the resident
+engine, so the C1-C3 golden tests in test_gpu_parity.py already run on it; here both engines are
+forced and compared bit for bit, the repair paths are forced, and the shared-memory overflow
+fallback is exercised."""
+import numpy as np
+import pytest
+
+from tests.conftest import sort_trace
+from tests.golden.inputs import rng_signal
+
+pytestmark = pytest.mark.gpu
+
+AUTO, LOCKSTEP, RESIDENT = 0, 1, 2
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.int64)
+
+
+def run(se, engine, x, algo, debug=0, **kw):
+    c = se.context()
+    c.check(c.lib.semd_set_engine(c.ptr, engine))
+    c.check(c.lib.semd_set_debug(c.ptr, debug))
+    try:
+        return se.decompose_full(x, algo, trace_cap=200000, **kw)
+    finally:
+        c.check(c.lib.semd_set_debug(c.ptr, 0))
+        c.check(c.lib.semd_set_engine(c.ptr, AUTO))
+
+
+def same(a, b):
+    assert a["imfs"].shape == b["imfs"].shape
+    assert np.array_equal(bits(a["imfs"]), bits(b["imfs"]))
+    assert np.array_equal(bits(a["residue"]), bits(b["residue"]))
+    assert np.array_equal(sort_trace(a["trace"]), sort_trace(b["trace"]))
+
+
+def pickup(se, D=50):
+    from paper_2106_15319_b200 import workloads as W
+    return se.concatenate(W.pickup_signals(), D)
+
+
+@pytest.mark.parametrize("algo,kw", [("emd", dict(max_sift_iters=1000)),
+                                     ("eemd", dict(max_sift_iters=300, max_imfs=10, nr=100)),
+                                     ("ceemdan", dict(max_sift_iters=5000, nr=100))])
+def test_resident_equals_lockstep_pickup(se, algo, kw):
+    """C1-C3 inputs: IMFs, residue and the full parity trace bit-identical across the two engines."""
+    s = pickup(se)
+    a = run(se, LOCKSTEP, s, algo, **kw)
+    b = run(se, RESIDENT, s, algo, **kw)
+    assert a["stats"]["resident_jobs"] == 0 and b["stats"]["resident_jobs"] > 0
+    same(a, b)
+    if algo == "emd":
+        assert np.array_equal(a["sift_counts"], b["sift_counts"])
+
+
+def test_resident_emd_vs_oracle_many_lengths(se, oracle):
+    """Plain EMD, bit-exact against the oracle at lengths 4 .. the resident maximum (white noise of
+    8188 samples has ~5.5k extrema: its tables outgrow the shared memory and the call falls back)."""
+    for n in (4, 5, 7, 64, 129, 1000, 3001, 6250, 8188):
+        x = rng_signal(n, n)
+        d = run(se, RESIDENT, x, "emd", max_sift_iters=300)
+        oi, ores, _, otr = oracle.decompose(x, 0, trace_cap=100000)
+        assert d["stats"]["resident_jobs"] == (1 if n <= 6250 else 0), n
+        assert np.array_equal(bits(d["imfs"]), bits(oi)), n
+        assert np.array_equal(bits(d["residue"]), bits(ores)), n
+        assert np.array_equal(sort_trace(d["trace"]), sort_trace(otr)), n
+
+
+def test_resident_plateaus_vs_oracle(se, oracle):
+    """find_extrema's plateau rule (emd.cpp:16-33) inside the resident detection."""
+    rng = np.random.default_rng(7)
+    for n in (300, 2500):
+        x = np.round(rng.standard_normal(n).cumsum() * 2) / 2  # many equal neighbours
+        x[100:140] = x[99]  # one long plateau
+        d = run(se, RESIDENT, x, "emd", max_sift_iters=50)
+        oi, ores, _, otr = oracle.decompose(x, 0, iters=50, trace_cap=100000)
+        assert np.array_equal(bits(d["imfs"]), bits(oi)) and np.array_equal(bits(d["residue"]), bits(ores))
+        assert np.array_equal(sort_trace(d["trace"]), sort_trace(otr))
+
+
+def test_resident_forced_replays_bit_exact(se):
+    """Debug bit 0: two-row warm-ups make the speculative chains disagree at their boundaries; the
+    in-order replay must restore the sequential Thomas result exactly."""
+    s = pickup(se)
+    a = run(se, LOCKSTEP, s, "eemd", max_imfs=10, nr=20)
+    b = run(se, RESIDENT, s, "eemd", debug=1, max_imfs=10, nr=20)
+    assert b["stats"]["solve_hazards"] > 0
+    same(a, b)
+
+
+def test_resident_sd_sequential_path(se):
+    """Debug bit 2: every SD decision redone with the reference's left-to-right sums."""
+    s = pickup(se)
+    a = run(se, LOCKSTEP, s, "emd", max_sift_iters=1000)
+    b = run(se, RESIDENT, s, "emd", debug=4, max_sift_iters=1000)
+    assert b["stats"]["sd_rechecks"] == b["stats"]["sift_iterations"] > 0
+    same(a, b)
+
+
+def test_resident_smem_overflow_falls_back(se, oracle):
+    """Segment tables larger than the shared memory (every sample an extremum) rerun the call on the
+    lockstep engine; the result is still the reference's."""
+    n = 8188
+    x = np.where(np.arange(n) % 2 == 0, 1.0, -1.0) + np.arange(n) * 1e-6
+    d = run(se, RESIDENT, x, "emd", max_sift_iters=20)
+    oi, ores, _, otr = oracle.decompose(x, 0, iters=20, trace_cap=100000)
+    assert np.array_equal(bits(d["imfs"]), bits(oi)) and np.array_equal(bits(d["residue"]), bits(ores))
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(otr))
+    assert d["stats"]["steps"] > 0  # the lockstep engine ran
+
+
+def test_resident_ceemdan_vs_oracle(se, oracle):
+    """CEEMDAN task jobs (noise modes in place, first modes accumulated in realization order)."""
+    s = pickup(se)[:3000]
+    d = run(se, RESIDENT, s, "ceemdan", max_sift_iters=300, nr=16)
+    oi, ores, _, otr = oracle.decompose(s, 2, nr=16, trace_cap=200000)
+    assert np.array_equal(bits(d["imfs"]), bits(oi)) and np.array_equal(bits(d["residue"]), bits(ores))
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(otr))
