@@ -527,6 +527,14 @@ void launch_envelope_knots(const unsigned long long* idx, const double* val, lon
     k_envelope_knots<<<grid_for(n + 4), 256, 0, st>>>(idx, val, n, length, xs, ys);
     count_launches(1);
 }
+__global__ void k_fill_i32(int* p, long long n, int v) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+void launch_fill_i32(int* p, long long n, int v, cudaStream_t st) {
+    k_fill_i32<<<(unsigned)std::min<long long>((n + 255) / 256, 1024), 256, 0, st>>>(p, n, v);
+    count_launches(1);
+}
 void launch_fill(double* p, long long n, double v, cudaStream_t st) { k_fill<<<grid_for(n), 256, 0, st>>>(p, n, v); }
 void launch_copy(const double* src, double* dst, long long n, cudaStream_t st) {
     k_copy<<<grid_for(n), 256, 0, st>>>(src, dst, n);

@@ -542,6 +542,13 @@ struct semd_ctx {
         const long long fixed = (long long)semd::dev::resident_smem_bytes((int)L, 0);
         return (int)std::max(0LL, ((long long)semd::dev::resident_max_smem() - fixed) / 16);
     }
+    static int res_chain_div() {
+        static const int v = [] {
+            const char* e = std::getenv("SEMD_RES_CHAINS");
+            return e ? std::atoi(e) : 0;
+        }();
+        return v;
+    }
     bool resident_for(long long L) const {
         const int mode = engine != SEMD_ENGINE_AUTO ? engine : env_engine();
         if (mode == SEMD_ENGINE_LOCKSTEP) return false;
@@ -622,10 +629,11 @@ struct semd_ctx {
         P.trace_count = &A.ctrl->trace_count;
         P.sd_rechecks = &A.ctrl->sd_rechecks;
         P.debug = debug_flags;
+        P.chain_div = res_chain_div();
         if (debug_flags & 2) {
-            r_prof.alloc(64);
+            r_prof.alloc(128);
             if (!r_prof_init) {
-                ck(cudaMemsetAsync(r_prof.p, 0, 64, stream), "prof");
+                ck(cudaMemsetAsync(r_prof.p, 0, 128, stream), "prof");
                 r_prof_init = true;
             }
             P.prof = r_prof.as<unsigned long long>();
@@ -1179,6 +1187,102 @@ struct semd_ctx {
         }
     }
 
+    // The whole CEEMDAN in one cooperative launch of the resident engine (single GPU): stages,
+    // ordered stage means, residue checks and beta_K on the device, no host round trip. False
+    // (nothing produced) when it cannot run or a stage outgrew it; the caller then runs the
+    // per-stage drivers.
+    DBuf ce_e1, ce_ok, ce_alive, ce_ctl;
+    bool ceemdan_fused(const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens,
+                       semd_trace* tr) {
+        using namespace semd::dev;
+        ceemdan_begin(d_x, n, cfg, ens, 0, ens.nr, tr);
+        const int nr = ens.nr;
+        const long long Lp = (n + 3) & ~3LL;
+        ce_e1.alloc((size_t)nr * Lp * 8);
+        ce_ok.alloc((size_t)nr * 4);
+        ce_alive.alloc((size_t)nr * 4);
+        ce_ctl.alloc(sizeof(CeeCtl));
+        semd::dev::launch_fill_i32(ce_alive.as<int>(), nr, 1, stream);
+        ck(cudaMemsetAsync(ce_ctl.p, 0, sizeof(CeeCtl), stream), "ctl");
+        const int grid = std::max(1, std::min(nr, sms));
+        r_scratch.alloc((size_t)grid * 2 * Lp * 8);
+        ensure_pin(A.G);
+        ResArgs P{};
+        P.L = (int)n;
+        P.scratch = r_scratch.as<double>();
+        P.max_iters = A.max_sift_iters;
+        P.sd_thr = A.sd_threshold;
+        P.tab_rows = res_tab_rows(n);
+        P.trace = A.trace_cap > 0 ? A.trace : nullptr;
+        P.trace_cap = A.trace_cap;
+        P.trace_count = &A.ctrl->trace_count;
+        P.sd_rechecks = &A.ctrl->sd_rechecks;
+        P.debug = debug_flags;
+        P.chain_div = res_chain_div();
+        if (debug_flags & 2) {
+            r_prof.alloc(128);
+            if (!r_prof_init) {
+                ck(cudaMemsetAsync(r_prof.p, 0, 128, stream), "prof");
+                r_prof_init = true;
+            }
+            P.prof = r_prof.as<unsigned long long>();
+        }
+        CeeArgs Q{};
+        Q.x = d_x;
+        Q.residue = cs_residue();
+        Q.nres = cs_noise();
+        Q.Ls = cs.Ls;
+        Q.e1 = ce_e1.as<double>();
+        Q.e1_ok = ce_ok.as<int>();
+        Q.alive = ce_alive.as<int>();
+        Q.modes = A.sums;
+        Q.kcap = A.kcap;
+        Q.nr = nr;
+        Q.m0 = 0;
+        Q.max_imfs = cfg.max_imfs;
+        Q.nstd = ens.nstd;
+        Q.beta0 = cs.beta0;
+        Q.inv_nr = 1.0 / (double)nr;
+        Q.ctl = ce_ctl.as<CeeCtl>();
+        const cudaError_t e = (cudaError_t)launch_res_ceemdan(P, Q, grid, stream);
+        if (e != cudaSuccess) {  // e.g. the grid cannot be co-resident: per-stage drivers instead
+            cudaGetLastError();
+            cs.active = false;
+            return false;
+        }
+        CeeCtl h{};
+        Ctrl c;
+        ck(cudaMemcpyAsync(&h, ce_ctl.p, sizeof(CeeCtl), cudaMemcpyDeviceToHost, stream), "ceemdan ctl");
+        ck(cudaMemcpyAsync(pin_jobs, A.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream), "ctrl");
+        ck(cudaStreamSynchronize(stream), "ceemdan (resident)");
+        std::memcpy(&c, pin_jobs, sizeof(Ctrl));
+        ck(cudaMemcpyAsync(A.ctrl, pin_reset_ctrl(), sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
+        if (h.status) {  // outgrew the shared memory or the mode rows: rerun per stage (new noise)
+            ck(cudaStreamSynchronize(stream), "ctrl reset");
+            cs.active = false;
+            h_trace.clear();
+            trace_total = 0;
+            return false;
+        }
+        stats.sifted_samples += h.sifted;
+        stats.sift_iterations += h.sifted / (uint64_t)std::max(1LL, n);
+        stats.solve_hazards += (uint64_t)h.hazards;
+        stats.sd_rechecks += (uint64_t)c.sd_rechecks;
+        stats.resident_jobs += (uint64_t)nr * (uint64_t)(h.K + 1);
+        if (A.trace) {
+            const int cnt = std::min(c.trace_count, A.trace_cap);
+            const size_t old = h_trace.size();
+            h_trace.resize(old + cnt);
+            if (cnt)
+                ck(cudaMemcpy(h_trace.data() + old, A.trace, (size_t)cnt * sizeof(TraceRec), cudaMemcpyDeviceToHost),
+                   "trace");
+            trace_total += c.trace_count;
+        }
+        cs.K = h.K;
+        cs.waves += 1;
+        return true;
+    }
+
     // mode_K = total / nr; false (and no update) when check_zero and the mode is all zero.
     bool ceemdan_finish(const double* d_total, int nr, bool check_zero, double* d_mode_out) {
         if (!cs.active) raise(SEMD_INVALID_INPUT, "ceemdan: no active shard (call begin)");
@@ -1207,17 +1311,19 @@ struct semd_ctx {
                        double* out_imfs, int k_cap, double* out_res, semd_trace* tr, int* k_needed) {
         int mb = 0, me = ens.nr;
         if (comm) shard_range(ens.nr, rank, world, &mb, &me);
-        ceemdan_begin(d_x, n, cfg, ens, mb, me, tr);
-        auto stage_total = [&] {
-            ceemdan_stage();
-            comm_sum(A.sums + (size_t)cs.K * n, (size_t)n, false);
-        };
-        stage_total();
-        ceemdan_finish(nullptr, ens.nr, false, nullptr);
-        while (cfg.max_imfs == 0 || cs.K < cfg.max_imfs) {  // emd.cpp:310
-            if (ceemdan_residue_extrema() < 3) break;        // emd.cpp:311
-            stage_total();                                   // grows the IMF rows when needed
-            if (!ceemdan_finish(nullptr, ens.nr, true, nullptr)) break;
+        if (comm || !resident_for(n) || !ceemdan_fused(d_x, n, cfg, ens, tr)) {
+            ceemdan_begin(d_x, n, cfg, ens, mb, me, tr);
+            auto stage_total = [&] {
+                ceemdan_stage();
+                comm_sum(A.sums + (size_t)cs.K * n, (size_t)n, false);
+            };
+            stage_total();
+            ceemdan_finish(nullptr, ens.nr, false, nullptr);
+            while (cfg.max_imfs == 0 || cs.K < cfg.max_imfs) {  // emd.cpp:310
+                if (ceemdan_residue_extrema() < 3) break;        // emd.cpp:311
+                stage_total();                                   // grows the IMF rows when needed
+                if (!ceemdan_finish(nullptr, ens.nr, true, nullptr)) break;
+            }
         }
         const int K = cs.K;
         stats.waves += cs.waves;
@@ -1713,10 +1819,10 @@ int semd_set_debug(semd_ctx* ctx, int flags) {
 int semd_resident_profile(semd_ctx* ctx, uint64_t* out) {
     return guard([&] {
         need_ctx(ctx);
-        for (int i = 0; i < 8; ++i) out[i] = 0;
+        for (int i = 0; i < 16; ++i) out[i] = 0;
         if (!ctx->r_prof_init) return;
-        ck(cudaMemcpy(out, ctx->r_prof.p, 64, cudaMemcpyDeviceToHost), "prof");
-        ck(cudaMemset(ctx->r_prof.p, 0, 64), "prof");
+        ck(cudaMemcpy(out, ctx->r_prof.p, 128, cudaMemcpyDeviceToHost), "prof");
+        ck(cudaMemset(ctx->r_prof.p, 0, 128), "prof");
     });
 }
 

@@ -45,6 +45,7 @@ void launch_sub(double* residue, const double* mode, long long n, cudaStream_t s
 void launch_envelope_knots(const unsigned long long* idx, const double* val, long long n, long long length,
                            double* xs, double* ys, cudaStream_t st);
 void launch_fill(double* p, long long n, double v, cudaStream_t st);
+void launch_fill_i32(int* p, long long n, int v, cudaStream_t st);
 void launch_copy(const double* src, double* dst, long long n, cudaStream_t st);
 void launch_gather(const int* idx, unsigned n, const double* src, double* out, cudaStream_t st);
 void launch_signal_std_batch(const double* x, long long n, int B, double* out, double scale, cudaStream_t st);
@@ -89,11 +90,40 @@ struct ResArgs {
     int* trace_count;
     int* sd_rechecks;
     int debug;         // bit 2: every SD decision by the sequential sums; bit 1: phase cycle profile
-    unsigned long long* prof;  // [8] SM cycles per phase (debug bit 1): detect, tables, solve, eval, sums, final, init
+    int chain_div;     // tuning (SEMD_RES_CHAINS): solve chains per side aimed at (0: default)
+    unsigned long long* prof;  // [16] SM cycles per phase (debug bit 1): detect, tables, solve, eval, sums, final, init, -, solve: rhs, fwd, back, table
 };
 size_t resident_smem_bytes(int L, int rows);
 int resident_max_smem();
 void launch_resident(const ResArgs& P, int grid, cudaStream_t st);
+
+// The whole CEEMDAN (emd.cpp:264-344) in one cooperative launch of the resident engine.
+struct CeeCtl {              // zeroed by the host before the launch
+    unsigned bar_count, bar_gen;  // grid barrier
+    unsigned ticket[64];     // per-stage job queues
+    int beta_stage;          // highest stage whose beta is published
+    int K;                   // modes produced
+    int status;              // 1: segment tables outgrew the shared memory, 2: mode rows exhausted
+    int stop[64];            // per stage: the residue check ended the loop
+    int nonzero[64];         // per stage: the averaged mode has a nonzero sample
+    double beta[64];
+    unsigned long long sifted;
+    int hazards;
+};
+struct CeeArgs {
+    const double* x;     // the signal
+    double* residue;     // running residue (starts as x)
+    double* nres;        // [nr][Ls] noise residues (white noise at the start), updated in place
+    long long Ls;
+    double* e1;          // [nr][Lp] first modes of the stage
+    int* e1_ok;          // [nr] first mode present (0: InsufficientExtrema -> zeros)
+    int* alive;          // [nr] noise still yields modes (emd.cpp:318-324)
+    double* modes;       // [kcap][L] the averaged modes
+    int kcap, nr, m0, max_imfs;
+    double nstd, beta0, inv_nr;
+    CeeCtl* ctl;
+};
+int launch_res_ceemdan(const ResArgs& P, const CeeArgs& Q, int grid, cudaStream_t st);  // cudaError_t
 void launch_res_accum(const RJob* jobs, const RResult* res, int njobs, const double* store, int kc, long long Lp,
                       int L, double* sums, int rows, cudaStream_t st);
 

@@ -35,15 +35,24 @@ namespace dev {
 
 constexpr int kResWarps = kResThreads / 32;
 constexpr int kResChains = kResThreads / 2;  // chains per side (both sides solve concurrently)
-constexpr int kResWarm = 40;                 // speculative warm-up rows of a chain (forward and back)
-constexpr int kResChainMin = 8;              // rows per chain at least (R <= 8 * kResChains uses more chains' worth)
+constexpr int kResWarm = 32;      // speculative warm-up rows of a chain (forward and back), as the lockstep solve
+constexpr int kResChainMin = 8;   // rows per chain at least
+constexpr int kResChainDiv = 96;  // chains per side aimed at: longer chains cost latency, more chains redundant warm-up rows
+
+extern __shared__ __align__(16) unsigned char res_smem[];
+__device__ __forceinline__ double* sm_d(int off) { return reinterpret_cast<double*>(res_smem + off); }
+__device__ __forceinline__ double2* sm_d2(int off) { return reinterpret_cast<double2*>(res_smem + off); }
+__device__ __forceinline__ unsigned short* sm_u16(int off) { return reinterpret_cast<unsigned short*>(res_smem + off); }
+__device__ __forceinline__ unsigned char* sm_u8(int off) { return res_smem + off; }
 
 struct ResShared {
     double red[2][kResWarps];
     int scan[kResWarps];
+    int scan4[4][kResWarps];
     unsigned long long hred[kResWarps];
     int job;
-    int bad;  // bit s: side s's speculative solve disagreed at a chain boundary
+    bool moved[kResThreads];  // solve replay rounds: the chain's end changed
+    int bad;
     int unc;
 };
 
@@ -116,105 +125,188 @@ __device__ __forceinline__ unsigned long long res_sum_u64(unsigned long long v, 
 }
 
 // find_extrema flags of the 4 samples of group g (emd.cpp:16-33): bit k max, bit 4+k min.
-__device__ __forceinline__ unsigned res_group_flags(const double* cur, int L, int g) {
-    unsigned f = 0;
-    const int t0 = 4 * g;
-#pragma unroll
+// The window t0-2 .. t0+5 arrives as four aligned 16-byte loads; each neighbour pair is compared
+// once; samples equal to a neighbour take the reference's plateau rule (rare, out of line).
+__device__ __noinline__ unsigned res_plateau_flags(const double* cur, int L, int t0, unsigned f, unsigned plat) {
     for (int k = 0; k < 4; ++k) {
+        if (!((plat >> k) & 1u)) continue;
         const int t = t0 + k;
-        if (t < 1 || t > L - 2) continue;
-        const double v = cur[t], l = cur[t - 1], r = cur[t + 1];
-        if (v == l || v == r) {  // plateau: the maximal run of samples equal to v, extremum at its middle
-            int rs = t, re = t;
-            while (rs > 0 && cur[rs - 1] == v) --rs;
-            while (re < L - 1 && cur[re + 1] == v) ++re;
-            if (rs > 0 && re < L - 1 && t == (rs + re) / 2) {
-                const double lv = cur[rs - 1], rv = cur[re + 1];
-                if (v > lv && v > rv) f |= 1u << k;
-                else if (v < lv && v < rv) f |= 16u << k;
-            }
-        } else if (v > l && v > r) {
-            f |= 1u << k;
-        } else if (v < l && v < r) {
-            f |= 16u << k;
+        const double v = cur[t];
+        int rs = t, re = t;
+        while (rs > 0 && cur[rs - 1] == v) --rs;
+        while (re < L - 1 && cur[re + 1] == v) ++re;
+        if (rs > 0 && re < L - 1 && t == (rs + re) / 2) {
+            const double lv = cur[rs - 1], rv = cur[re + 1];
+            if (v > lv && v > rv) f |= 1u << k;
+            else if (v < lv && v < rv) f |= 16u << k;
         }
     }
     return f;
 }
+__device__ __forceinline__ unsigned res_group_flags(const double* cur, int L, int g) {
+    const int t0 = 4 * g;
+    double w[8];  // t0-2 .. t0+5 (padding beyond L reads zeros or the next group: masked below)
+    if (t0 >= 4 && t0 + 8 <= ((L + 3) & ~3)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 v = *reinterpret_cast<const double2*>(cur + t0 - 2 + 2 * q);
+            w[2 * q] = v.x;
+            w[2 * q + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int t = t0 - 2 + q;
+            w[q] = t >= 0 && t < L ? cur[t] : 0.0;
+        }
+    }
+    // pair j compares w[j+1] (sample t0-1+j) with w[j+2]
+    unsigned up = 0, dn = 0;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        up |= (unsigned)(w[j + 2] > w[j + 1]) << j;
+        dn |= (unsigned)(w[j + 2] < w[j + 1]) << j;
+    }
+    unsigned inm = 0;  // samples t0 .. t0+3 inside [1, L-2]
+#pragma unroll
+    for (int k = 0; k < 4; ++k) inm |= (unsigned)(t0 + k >= 1 && t0 + k <= L - 2) << k;
+    const unsigned eq = ~(up | dn) & 31u;   // pair j equal (or unordered)
+    unsigned fmax = up & (dn >> 1) & inm;   // v > l (pair k up) and v > r (pair k+1 down)
+    unsigned fmin = dn & (up >> 1) & inm;
+    unsigned f = fmax | (fmin << 4);
+    const unsigned plat = (eq | (eq >> 1)) & inm;  // v == l or v == r
+    if (plat) {
+        // an unordered pair (NaN) is not a plateau: the reference's run logic never extends a run
+        // over NaN and its strict comparisons fail, exactly like the fast path's bits
+        unsigned real = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double v = w[k + 2];
+            real |= (unsigned)(v == w[k + 1] || v == w[k + 3]) << k;
+        }
+        real &= inm;
+        if (real) f = res_plateau_flags(cur, L, t0, f & ~(real | (real << 4)), real);
+    }
+    return f;
+}
 
+// Per-CTA context. Shared-memory arrays are byte offsets into res_smem (pointers rebuilt from the
+// __shared__ symbol keep the compiler on LDS/STS; pointers loaded from this stack struct would
+// be generic loads).
 struct ResCtx {
     const ResArgs* P;
     int L, Lp, NG;
-    double* cur;               // shared: the candidate (in place)
-    unsigned short* pre[2];    // shared: extrema of side s before group g
-    unsigned char* fl;         // shared: group flags
-    double2* tab;              // shared: segment tables (rows {x, y} then {m, 1/h}, side 0 then side 1)
+    int o_cur;                 // double[Lp]: the candidate (in place)
+    int o_pre0, o_pre1;        // ushort[NG]: extrema of side s before group g
+    int o_fl;                  // uchar[NG]: group flags
+    int o_tab;                 // segment tables (rows {x, y} then {m, 1/h}, side 0 then side 1)
     int tab_rows;              // capacity in double2 rows
     double* xg;                // global (this CTA): the IMF input X (the running residue)
     double* oldc;              // global (this CTA): the candidate before the last eval (SD recheck)
     int n[2];                  // extrema counts of the last detection
-    double2 *A[2], *B[2];      // table planes of the current sift
+    int o_A[2], o_B[2];        // table planes of the current sift
     int N[2];
 };
 
 // find_extrema over the candidate: group flags and prefix counts; returns the trace hash (when
 // tracing) = sum over extrema of knot_hash(side, rank, index), the lockstep engine's definition.
-__device__ unsigned long long res_detect(ResCtx& C, ResShared& sh, bool tracing) {
-    int base0 = 0, base1 = 0;
+__device__ __forceinline__ unsigned long long res_detect(ResCtx& C, ResShared& sh, bool tracing) {
+    const double* const cur = sm_d(C.o_cur);
+    unsigned short* const pre0 = sm_u16(C.o_pre0);
+    unsigned short* const pre1 = sm_u16(C.o_pre1);
+    unsigned char* const fl = sm_u8(C.o_fl);
+    const int NG = C.NG, L = C.L;
+    static_assert(kResMaxL <= 4 * 4 * kResThreads, "at most four groups per thread");
+    // group g = i * kResThreads + tid, i < 4: flags and packed counts (max | min << 16) per round
+    unsigned f[4];
+    int cnt[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int g = i * kResThreads + (int)threadIdx.x;
+        f[i] = g < NG ? res_group_flags(cur, L, g) : 0u;
+        cnt[i] = __popc(f[i] & 15u) | (__popc(f[i] >> 4) << 16);
+    }
+    // one block scan of the four rounds at once: within-round exclusive prefixes + round totals
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) incl[i] = cnt[i];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int y = __shfl_up_sync(0xffffffffu, incl[i], o);
+            if (lane >= o) incl[i] += y;
+        }
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sh.scan4[i][wid] = incl[i];
+    }
+    __syncthreads();
+    if (wid < 4) {  // warp i scans round i's warp totals
+        int x = lane < kResWarps ? sh.scan4[wid][lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane < kResWarps) sh.scan4[wid][lane] = x;
+    }
+    __syncthreads();
+    int base = 0;  // packed running total of the earlier rounds
     unsigned long long h = 0;
-    for (int g0 = 0; g0 < C.NG; g0 += kResThreads) {
-        const int g = g0 + (int)threadIdx.x;
-        const unsigned f = g < C.NG ? res_group_flags(C.cur, C.L, g) : 0u;
-        const int c = __popc(f & 15u) | (__popc(f >> 4) << 16);
-        int tot;
-        const int ex = res_excl_scan(c, &tot, sh);
-        if (g < C.NG) {
-            const int r0 = base0 + (ex & 0xFFFF), r1 = base1 + (ex >> 16);
-            C.pre[0][g] = (unsigned short)r0;
-            C.pre[1][g] = (unsigned short)r1;
-            C.fl[g] = (unsigned char)f;
-            if (tracing && f) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int g = i * kResThreads + (int)threadIdx.x;
+        const int ex = base + (wid ? sh.scan4[i][wid - 1] : 0) + incl[i] - cnt[i];
+        if (g < NG) {
+            const int r0 = ex & 0xFFFF, r1 = ex >> 16;
+            pre0[g] = (unsigned short)r0;
+            pre1[g] = (unsigned short)r1;
+            fl[g] = (unsigned char)f[i];
+            if (tracing && f[i]) {
                 unsigned q = (unsigned)r0;
-                for (unsigned m = f & 15u; m; m &= m - 1u) h += knot_hash(0, q++, (unsigned)(4 * g + __ffs(m) - 1));
+                for (unsigned m = f[i] & 15u; m; m &= m - 1u) h += knot_hash(0, q++, (unsigned)(4 * g + __ffs(m) - 1));
                 q = (unsigned)r1;
-                for (unsigned m = f >> 4; m; m &= m - 1u) h += knot_hash(1, q++, (unsigned)(4 * g + __ffs(m) - 1));
+                for (unsigned m = f[i] >> 4; m; m &= m - 1u) h += knot_hash(1, q++, (unsigned)(4 * g + __ffs(m) - 1));
             }
         }
-        base0 += tot & 0xFFFF;
-        base1 += tot >> 16;
+        base += sh.scan4[i][kResWarps - 1];
     }
-    C.n[0] = base0;
-    C.n[1] = base1;
+    C.n[0] = base & 0xFFFF;
+    C.n[1] = base >> 16;
+    __syncthreads();
     return tracing ? res_sum_u64(h, sh) : 0ull;
 }
 
 // Mirrored knot rows {x, y} of both envelopes (envelope(), emd.cpp:107-122). Sifting always has
 // both mirror pairs: find_extrema never reports index 0 or L-1. Returns false when the tables do
 // not fit the shared-memory capacity (the host reruns the call on the lockstep engine).
-__device__ bool res_tables(ResCtx& C) {
+__device__ __forceinline__ bool res_tables(ResCtx& C) {
     C.N[0] = C.n[0] + 4;
     C.N[1] = C.n[1] + 4;
     if (2 * (C.N[0] + C.N[1]) > C.tab_rows) return false;
-    C.A[0] = C.tab;
-    C.B[0] = C.A[0] + C.N[0];
-    C.A[1] = C.B[0] + C.N[0];
-    C.B[1] = C.A[1] + C.N[1];
+    C.o_A[0] = C.o_tab;
+    C.o_B[0] = C.o_A[0] + 16 * C.N[0];
+    C.o_A[1] = C.o_B[0] + 16 * C.N[0];
+    C.o_B[1] = C.o_A[1] + 16 * C.N[1];
     for (int g = threadIdx.x; g < C.NG; g += kResThreads) {
-        const unsigned f = C.fl[g];
+        const unsigned f = sm_u8(C.o_fl)[g];
         if (!f) continue;
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            int q = 2 + C.pre[s][g];
+            int q = 2 + sm_u16(s ? C.o_pre1 : C.o_pre0)[g];
             for (unsigned m = (f >> (4 * s)) & 15u; m; m &= m - 1u) {
                 const int t = 4 * g + __ffs(m) - 1;
-                C.A[s][q++] = make_double2((double)t, C.cur[t]);
+                sm_d2(C.o_A[s])[q++] = make_double2((double)t, sm_d(C.o_cur)[t]);
             }
         }
     }
     __syncthreads();
     if (threadIdx.x < 2) {
         const int s = threadIdx.x, n = C.n[s];
-        double2* A = C.A[s];
+        double2* A = sm_d2(C.o_A[s]);
         const double e2 = 2.0 * (double)(C.L - 1);
         const double2 k0 = A[2], k1 = A[3], kn2 = A[n], kn1 = A[n + 1];
         A[0] = make_double2(-k1.x, k1.y);  // descending source order: -idx[1], -idx[0]
@@ -236,14 +328,25 @@ __device__ bool res_tables(ResCtx& C) {
 // Each boundary is verified bitwise (the guessed state at a chain's start against its
 // predecessor's stored end); a mismatch replays the chains from there in order (one thread per
 // side) until the recomputed rows agree with the stored ones. Returns the number of replays.
-__device__ int res_solve(ResCtx& C, ResShared& sh, int& replays_out) {
+#define SOLVE_SUB(k)                                                        \
+    do {                                                                    \
+        if (sprof && threadIdx.x == 0) {                                    \
+            const long long now_ = clock64();                               \
+            atomicAdd(&C.P->prof[k], (unsigned long long)(now_ - sprof_t)); \
+            sprof_t = now_;                                                 \
+        }                                                                   \
+    } while (0)
+__device__ __forceinline__ int res_solve(ResCtx& C, ResShared& sh, int& replays_out) {
+    const bool sprof = (C.P->debug & 2) && C.P->prof;
+    long long sprof_t = clock64();
     const int side = threadIdx.x >= kResChains ? 1 : 0;
     const int c = threadIdx.x - side * kResChains;
-    double2* A = C.A[side];
-    double2* B = C.B[side];
+    double2* A = sm_d2(C.o_A[side]);
+    double2* B = sm_d2(C.o_B[side]);
     const int N = C.N[side];
     const int R = N - 2;  // rows 1 .. N-2
-    const int CH = max(kResChainMin, (R + kResChains - 1) / kResChains);
+    const int cdiv = C.P->chain_div > 0 ? C.P->chain_div : kResChainDiv;
+    const int CH = max(kResChainMin, max((R + kResChains - 1) / kResChains, (R + cdiv - 1) / cdiv));
     const int nch = (R + CH - 1) / CH;
     const bool mine = c < nch;
     const int s = 1 + c * CH, e = min(s + CH, N - 1);
@@ -258,6 +361,7 @@ __device__ int res_solve(ResCtx& C, ResShared& sh, int& replays_out) {
     __syncthreads();
     for (int i = c + 1; i <= R; i += kResChains) A[i].y = B[i].x;
     __syncthreads();
+    SOLVE_SUB(8);
     // ---- 2. forward sweep
     double gd = 0.0, gr = 0.0;
     const int i0 = max(1, s - warm);
@@ -284,64 +388,95 @@ __device__ int res_solve(ResCtx& C, ResShared& sh, int& replays_out) {
         }
     }
     __syncthreads();
+    // Boundary check and replay rounds: a chain whose guessed start state differs from its
+    // predecessor's stored end replays its rows from that end until a recomputed row equals the
+    // stored one (from there on the stored rows are the sequential ones); a replay that reaches the
+    // chain's end moved that end, and the successor is checked in the next round.
+    int replays = 0;
+    bool dirty = false;
     if (mine && i0 < s) {
         const double2 t = B[s - 1];  // the predecessor chain's state at row s-1
-        if (!same_bits(t.x, gd) || !same_bits(t.y, gr)) atomicOr(&sh.bad, 1 << side);
+        dirty = !same_bits(t.x, gd) || !same_bits(t.y, gr);
     }
-    __syncthreads();
-    int replays = 0;
-    if (((sh.bad >> side) & 1) && c == 0) {  // replay chain heads in order until they agree
-        for (int cc = 1; cc < nch; ++cc) {
-            const int s2 = 1 + cc * CH, e2 = min(s2 + CH, N - 1);
-            double d = B[s2 - 1].x, r = B[s2 - 1].y;
-            for (int i = s2; i < e2; ++i) {
+    while (__syncthreads_or(dirty)) {
+        bool moved = false;
+        if (dirty) {
+            double d = B[s - 1].x, r = B[s - 1].y;
+            moved = true;
+            for (int i = s; i < e; ++i) {
                 const double h0 = A[i].x - A[i - 1].x, h1 = A[i + 1].x - A[i].x;
                 const double w = h0 / d;
                 d = 2.0 * (h0 + h1) - w * h0;
                 r = A[i].y - w * r;
                 const double2 st = B[i];
-                if (same_bits(st.x, d) && same_bits(st.y, r)) break;  // the rest of the chain agrees
+                if (same_bits(st.x, d) && same_bits(st.y, r)) {
+                    moved = false;
+                    break;
+                }
                 B[i] = make_double2(d, r);
                 ++replays;
             }
         }
+        sh.moved[threadIdx.x] = moved;
+        __syncthreads();
+        dirty = mine && c > 0 && sh.moved[threadIdx.x - 1];
     }
+    SOLVE_SUB(9);
+    // ---- 3. back substitution. rhs is consumed: A[i].y = RN(1/diag_i), so each row is the exactly
+    // rounded div_rn (r - h m) / diag (Markstein, as the lockstep solve) off a 5-op critical path.
+    // Phase a: every chain runs its warm-up rows (reading other chains' rows); phase b: its own
+    // rows from the guessed m_e, writing m_i over A[i].y row by row (only its own rows).
+    for (int i = c + 1; i <= R; i += kResChains) A[i].y = 1.0 / B[i].x;
     __syncthreads();
-    // ---- 3. back substitution: m_i into A[i].y (rhs is consumed; chains read only B and A.x)
+    SOLVE_SUB(12);
     double mg = 0.0;
     const int top = min(e + warm, N - 1);
     if (mine) {
         double m = 0.0;  // exact when top == N-1
         for (int i = top - 1; i >= e; --i) {
             const double2 dr = B[i];
-            m = (dr.y - (A[i + 1].x - A[i].x) * m) / dr.x;
+            const double2 a0 = A[i];
+            m = div_rn(dr.y - (A[i + 1].x - a0.x) * m, dr.x, a0.y);
         }
         mg = m;  // guessed m_e
+    }
+    __syncthreads();
+    if (mine) {
+        double m = mg;
         for (int i = e - 1; i >= s; --i) {
             const double2 dr = B[i];
-            m = (dr.y - (A[i + 1].x - A[i].x) * m) / dr.x;
+            const double2 a0 = A[i];
+            m = div_rn(dr.y - (A[i + 1].x - a0.x) * m, dr.x, a0.y);
             A[i].y = m;
         }
     }
-    if (threadIdx.x == 0) sh.bad = 0;
     __syncthreads();
-    if (mine && top < N - 1 && !same_bits(mg, A[e].y)) atomicOr(&sh.bad, 1 << side);
-    __syncthreads();
-    if (((sh.bad >> side) & 1) && c == 0) {  // replay from the top chain down
-        for (int cc = nch - 2; cc >= 0; --cc) {
-            const int s2 = 1 + cc * CH, e2 = min(s2 + CH, N - 1);
-            double m = A[e2].y;
-            for (int i = e2 - 1; i >= s2; --i) {
+    // the same rounds downwards: chain c starts from m_e = A[e].y (chain c+1's first row); own
+    // rows hold m now, so replays divide exactly (IEEE)
+    dirty = mine && top < N - 1 && !same_bits(mg, A[e].y);
+    while (__syncthreads_or(dirty)) {
+        bool moved = false;
+        if (dirty) {
+            double m = A[e].y;
+            moved = true;
+            for (int i = e - 1; i >= s; --i) {
                 const double2 dr = B[i];
                 m = (dr.y - (A[i + 1].x - A[i].x) * m) / dr.x;
-                if (same_bits(A[i].y, m)) break;
+                if (same_bits(A[i].y, m)) {
+                    moved = false;
+                    break;
+                }
                 A[i].y = m;
                 ++replays;
             }
         }
+        sh.moved[threadIdx.x] = moved;
+        __syncthreads();
+        dirty = mine && c + 1 < nch && sh.moved[threadIdx.x + 1];
     }
-    __syncthreads();
+    SOLVE_SUB(10);
     // ---- the segment table {m, 1/h}; y back from the candidate
+    const double* const cur = sm_d(C.o_cur);
     const double e2 = 2.0 * (double)(C.L - 1);
     for (int v = c; v < N; v += kResChains) {
         const double x = A[v].x;
@@ -352,9 +487,10 @@ __device__ int res_solve(ResCtx& C, ResShared& sh, int& replays_out) {
     for (int v = c; v < N; v += kResChains) {
         const double x = A[v].x;
         const int t = v <= 1 ? (int)(-x) : (v <= N - 3 ? (int)x : (int)(e2 - x));
-        A[v].y = C.cur[t];
+        A[v].y = cur[t];
     }
     __syncthreads();
+    SOLVE_SUB(11);
     replays_out = replays;
     return 0;
 }
@@ -368,15 +504,21 @@ __device__ __forceinline__ double res_env(const double2* A, const double2* B, in
 }
 
 // One sift pass (emd.cpp:142-148) in place; the candidate before it goes to oldc (SD recheck).
-__device__ void res_eval(ResCtx& C, double& num, double& den) {
+__device__ __forceinline__ void res_eval(ResCtx& C, double& num, double& den) {
     double x = 0.0, y = 0.0;
-    const double2 *A0 = C.A[0], *B0 = C.B[0], *A1 = C.A[1], *B1 = C.B[1];
-    for (int g = threadIdx.x; g < C.NG; g += kResThreads) {
+    const double2 *const A0 = sm_d2(C.o_A[0]), *const B0 = sm_d2(C.o_B[0]), *const A1 = sm_d2(C.o_A[1]), *const B1 = sm_d2(C.o_B[1]);
+    double* const cur = sm_d(C.o_cur);
+    double* const oldc = C.oldc;
+    const unsigned char* const fl = sm_u8(C.o_fl);
+    const unsigned short* const pre0 = sm_u16(C.o_pre0);
+    const unsigned short* const pre1 = sm_u16(C.o_pre1);
+    const int NG = C.NG, L = C.L;
+    for (int g = threadIdx.x; g < NG; g += kResThreads) {
         const int t0 = 4 * g;
-        const unsigned f = C.fl[g];
-        const int q0 = 1 + C.pre[0][g], q1 = 1 + C.pre[1][g];
-        const double2 v01 = *reinterpret_cast<const double2*>(C.cur + t0);
-        const double2 v23 = *reinterpret_cast<const double2*>(C.cur + t0 + 2);
+        const unsigned f = fl[g];
+        const int q0 = 1 + pre0[g], q1 = 1 + pre1[g];
+        const double2 v01 = *reinterpret_cast<const double2*>(cur + t0);
+        const double2 v23 = *reinterpret_cast<const double2*>(cur + t0 + 2);
         const double cv[4] = {v01.x, v01.y, v23.x, v23.y};
         double nv[4];
 #pragma unroll
@@ -387,7 +529,7 @@ __device__ void res_eval(ResCtx& C, double& num, double& den) {
             const double u = res_env(A0, B0, q0 + __popc(f & below), tt);
             const double l = res_env(A1, B1, q1 + __popc((f >> 4) & below), tt);
             const double mean = 0.5 * (u + l);
-            if (t < C.L) {
+            if (t < L) {
                 x += mean * mean;
                 y += cv[k] * cv[k];
                 nv[k] = cv[k] - mean;
@@ -395,10 +537,10 @@ __device__ void res_eval(ResCtx& C, double& num, double& den) {
                 nv[k] = 0.0;
             }
         }
-        *reinterpret_cast<double2*>(C.cur + t0) = make_double2(nv[0], nv[1]);
-        *reinterpret_cast<double2*>(C.cur + t0 + 2) = make_double2(nv[2], nv[3]);
-        *reinterpret_cast<double2*>(C.oldc + t0) = v01;
-        *reinterpret_cast<double2*>(C.oldc + t0 + 2) = v23;
+        *reinterpret_cast<double2*>(cur + t0) = make_double2(nv[0], nv[1]);
+        *reinterpret_cast<double2*>(cur + t0 + 2) = make_double2(nv[2], nv[3]);
+        *reinterpret_cast<double2*>(oldc + t0) = v01;
+        *reinterpret_cast<double2*>(oldc + t0 + 2) = v23;
     }
     num = x;
     den = y;
@@ -413,8 +555,8 @@ __device__ __noinline__ void res_sd_sequential(const ResCtx& C, double* num, dou
         const double tt = (double)t;
         double e[2];
         for (int k = 0; k < 2; ++k) {
-            while (seg[k] + 2 < C.N[k] && tt > C.A[k][seg[k] + 1].x) ++seg[k];
-            e[k] = res_env(C.A[k], C.B[k], seg[k], tt);
+            while (seg[k] + 2 < C.N[k] && tt > sm_d2(C.o_A[k])[seg[k] + 1].x) ++seg[k];
+            e[k] = res_env(sm_d2(C.o_A[k]), sm_d2(C.o_B[k]), seg[k], tt);
         }
         const double mean = 0.5 * (e[0] + e[1]);
         const double cv = C.oldc[t];
@@ -425,13 +567,13 @@ __device__ __noinline__ void res_sd_sequential(const ResCtx& C, double* num, dou
     *den = y;
 }
 
-__device__ void res_trace(const ResArgs& P, const RJob& J, int k, int iter, unsigned n0, unsigned n1,
+__device__ void res_trace(const ResArgs& P, int task, int m, int k, int iter, unsigned n0, unsigned n1,
                           unsigned long long h) {
     const int pos = atomicAdd(P.trace_count, 1);
     if (pos < P.trace_cap) {
         TraceRec r;
-        r.task = J.task;
-        r.m = J.m;
+        r.task = task;
+        r.m = m;
         r.k = k;
         r.iter = iter;
         r.n_max = n0;
@@ -450,6 +592,76 @@ __device__ void res_trace(const ResArgs& P, const RJob& J, int k, int iter, unsi
         }                                                               \
     } while (0)
 
+enum { RX_IMF = 0, RX_INSUFFICIENT = 1, RX_OVERFLOW = 2 };
+struct RxStats {
+    long long sifted;
+    int hazards;
+    unsigned n0, n1;  // extrema counts of the last detection
+};
+
+// extract_imf (emd.cpp:127-153) on the shared-memory candidate X: RX_IMF leaves the IMF in cur
+// after *iter sifts; RX_INSUFFICIENT: X itself has fewer than 2 maxima or minima (emd.cpp:138,
+// cur = X untouched); RX_OVERFLOW: the segment tables outgrew the shared memory. Trace records
+// (task, m, k, iter) of every find_extrema call, as the lockstep engine writes them.
+__device__ __forceinline__ int res_extract(ResCtx& C, ResShared& sh, int task, int m, int k, int* iter_out, RxStats& st) {
+    const ResArgs& P = *C.P;
+    const int L = C.L;
+    const bool tracing = P.trace != nullptr;
+    const bool prof_on = (P.debug & 2) && P.prof;
+    long long prof_t = clock64();
+    int iter = 0;
+    *iter_out = 0;
+    if (P.max_iters <= 0) return RX_IMF;  // the sift loop never runs: the IMF is X
+    {
+        const unsigned long long h = res_detect(C, sh, tracing);
+        if (tracing && threadIdx.x == 0) res_trace(P, task, m, k, 0, C.n[0], C.n[1], h);
+        RES_PROF(0);
+    }
+    st.n0 = C.n[0];
+    st.n1 = C.n[1];
+    if (C.n[0] < 2 || C.n[1] < 2) return RX_INSUFFICIENT;
+    while (true) {
+        if (!res_tables(C)) return RX_OVERFLOW;
+        RES_PROF(1);
+        {
+            int rp = 0;
+            res_solve(C, sh, rp);
+            st.hazards += rp > 0;
+        }
+        RES_PROF(2);
+        double num, den;
+        res_eval(C, num, den);
+        __syncthreads();
+        RES_PROF(3);
+        res_sum2(num, den, sh);
+        ++iter;
+        st.sifted += L;
+        const bool unc = (P.debug & 4) || sd_decision_uncertain(num, den, L, P.sd_thr);
+        if (unc) {  // the reference's sequential sums decide (rare)
+            if (threadIdx.x == 0) {
+                res_sd_sequential(C, &num, &den);
+                sh.red[0][0] = num;
+                sh.red[1][0] = den;
+                atomicAdd(P.sd_rechecks, 1);
+            }
+            __syncthreads();
+            num = sh.red[0][0];
+            den = sh.red[1][0];
+            __syncthreads();
+        }
+        RES_PROF(4);
+        if (den == 0.0 || num / den < P.sd_thr || iter >= P.max_iters) break;  // emd.cpp:150, :131
+        const unsigned long long h = res_detect(C, sh, tracing);
+        if (tracing && threadIdx.x == 0) res_trace(P, task, m, k, iter, C.n[0], C.n[1], h);
+        RES_PROF(0);
+        st.n0 = C.n[0];
+        st.n1 = C.n[1];
+        if (C.n[0] < 2 || C.n[1] < 2) break;  // envelope throws: the candidate is the IMF
+    }
+    *iter_out = iter;
+    return RX_IMF;
+}
+
 // One job: emd()'s IMF loop (emd.cpp:155-172) with extract_imf (:127-153).
 __device__ void res_job(ResCtx& C, ResShared& sh, int j) {
     const ResArgs& P = *C.P;
@@ -464,117 +676,90 @@ __device__ void res_job(ResCtx& C, ResShared& sh, int j) {
     for (int t = threadIdx.x; t < C.Lp; t += kResThreads) {
         double v = 0.0;
         if (t < L) v = J.init_kind == 1 ? J.a[t] + J.beta * J.b[t] : J.a[t];
-        C.cur[t] = v;
+        sm_d(C.o_cur)[t] = v;
         C.xg[t] = v;
     }
     __syncthreads();
     RES_PROF(6);
     int produced = 0;
     int* sifts = P.sifts + (size_t)j * P.kc;
+    RxStats st{};
     while (true) {
         if (J.kmax > 0 && out.k >= J.kmax) break;
-        // ---- extract_imf(X): iteration 0's find_extrema (emd.cpp:133-140, :164)
-        int iter = 0;
-        if (P.max_iters > 0 || J.detect_only) {
+        if (J.detect_only) {  // one find_extrema (the CEEMDAN stage check, emd.cpp:311)
             const unsigned long long h = res_detect(C, sh, tracing);
-            if (tracing && threadIdx.x == 0) res_trace(P, J, out.k, 0, C.n[0], C.n[1], h);
-            RES_PROF(0);
-            out.n0 = C.n[0];
-            out.n1 = C.n[1];
-            if (J.detect_only) break;
-            if (C.n[0] < 2 || C.n[1] < 2) {  // InsufficientExtrema on X: the decomposition ends
-                out.ended_insufficient = 1;
-                break;
-            }
-            while (true) {
-                if (!res_tables(C)) {
-                    out.smem_overflow = 1;
-                    goto done;
-                }
-                RES_PROF(1);
-                {
-                    int rp = 0;
-                    res_solve(C, sh, rp);
-                    out.hazards += rp > 0;
-                }
-                RES_PROF(2);
-                double num, den;
-                res_eval(C, num, den);
-                __syncthreads();
-                RES_PROF(3);
-                res_sum2(num, den, sh);
-                ++iter;
-                out.sifted += L;
-                const bool unc = (P.debug & 4) || sd_decision_uncertain(num, den, L, P.sd_thr);
-                if (unc) {  // the reference's sequential sums decide (rare)
-                    if (threadIdx.x == 0) {
-                        res_sd_sequential(C, &num, &den);
-                        sh.red[0][0] = num;
-                        sh.red[1][0] = den;
-                        atomicAdd(P.sd_rechecks, 1);
-                    }
-                    __syncthreads();
-                    num = sh.red[0][0];
-                    den = sh.red[1][0];
-                    __syncthreads();
-                }
-                RES_PROF(4);
-                if (den == 0.0 || num / den < P.sd_thr || iter >= P.max_iters) break;  // emd.cpp:150, :131
-                const unsigned long long h = res_detect(C, sh, tracing);
-                if (tracing && threadIdx.x == 0) res_trace(P, J, out.k, iter, C.n[0], C.n[1], h);
-                RES_PROF(0);
-                if (C.n[0] < 2 || C.n[1] < 2) break;  // envelope throws: the candidate is the IMF
-            }
+            if (tracing && threadIdx.x == 0) res_trace(P, J.task, J.m, out.k, 0, C.n[0], C.n[1], h);
+            st.n0 = C.n[0];
+            st.n1 = C.n[1];
+            break;
+        }
+        int iter = 0;
+        const int rc = res_extract(C, sh, J.task, J.m, out.k, &iter, st);
+        if (rc == RX_OVERFLOW) {
+            out.smem_overflow = 1;
+            break;
+        }
+        if (rc == RX_INSUFFICIENT) {  // InsufficientExtrema on X: the decomposition ends (emd.cpp:164)
+            out.ended_insufficient = 1;
+            break;
         }
         // ---- the IMF is the candidate: store it, residue -= imf (emd.cpp:167)
         if (J.write_imf && produced >= P.kc) {
             out.k_overflow = 1;
             break;
         }
+        prof_t = clock64();
         if (threadIdx.x == 0 && produced < P.kc) sifts[produced] = iter;
         double* row = J.write_imf ? P.store + ((size_t)j * P.kc + produced) * C.Lp : nullptr;
         for (int t = threadIdx.x; t < L; t += kResThreads) {
-            const double imf = C.cur[t];
+            const double imf = sm_d(C.o_cur)[t];
             const double rv = C.xg[t] - imf;
             if (row) row[t] = imf;
             if (J.imf_out) J.imf_out[t] = imf;
             if (J.res_out) J.res_out[t] = rv;
             C.xg[t] = rv;
-            C.cur[t] = rv;
+            sm_d(C.o_cur)[t] = rv;
         }
         __syncthreads();
         RES_PROF(5);
         ++produced;
         ++out.k;
     }
-done:
     if (J.res_final)
         for (int t = threadIdx.x; t < L; t += kResThreads) J.res_final[t] = C.xg[t];
     out.produced = produced;
+    out.sifted = st.sifted;
+    out.hazards = st.hazards;
+    out.n0 = st.n0;
+    out.n1 = st.n1;
     if (threadIdx.x == 0) P.res[j] = out;
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kResThreads, 1) k_resident(ResArgs P) {
-    extern __shared__ __align__(16) unsigned char res_smem[];
-    __shared__ ResShared sh;
-    ResCtx C;
+// Shared-memory carve-up common to the resident kernels.
+__device__ __forceinline__ void res_setup(ResCtx& C, const ResArgs& P) {
     C.P = &P;
     C.L = P.L;
     C.Lp = (P.L + 3) & ~3;
     C.NG = C.Lp / 4;
-    unsigned char* p = res_smem;
-    C.cur = reinterpret_cast<double*>(p);
-    p += (size_t)C.Lp * 8;
-    C.tab = reinterpret_cast<double2*>(p);
-    p += (size_t)P.tab_rows * 16;
-    C.pre[0] = reinterpret_cast<unsigned short*>(p);
-    C.pre[1] = C.pre[0] + C.NG;
-    p += (size_t)C.NG * 4;
-    C.fl = p;
+    int o = 0;
+    C.o_cur = o;
+    o += C.Lp * 8;
+    C.o_tab = o;
+    o += P.tab_rows * 16;
+    C.o_pre0 = o;
+    C.o_pre1 = o + C.NG * 2;
+    o += C.NG * 4;
+    C.o_fl = o;
     C.tab_rows = P.tab_rows;
     C.xg = P.scratch + (size_t)blockIdx.x * 2 * C.Lp;
     C.oldc = C.xg + C.Lp;
+}
+
+__global__ void __launch_bounds__(kResThreads, 1) k_resident(ResArgs P) {
+    __shared__ ResShared sh;
+    ResCtx C;
+    res_setup(C, P);
     while (true) {
         if (threadIdx.x == 0) sh.job = (int)atomicAdd(P.ticket, 1u);
         __syncthreads();
@@ -610,6 +795,170 @@ void launch_resident(const ResArgs& P, int grid, cudaStream_t st) {
     }
     k_resident<<<grid, kResThreads, smem, st>>>(P);
     count_launches(1);
+}
+
+// ---------------------------------------------------------------- CEEMDAN on the device
+//
+// emd.cpp:264-344 in one cooperative launch (every CTA resident): stage K runs one job per
+// realization m -- the next mode of the noise residue (task 1, emd.cpp:316-325; the mode stays in
+// shared memory) and the first mode of r_K + beta_K E_K(w_m) (task 2, :326-329), or of
+// x + beta_0 w_m at K = 0 (:296-300) -- then a grid barrier, the ordered mean of the first modes
+// (:301-306 / :331-338, realization order), the all-zero test and the residue update. The residue
+// check (find_extrema(residue).total() < 3, :311) and beta_K = nstd * signal_std(r_K) (:312, the
+// reference's two sequential passes) run in CTA 0 while the other CTAs start their noise modes.
+
+__device__ __forceinline__ void grid_sync(CeeCtl* ctl) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = &ctl->bar_gen;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
+            ctl->bar_count = 0;
+            __threadfence();
+            atomicAdd(&ctl->bar_gen, 1u);
+        } else {
+            while (*gen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// emd.cpp:209-217 on the shared-memory copy (one thread; two sequential passes)
+__device__ double res_std_seq(const double* v, int n) {
+    double mean = 0.0;
+    for (int i = 0; i < n; ++i) mean += v[i];
+    mean /= (double)n;
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += (v[i] - mean) * (v[i] - mean);
+    return sqrt(acc / (double)n);
+}
+
+__global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeArgs Q) {
+    __shared__ ResShared sh;
+    ResCtx C;
+    res_setup(C, P);
+    CeeCtl* ctl = Q.ctl;
+    const int L = C.L;
+    const bool tracing = P.trace != nullptr;
+    RxStats st{};
+    int K = 0;
+    for (;; ++K) {
+        if (K >= Q.kcap || K >= 64) {  // the host grows the rows and reruns the call
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->status = 2;
+            break;
+        }
+        if (K > 0) {
+            if (blockIdx.x == 0) {  // emd.cpp:310-311
+                int stop = Q.max_imfs > 0 && K >= Q.max_imfs;
+                if (!stop) {
+                    for (int t = threadIdx.x; t < C.Lp; t += kResThreads) sm_d(C.o_cur)[t] = t < L ? __ldcg(Q.residue + t) : 0.0;
+                    __syncthreads();
+                    const unsigned long long h = res_detect(C, sh, tracing);
+                    if (tracing && threadIdx.x == 0) res_trace(P, 3, -1, K, 0, C.n[0], C.n[1], h);
+                    stop = C.n[0] + C.n[1] < 3;
+                }
+                if (threadIdx.x == 0) ctl->stop[K] = stop;
+            }
+            grid_sync(ctl);
+            if (*(volatile int*)&ctl->stop[K]) break;
+            if (blockIdx.x == 0 && threadIdx.x == 0) {  // beta_K (emd.cpp:312); cur holds the residue
+                ctl->beta[K] = Q.nstd * res_std_seq(sm_d(C.o_cur), L);
+                __threadfence();
+                atomicMax(&ctl->beta_stage, K);
+            }
+        }
+        while (true) {
+            if (threadIdx.x == 0) sh.job = (int)atomicAdd(&ctl->ticket[K], 1u);
+            __syncthreads();
+            const int j = sh.job;
+            __syncthreads();
+            if (j >= Q.nr) break;
+            const int m = Q.m0 + j;
+            double* w = Q.nres + (size_t)j * Q.Ls;
+            int iter = 0;
+            if (K == 0) {  // x + beta_0 w (emd.cpp:297-298)
+                for (int t = threadIdx.x; t < C.Lp; t += kResThreads)
+                    sm_d(C.o_cur)[t] = t < L ? Q.x[t] + Q.beta0 * __ldcg(w + t) : 0.0;
+                __syncthreads();
+            } else {
+                bool have = false;
+                if (__ldcg(Q.alive + j)) {  // E_K(w_m): the next mode of the noise residue (emd.cpp:316-325)
+                    for (int t = threadIdx.x; t < C.Lp; t += kResThreads) sm_d(C.o_cur)[t] = t < L ? __ldcg(w + t) : 0.0;
+                    __syncthreads();
+                    const int rc = res_extract(C, sh, 1, m, K, &iter, st);
+                    if (rc == RX_OVERFLOW) {
+                        if (threadIdx.x == 0) ctl->status = 1;
+                        continue;
+                    }
+                    if (rc == RX_INSUFFICIENT) {
+                        if (threadIdx.x == 0) Q.alive[j] = 0;
+                    } else {
+                        for (int t = threadIdx.x; t < L; t += kResThreads) w[t] = __ldcg(w + t) - sm_d(C.o_cur)[t];
+                        have = true;
+                    }
+                }
+                if (threadIdx.x == 0)
+                    while (*(volatile int*)&ctl->beta_stage < K) __nanosleep(256);
+                __syncthreads();
+                const double beta = *(volatile double*)&ctl->beta[K];
+                for (int t = threadIdx.x; t < C.Lp; t += kResThreads)  // r + beta * E (zeros when exhausted)
+                    sm_d(C.o_cur)[t] = t < L ? __ldcg(Q.residue + t) + beta * (have ? sm_d(C.o_cur)[t] : 0.0) : 0.0;
+                __syncthreads();
+            }
+            const int rc = res_extract(C, sh, 2, m, K, &iter, st);  // first_mode (emd.cpp:285-290)
+            if (rc == RX_OVERFLOW) {
+                if (threadIdx.x == 0) ctl->status = 1;
+                continue;
+            }
+            double* row = Q.e1 + (size_t)j * C.Lp;
+            if (rc == RX_IMF)
+                for (int t = threadIdx.x; t < L; t += kResThreads) row[t] = sm_d(C.o_cur)[t];
+            if (threadIdx.x == 0) Q.e1_ok[j] = rc == RX_IMF;
+            __syncthreads();
+        }
+        grid_sync(ctl);
+        if (*(volatile int*)&ctl->status) break;
+        // the stage mean in realization order (emd.cpp:301-306, :331-338)
+        int nz = 0;
+        for (int t = blockIdx.x * kResThreads + threadIdx.x; t < L; t += gridDim.x * kResThreads) {
+            double acc = 0.0;
+            for (int j = 0; j < Q.nr; ++j)
+                if (__ldcg(Q.e1_ok + j)) acc += __ldcg(Q.e1 + (size_t)j * C.Lp + t);
+            const double mode = acc * Q.inv_nr;
+            Q.modes[(size_t)K * L + t] = mode;
+            if (K == 0) Q.residue[t] -= mode;
+            nz |= mode != 0.0;
+        }
+        if (K > 0) {
+            if (__syncthreads_or(nz) && threadIdx.x == 0) ctl->nonzero[K] = 1;
+            grid_sync(ctl);
+            if (!*(volatile int*)&ctl->nonzero[K]) break;  // nothing extractable anywhere (emd.cpp:336)
+            for (int t = blockIdx.x * kResThreads + threadIdx.x; t < L; t += gridDim.x * kResThreads)
+                Q.residue[t] -= Q.modes[(size_t)K * L + t];
+        }
+        grid_sync(ctl);
+    }
+    if (threadIdx.x == 0) {
+        atomicAdd(&ctl->sifted, (unsigned long long)st.sifted);
+        atomicAdd(&ctl->hazards, st.hazards);
+        if (blockIdx.x == 0) ctl->K = K;
+    }
+}
+
+int launch_res_ceemdan(const ResArgs& P, const CeeArgs& Q, int grid, cudaStream_t st) {
+    const size_t smem = resident_smem_bytes(P.L, P.tab_rows);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_res_ceemdan, cudaFuncAttributeMaxDynamicSharedMemorySize, resident_max_smem());
+        attr = true;
+    }
+    ResArgs p = P;
+    CeeArgs q = Q;
+    void* args[] = {&p, &q};
+    count_launches(1);
+    return (int)cudaLaunchCooperativeKernel((const void*)k_res_ceemdan, dim3(grid), dim3(kResThreads), args, smem, st);
 }
 
 // sums[r][t] += store rows of every write_imf job in job order (emd.cpp:246-251 / :301-306):

@@ -11,14 +11,14 @@ from paper_2106_15319_b200 import workloads as W
 
 keys = sys.argv[1:] or ["c1", "c2", "c3"]
 c = se.context()
-names = ["detect", "tables", "solve", "eval", "sums", "imf", "input", "-"]
+names = ["detect", "tables", "solve", "eval", "sums", "imf", "input", "-", "s.rhs", "s.fwd", "s.back", "s.table", "s.rcp", "-", "-", "-"]
 for key in keys:
     cfg = W.CONFIGS[key]
     s = se.concatenate(W.config_input(key), cfg["D"])
     c.check(c.lib.semd_set_engine(c.ptr, 2))
     se.decompose_full(s, cfg["algo"], max_sift_iters=cfg["max_sift_iters"], max_imfs=cfg["max_imfs"], nr=cfg["nr"])
     c.check(c.lib.semd_set_debug(c.ptr, 2))
-    prof = (C.c_uint64 * 8)()
+    prof = (C.c_uint64 * 16)()
     c.check(c.lib.semd_resident_profile(c.ptr, prof))
     t = time.perf_counter()
     d = se.decompose_full(s, cfg["algo"], max_sift_iters=cfg["max_sift_iters"], max_imfs=cfg["max_imfs"], nr=cfg["nr"])
