@@ -198,15 +198,22 @@ def run_ours(args, rank, world, local):
             traffic, traffic_src = t.get("traffic_bytes_per_launch"), t
         except Exception:
             traffic = None
+    resident = _stats(ctx)["resident_jobs"] > 0  # short signals: the resident engine ran the step
+    dom_name = ("k_res_ceemdan (the whole CEEMDAN: one persistent CTA per realization task, candidate and "
+                "segment tables in shared memory)" if cfg["algo"] == "ceemdan" else
+                "k_resident (one persistent CTA per realization, candidate and segment tables in shared memory)") \
+        if resident else "k_eval (sift pass: envelopes, mean, SD sums, next extrema detection)"
+    dom_timing = ("CUDA events around the resident-engine launch on the engine stream" if resident else
+                  "device time of every k_eval launch (%globaltimer span, first CTA start to last CTA end)")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "scope": "whole step: 16 B x sifted samples / device time of the step / N GPUs (BASELINE.md)",
             "dominant_kernel": {
-                "kernel": "k_eval (sift pass: envelopes, mean, SD sums, next extrema detection)",
+                "kernel": dom_name,
                 "achieved": eval_ach, "frac": (eval_ach / peak) if eval_ach else None,
                 "ms_per_step": tot["eval_ms"] / args.steps,
                 "share_of_step": (tot["eval_ms"] / args.steps) / (ms.value / args.steps) if ms.value else None,
-                "timing": "device time of every k_eval launch (%globaltimer span, first CTA start to last CTA end)",
+                "timing": dom_timing,
                 "launches_per_step": tot["eval_launches"] / args.steps},
             "traffic_detail": traffic_src,
             "algorithmic_bytes": "16 B per sifted sample (SURVEY.md §8(d))"}

@@ -83,7 +83,8 @@ typedef struct semd_stats {
                                 was re-solved by the exact sequential fallback (results stay bit-exact) */
     int32_t slots;           /* concurrent sift jobs used */
     int32_t waves;
-    double eval_ms;          /* optional: device time of the sift (eval) kernel, if timing enabled */
+    double eval_ms;          /* optional (timing enabled): device time of the sift kernel -- k_eval on the
+                                lockstep engine, k_resident / k_res_ceemdan on the resident engine */
     uint64_t eval_launches;
     uint64_t sd_rechecks;    /* SD stop tests whose tree-summed ratio was too close to sd_threshold to certify
                                 and were redone with the reference's sequential sums */

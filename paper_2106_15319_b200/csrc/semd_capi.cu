@@ -549,6 +549,13 @@ struct semd_ctx {
         }();
         return v;
     }
+    void res_timer_start() {
+        if (!r_t0) {
+            ck(cudaEventCreate(&r_t0), "event");
+            ck(cudaEventCreate(&r_t1), "event");
+        }
+        ck(cudaEventRecord(r_t0, stream), "ev");
+    }
     bool resident_for(long long L) const {
         const int mode = engine != SEMD_ENGINE_AUTO ? engine : env_engine();
         if (mode == SEMD_ENGINE_LOCKSTEP) return false;
@@ -639,18 +646,20 @@ struct semd_ctx {
             P.prof = r_prof.as<unsigned long long>();
         }
         static const bool res_log = std::getenv("SEMD_RES_LOG") != nullptr;
-        if (res_log && !r_t0) {
-            ck(cudaEventCreate(&r_t0), "event");
-            ck(cudaEventCreate(&r_t1), "event");
-        }
-        if (res_log) ck(cudaEventRecord(r_t0, stream), "ev");
+        const bool timed = res_log || timing;
+        if (timed) res_timer_start();
         launch_resident(P, grid, stream);
         ck(cudaGetLastError(), "resident launch");
-        if (res_log) ck(cudaEventRecord(r_t1, stream), "ev");
+        if (timed) ck(cudaEventRecord(r_t1, stream), "ev");
         r_out.resize(nj);
         ck(cudaMemcpyAsync(r_out.data(), r_res.p, (size_t)nj * sizeof(RResult), cudaMemcpyDeviceToHost, stream),
            "resident results");
         ck(cudaStreamSynchronize(stream), "resident run");  // also keeps h alive for the upload
+        if (timed) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r_t0, r_t1);
+            stats.eval_ms += ms;  // the dominant (sift) kernel's device time
+        }
         if (res_log) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, r_t0, r_t1);
@@ -1244,7 +1253,9 @@ struct semd_ctx {
         Q.beta0 = cs.beta0;
         Q.inv_nr = 1.0 / (double)nr;
         Q.ctl = ce_ctl.as<CeeCtl>();
+        if (timing) res_timer_start();
         const cudaError_t e = (cudaError_t)launch_res_ceemdan(P, Q, grid, stream);
+        if (timing && e == cudaSuccess) ck(cudaEventRecord(r_t1, stream), "ev");
         if (e != cudaSuccess) {  // e.g. the grid cannot be co-resident: per-stage drivers instead
             cudaGetLastError();
             cs.active = false;
@@ -1263,6 +1274,11 @@ struct semd_ctx {
             h_trace.clear();
             trace_total = 0;
             return false;
+        }
+        if (timing) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r_t0, r_t1);
+            stats.eval_ms += ms;
         }
         stats.sifted_samples += h.sifted;
         stats.sift_iterations += h.sifted / (uint64_t)std::max(1LL, n);

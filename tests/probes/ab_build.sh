@@ -9,7 +9,7 @@ NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=
 $NV -c _ab_src.cu -o /tmp/ab.o
 rm -f _ab_src.cu
 objs=""
-for f in semd_eval semd_sift semd_aux semd_capi; do
+for f in semd_eval semd_sift semd_aux semd_resident semd_capi; do
   if [ "$f.cu" = "${1:-semd_eval.cu}" ]; then objs="$objs /tmp/ab.o"; else objs="$objs $f.o"; fi
 done
 nvcc -shared -gencode arch=compute_100a,code=sm_100a -o ../libsemd_b200_ab.so $objs -lcudart
