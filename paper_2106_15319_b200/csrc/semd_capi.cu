@@ -1200,7 +1200,7 @@ struct semd_ctx {
     // ordered stage means, residue checks and beta_K on the device, no host round trip. False
     // (nothing produced) when it cannot run or a stage outgrew it; the caller then runs the
     // per-stage drivers.
-    DBuf ce_e1, ce_ok, ce_alive, ce_ctl;
+    DBuf ce_e1, ce_ok, ce_alive, ce_ctl, ce_E, ce_flags;
     bool ceemdan_fused(const double* d_x, long long n, const semd_sift_cfg& cfg, const semd_ens_cfg& ens,
                        semd_trace* tr) {
         using namespace semd::dev;
@@ -1210,6 +1210,9 @@ struct semd_ctx {
         ce_e1.alloc((size_t)nr * Lp * 8);
         ce_ok.alloc((size_t)nr * 4);
         ce_alive.alloc((size_t)nr * 4);
+        ce_E.alloc((size_t)nr * Lp * 8);
+        ce_flags.alloc((size_t)nr * 8);
+        ck(cudaMemsetAsync(ce_flags.p, 0, (size_t)nr * 8, stream), "flags");
         ce_ctl.alloc(sizeof(CeeCtl));
         semd::dev::launch_fill_i32(ce_alive.as<int>(), nr, 1, stream);
         ck(cudaMemsetAsync(ce_ctl.p, 0, sizeof(CeeCtl), stream), "ctl");
@@ -1244,6 +1247,9 @@ struct semd_ctx {
         Q.e1 = ce_e1.as<double>();
         Q.e1_ok = ce_ok.as<int>();
         Q.alive = ce_alive.as<int>();
+        Q.E = ce_E.as<double>();
+        Q.e_have = ce_flags.as<int>();
+        Q.edone = ce_flags.as<int>() + nr;
         Q.modes = A.sums;
         Q.kcap = A.kcap;
         Q.nr = nr;
@@ -1327,7 +1333,8 @@ struct semd_ctx {
                        double* out_imfs, int k_cap, double* out_res, semd_trace* tr, int* k_needed) {
         int mb = 0, me = ens.nr;
         if (comm) shard_range(ens.nr, rank, world, &mb, &me);
-        if (comm || !resident_for(n) || !ceemdan_fused(d_x, n, cfg, ens, tr)) {
+        // the fused device loop has no stage exchange: single GPU (or a 1-rank communicator) only
+        if ((comm && world > 1) || !resident_for(n) || !ceemdan_fused(d_x, n, cfg, ens, tr)) {
             ceemdan_begin(d_x, n, cfg, ens, mb, me, tr);
             auto stage_total = [&] {
                 ceemdan_stage();

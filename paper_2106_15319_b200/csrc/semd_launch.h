@@ -118,6 +118,9 @@ struct CeeArgs {
     double* e1;          // [nr][Lp] first modes of the stage
     int* e1_ok;          // [nr] first mode present (0: InsufficientExtrema -> zeros)
     int* alive;          // [nr] noise still yields modes (emd.cpp:318-324)
+    double* E;           // [nr][Lp] this stage's noise modes E_K(w_m) (noise item -> first-mode item)
+    int* e_have;         // [nr] E_K(w_m) present (0: exhausted, zeros)
+    int* edone;          // [nr] stage whose noise item has finished (stage-tagged, zeroed at launch)
     double* modes;       // [kcap][L] the averaged modes
     int kcap, nr, m0, max_imfs;
     double nstd, beta0, inv_nr;

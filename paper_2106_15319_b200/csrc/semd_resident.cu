@@ -869,42 +869,63 @@ __global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeAr
                 atomicMax(&ctl->beta_stage, K);
             }
         }
+        // items: K == 0: the nr first modes; K > 0: the nr noise modes, then the nr first modes
+        // (a first mode waits for its noise mode, handed over through Q.E and the stage-tagged
+        // Q.edone flag) -- finer items shorten the stage's tail
+        const int nitems = K == 0 ? Q.nr : 2 * Q.nr;
         while (true) {
             if (threadIdx.x == 0) sh.job = (int)atomicAdd(&ctl->ticket[K], 1u);
             __syncthreads();
-            const int j = sh.job;
+            const int item = sh.job;
             __syncthreads();
-            if (j >= Q.nr) break;
+            if (item >= nitems) break;
+            const bool noise_item = K > 0 && item < Q.nr;
+            const int j = K > 0 && item >= Q.nr ? item - Q.nr : item;
             const int m = Q.m0 + j;
             double* w = Q.nres + (size_t)j * Q.Ls;
+            double* E = Q.E + (size_t)j * C.Lp;
             int iter = 0;
-            if (K == 0) {  // x + beta_0 w (emd.cpp:297-298)
-                for (int t = threadIdx.x; t < C.Lp; t += kResThreads)
-                    sm_d(C.o_cur)[t] = t < L ? Q.x[t] + Q.beta0 * __ldcg(w + t) : 0.0;
-                __syncthreads();
-            } else {
-                bool have = false;
-                if (__ldcg(Q.alive + j)) {  // E_K(w_m): the next mode of the noise residue (emd.cpp:316-325)
+            if (noise_item) {  // E_K(w_m): the next mode of the noise residue (emd.cpp:316-325)
+                int have = 0;
+                if (__ldcg(Q.alive + j)) {
                     for (int t = threadIdx.x; t < C.Lp; t += kResThreads) sm_d(C.o_cur)[t] = t < L ? __ldcg(w + t) : 0.0;
                     __syncthreads();
                     const int rc = res_extract(C, sh, 1, m, K, &iter, st);
                     if (rc == RX_OVERFLOW) {
                         if (threadIdx.x == 0) ctl->status = 1;
-                        continue;
-                    }
-                    if (rc == RX_INSUFFICIENT) {
+                    } else if (rc == RX_INSUFFICIENT) {
                         if (threadIdx.x == 0) Q.alive[j] = 0;
                     } else {
-                        for (int t = threadIdx.x; t < L; t += kResThreads) w[t] = __ldcg(w + t) - sm_d(C.o_cur)[t];
-                        have = true;
+                        for (int t = threadIdx.x; t < L; t += kResThreads) {
+                            const double e = sm_d(C.o_cur)[t];
+                            w[t] = __ldcg(w + t) - e;
+                            E[t] = e;
+                        }
+                        have = 1;
                     }
                 }
-                if (threadIdx.x == 0)
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    Q.e_have[j] = have;
+                    __threadfence();
+                    atomicExch(Q.edone + j, K);
+                }
+                continue;
+            }
+            if (K == 0) {  // x + beta_0 w (emd.cpp:297-298)
+                for (int t = threadIdx.x; t < C.Lp; t += kResThreads)
+                    sm_d(C.o_cur)[t] = t < L ? Q.x[t] + Q.beta0 * __ldcg(w + t) : 0.0;
+                __syncthreads();
+            } else {
+                if (threadIdx.x == 0) {
+                    while (*(volatile int*)(Q.edone + j) < K) __nanosleep(128);
                     while (*(volatile int*)&ctl->beta_stage < K) __nanosleep(256);
+                }
                 __syncthreads();
                 const double beta = *(volatile double*)&ctl->beta[K];
+                const bool have = *(volatile int*)(Q.e_have + j) != 0;
                 for (int t = threadIdx.x; t < C.Lp; t += kResThreads)  // r + beta * E (zeros when exhausted)
-                    sm_d(C.o_cur)[t] = t < L ? __ldcg(Q.residue + t) + beta * (have ? sm_d(C.o_cur)[t] : 0.0) : 0.0;
+                    sm_d(C.o_cur)[t] = t < L ? __ldcg(Q.residue + t) + beta * (have ? __ldcg(E + t) : 0.0) : 0.0;
                 __syncthreads();
             }
             const int rc = res_extract(C, sh, 2, m, K, &iter, st);  // first_mode (emd.cpp:285-290)
