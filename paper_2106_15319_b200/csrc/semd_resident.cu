@@ -807,22 +807,37 @@ void launch_resident(const ResArgs& P, int grid, cudaStream_t st) {
 // check (find_extrema(residue).total() < 3, :311) and beta_K = nstd * signal_std(r_K) (:312, the
 // reference's two sequential passes) run in CTA 0 while the other CTAs start their noise modes.
 
+// GPU-scope acquire loads for flags other CTAs publish (volatile would make them system-scope)
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_acquire(const int* p) { return (int)ld_acquire(reinterpret_cast<const unsigned*>(p)); }
+
 __device__ __forceinline__ void grid_sync(CeeCtl* ctl) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* gen = &ctl->bar_gen;
-        const unsigned g = *gen;
+        const unsigned g = ld_acquire(&ctl->bar_gen);
         __threadfence();
         if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
             ctl->bar_count = 0;
             __threadfence();
             atomicAdd(&ctl->bar_gen, 1u);
         } else {
-            while (*gen == g) __nanosleep(64);
+            while (ld_acquire(&ctl->bar_gen) == g) __nanosleep(64);
         }
         __threadfence();
     }
     __syncthreads();
+}
+// a control word read once per CTA after a grid barrier and broadcast through shared memory
+__device__ __forceinline__ int cta_flag(const int* p, ResShared& sh) {
+    if (threadIdx.x == 0) sh.unc = ld_acquire(p);
+    __syncthreads();
+    const int v = sh.unc;
+    __syncthreads();
+    return v;
 }
 
 // emd.cpp:209-217 on the shared-memory copy (one thread; two sequential passes)
@@ -862,7 +877,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeAr
                 if (threadIdx.x == 0) ctl->stop[K] = stop;
             }
             grid_sync(ctl);
-            if (*(volatile int*)&ctl->stop[K]) break;
+            if (cta_flag(&ctl->stop[K], sh)) break;
             if (blockIdx.x == 0 && threadIdx.x == 0) {  // beta_K (emd.cpp:312); cur holds the residue
                 ctl->beta[K] = Q.nstd * res_std_seq(sm_d(C.o_cur), L);
                 __threadfence();
@@ -918,12 +933,15 @@ __global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeAr
                 __syncthreads();
             } else {
                 if (threadIdx.x == 0) {
-                    while (*(volatile int*)(Q.edone + j) < K) __nanosleep(128);
-                    while (*(volatile int*)&ctl->beta_stage < K) __nanosleep(256);
+                    while (ld_acquire(Q.edone + j) < K) __nanosleep(128);
+                    while (ld_acquire(&ctl->beta_stage) < K) __nanosleep(256);
+                    sh.red[0][0] = __ldcg(&ctl->beta[K]);
+                    sh.unc = __ldcg(Q.e_have + j);
                 }
                 __syncthreads();
-                const double beta = *(volatile double*)&ctl->beta[K];
-                const bool have = *(volatile int*)(Q.e_have + j) != 0;
+                const double beta = sh.red[0][0];
+                const bool have = sh.unc != 0;
+                __syncthreads();
                 for (int t = threadIdx.x; t < C.Lp; t += kResThreads)  // r + beta * E (zeros when exhausted)
                     sm_d(C.o_cur)[t] = t < L ? __ldcg(Q.residue + t) + beta * (have ? __ldcg(E + t) : 0.0) : 0.0;
                 __syncthreads();
@@ -940,7 +958,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeAr
             __syncthreads();
         }
         grid_sync(ctl);
-        if (*(volatile int*)&ctl->status) break;
+        if (cta_flag(&ctl->status, sh)) break;
         // the stage mean in realization order (emd.cpp:301-306, :331-338)
         int nz = 0;
         for (int t = blockIdx.x * kResThreads + threadIdx.x; t < L; t += gridDim.x * kResThreads) {
@@ -955,7 +973,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeAr
         if (K > 0) {
             if (__syncthreads_or(nz) && threadIdx.x == 0) ctl->nonzero[K] = 1;
             grid_sync(ctl);
-            if (!*(volatile int*)&ctl->nonzero[K]) break;  // nothing extractable anywhere (emd.cpp:336)
+            if (!cta_flag(&ctl->nonzero[K], sh)) break;  // nothing extractable anywhere (emd.cpp:336)
             for (int t = blockIdx.x * kResThreads + threadIdx.x; t < L; t += gridDim.x * kResThreads)
                 Q.residue[t] -= Q.modes[(size_t)K * L + t];
         }
