@@ -871,10 +871,11 @@ struct semd_ctx {
                             int m_begin, int m_end, semd_trace* tr) {
         if (n < 4) raise(SEMD_INVALID_INPUT, "emd: signal too short (need at least 4 samples)");
         const int jobs = std::max(0, m_end - m_begin);
-        const int G = auto_slots(n, jobs);
+        bool res = jobs > 0 && resident_for(n);
+        int G = res ? 1 : auto_slots(n, jobs);  // the resident engine needs no lockstep slots
         // W balanced waves (sizes differ by at most one): a short last wave would cost nearly a
         // full wave of lockstep steps
-        const int W = jobs > 0 ? (jobs + G - 1) / G : 0;
+        int W = jobs > 0 ? (jobs + G - 1) / G : 0;
         auto wave = [&](int i, int& w0, int& g) {
             const int base = jobs / W, extra = jobs % W;
             w0 = m_begin + i * base + std::min(i, extra);
@@ -882,7 +883,15 @@ struct semd_ctx {
         };
         int kcap = default_kcap(n, cfg.max_imfs);
         const long long Ls = (n + 1) / 2 * 2;
-        const bool res = jobs > 0 && resident_for(n);
+        if (res && !noise_override) {  // every realization's noise (side stream), overlapping the std
+            r_noise.alloc((size_t)jobs * Ls * 8);
+            semd::dev::launch_rng_ensemble(ens.base_seed, m_begin, jobs, reinterpret_cast<uint64_t*>(r_noise.as<double>()),
+                                           Ls, n, rng_stream);
+            semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(r_noise.as<double>()), (long long)jobs * Ls, 1.0,
+                                         rng_stream);
+            ck(cudaGetLastError(), "rng");
+            ck(cudaEventRecord(noise_ready[1], rng_stream), "rng event");
+        }
         // the first wave's noise (side stream) overlaps the sequential std on the main stream
         bool first_noise_ready = false;
         if (!noise_override && jobs > 0 && !res) {
@@ -921,15 +930,7 @@ struct semd_ctx {
             };
             try {
                 if (res) {  // every realization in one resident-engine launch, summed in m order
-                    if (!noise_override) {
-                        r_noise.alloc((size_t)jobs * Ls * 8);
-                        semd::dev::launch_rng_ensemble(ens.base_seed, m_begin, jobs,
-                                                       reinterpret_cast<uint64_t*>(r_noise.as<double>()), Ls, n,
-                                                       stream);
-                        semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(r_noise.as<double>()),
-                                                     (long long)jobs * Ls, 1.0, stream);
-                        ck(cudaGetLastError(), "rng");
-                    }
+                    if (!noise_override) ck(cudaStreamWaitEvent(stream, noise_ready[1], 0), "noise wait");
                     std::vector<JobSpec> js(jobs);
                     for (int i = 0; i < jobs; ++i) {
                         JobSpec& J = js[i];
@@ -949,8 +950,12 @@ struct semd_ctx {
                         stats.slots = std::min(jobs, sms);
                         return kmax_seen;
                     }
-                    fill_sums(kcap, 0.0);  // the tables outgrew the resident engine: lockstep waves below
-                    if (!noise_override) make_noise(0, 0), first_noise_ready = true;
+                    // the tables outgrew the resident engine: the lockstep engine, sized for it
+                    res = false;
+                    G = auto_slots(n, jobs);
+                    W = (jobs + G - 1) / G;
+                    --attempt;
+                    continue;
                 }
                 if (!noise_override && !first_noise_ready && W > 0) make_noise(0, 0);
                 first_noise_ready = false;  // a capacity retry regenerates it

@@ -120,3 +120,34 @@ def test_resident_ceemdan_vs_oracle(se, oracle):
     oi, ores, _, otr = oracle.decompose(s, 2, nr=16, trace_cap=200000)
     assert np.array_equal(bits(d["imfs"]), bits(oi)) and np.array_equal(bits(d["residue"]), bits(ores))
     assert np.array_equal(sort_trace(d["trace"]), sort_trace(otr))
+
+
+@pytest.mark.parametrize("n,nr,max_imfs,iters", [(12, 5, 0, 300), (64, 3, 0, 300), (200, 1, 0, 50),
+                                                 (700, 8, 2, 300), (1500, 6, 0, 1000)])
+def test_resident_ceemdan_edges_vs_lockstep_and_oracle(se, oracle, n, nr, max_imfs, iters):
+    """The fused device CEEMDAN (k_res_ceemdan) on small cases: noise modes running out (alive
+    flags), residue checks ending the stage loop, nr = 1 and a max_imfs limit -- IMFs, residue and
+    the full trace bit-identical to the lockstep per-stage drivers and to the oracle."""
+    rng = np.random.default_rng(n)
+    x = np.sin(np.arange(n) * 0.3) + 0.5 * rng.standard_normal(n)
+    kw = dict(nr=nr, max_imfs=max_imfs, max_sift_iters=iters)
+    a = run(se, LOCKSTEP, x, "ceemdan", **kw)
+    b = run(se, RESIDENT, x, "ceemdan", **kw)
+    assert b["stats"]["resident_jobs"] > 0
+    same(a, b)
+    oi, ores, _, otr = oracle.decompose(x, 2, iters=iters, imfs=max_imfs, nr=nr, trace_cap=200000)
+    assert np.array_equal(bits(b["imfs"]), bits(oi)) and np.array_equal(bits(b["residue"]), bits(ores))
+    assert np.array_equal(sort_trace(b["trace"]), sort_trace(otr))
+
+
+@pytest.mark.parametrize("n,nr", [(16, 4), (500, 3)])
+def test_resident_eemd_small_vs_oracle(se, oracle, n, nr):
+    """EEMD job queue + realization-ordered accumulation on small signals (IMF counts that differ
+    between realizations: shorter lists count as zeros, emd.cpp:246-251)."""
+    rng = np.random.default_rng(n + 1)
+    x = np.cos(np.arange(n) * 0.2) + 0.4 * rng.standard_normal(n)
+    b = run(se, RESIDENT, x, "eemd", nr=nr, max_sift_iters=300)
+    oi, ores, _, otr = oracle.decompose(x, 1, nr=nr, trace_cap=200000)
+    assert b["stats"]["resident_jobs"] == nr
+    assert np.array_equal(bits(b["imfs"]), bits(oi)) and np.array_equal(bits(b["residue"]), bits(ores))
+    assert np.array_equal(sort_trace(b["trace"]), sort_trace(otr))
