@@ -335,13 +335,16 @@ def test_slicewise(se, oracle):
         se.slicewise_decompose(np.zeros((0, 3)))
 
 
-def test_slicewise_ensembles(se):
-    """Batched slicewise EEMD (every channel x realization in one engine pass) and channel-by-channel
-    CEEMDAN equal the per-channel GPU decompositions bit-for-bit (same seeds, same sums order)."""
+def test_slicewise_ensembles(se, oracle):
+    """baseline.cpp:5-29: slicewise EEMD (every channel x realization in one batched engine pass) and
+    channel-by-channel CEEMDAN equal the oracle's decompose() of each channel bit-for-bit (the same
+    seeds per realization, the same realization-ordered sums), and the per-channel GPU calls."""
     rng = np.random.default_rng(12)
     x = rng.standard_normal((256, 4)) + np.cos(np.arange(256) / 7.0)[:, None]
-    for algo, nr in (("eemd", 6), ("ceemdan", 5)):
+    for algo, code, nr in (("eemd", 1, 6), ("ceemdan", 2, 5)):
         t = se.slicewise_decompose(x, algo, nr=nr)
+        ref = [oracle.decompose(np.ascontiguousarray(x[:, j]), code, nr=nr)[:2] for j in range(x.shape[1])]
+        assert np.array_equal(t, _slicewise_expected(ref)), algo
         per = []
         for j in range(x.shape[1]):
             d = se.decompose(x[:, j], algo, nr=nr)
