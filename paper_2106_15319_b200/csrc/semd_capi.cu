@@ -524,7 +524,7 @@ struct semd_ctx {
 
     // ---- the resident engine (semd_resident.cu): short signals, one persistent CTA per job ----
     int engine = SEMD_ENGINE_AUTO;
-    DBuf r_jobs, r_res, r_store, r_sifts, r_scratch, r_ticket, r_noise, r_prof;
+    DBuf r_jobs, r_res, r_store, r_sifts, r_scratch, r_ticket, r_noise, r_prof, r_rows;
     bool r_prof_init = false;
     cudaEvent_t r_t0 = nullptr, r_t1 = nullptr;  // SEMD_RES_LOG timing
     std::vector<semd::dev::RResult> r_out;
@@ -686,8 +686,23 @@ struct semd_ctx {
             if (overflow && !fail_write) raise(SEMD_CAPACITY, "IMF capacity exceeded (%d rows)", kc);
             return false;
         }
-        if (any_write)
-            launch_res_accum(P.jobs, P.res, nj, P.store, kc, Lp, L, A.sums, A.kcap, stream);
+        if (any_write) {  // per sums row, the range of jobs that can write it (job rows non-decreasing)
+            const int rows = A.kcap;
+            std::vector<int> rj(2 * (size_t)rows);
+            bool sorted = true;
+            for (int i = 1; i < nj; ++i) sorted = sorted && h[i].k0 + h[i].k >= h[i - 1].k0 + h[i - 1].k;
+            int lo = 0, hi = 0;
+            for (int r = 0; r < rows; ++r) {
+                while (sorted && lo < nj && h[lo].k0 + h[lo].k + kc <= r) ++lo;
+                while (sorted && hi < nj && h[hi].k0 + h[hi].k <= r) ++hi;
+                rj[2 * (size_t)r] = sorted ? lo : 0;
+                rj[2 * (size_t)r + 1] = sorted ? std::max(lo, hi) : nj;
+            }
+            r_rows.alloc(rj.size() * 4);
+            ck(cudaMemcpyAsync(r_rows.p, rj.data(), rj.size() * 4, cudaMemcpyHostToDevice, stream), "rows");
+            launch_res_accum(P.jobs, P.res, r_rows.as<int>(), P.store, kc, Lp, L, A.sums, rows, stream);
+            ck(cudaStreamSynchronize(stream), "accumulate");  // rj lifetime
+        }
         if (A.imf_sifts && js[0].write_imf && !js[0].detect_only) {
             const int base = js[0].k0 + js[0].k;
             const int cnt = std::min(r_out[0].produced, std::max(0, A.kcap - base));
@@ -1416,7 +1431,64 @@ struct semd_ctx {
                 }
             }
             const long long jobs = (long long)N * nr;
+            bool res_engine = resident_for(M);
             for (int attempt = 0;; ++attempt) {
+                if (res_engine) {  // every (channel, realization) job on the resident engine, in job order
+                    configure(M, 1, N * kc, 0);
+                    A.kper = kc;
+                    A.sd_threshold = cfg.sd_threshold;
+                    A.max_sift_iters = cfg.max_sift_iters;
+                    fill_sums(N * kc, ens_mode ? 0.0 : -0.0);
+                    if (!ens_mode)
+                        ck(cudaMemcpyAsync(res, d_x, (size_t)N * M * 8, cudaMemcpyDeviceToDevice, stream), "res");
+                    std::fill(kj.begin(), kj.end(), 0);
+                    // batches bounded by the IMF store (jobs x kc x M doubles), kept in job order
+                    const long long per = std::max<long long>(1, (1LL << 31) / ((long long)kc * ((M + 3) & ~3LL) * 8));
+                    bool ok = true;
+                    try {
+                        for (long long w0 = 0; w0 < jobs && ok; w0 += per) {
+                            const int g = (int)std::min<long long>(per, jobs - w0);
+                            std::vector<JobSpec> js(g);
+                            for (int i = 0; i < g; ++i) {
+                                const long long q = w0 + i;
+                                const int j = (int)(q / nr), m = (int)(q % nr);
+                                JobSpec& J = js[i];
+                                J.m = ens_mode ? m : j;
+                                J.task = 0;
+                                J.kmax = cfg.max_imfs;
+                                J.k0 = j * kc;
+                                J.a = d_x + (size_t)j * M;
+                                if (ens_mode) {
+                                    J.init_kind = 1;
+                                    J.beta = beta[j];
+                                    J.b = noise.as<double>() + (size_t)m * Ls;
+                                } else {
+                                    J.res_out = res + (size_t)j * M;
+                                }
+                            }
+                            std::vector<int> failed;
+                            ok = run_resident(js, kc, &failed);
+                            if (ok && !failed.empty()) ok = false;  // (EMD residues: rerun all on the lockstep engine)
+                            if (ok)
+                                for (int i = 0; i < g; ++i) {
+                                    const int j = (int)((w0 + i) / nr);
+                                    kj[j] = std::max(kj[j], r_out[i].k);
+                                }
+                        }
+                    } catch (const Error& e) {
+                        A.kper = 0;
+                        if (e.code == SEMD_CAPACITY && attempt < 3 && cfg.max_imfs == 0) {
+                            kc *= 2;
+                            continue;
+                        }
+                        throw;
+                    }
+                    A.kper = 0;
+                    if (ok) break;
+                    res_engine = false;  // tables outgrew the shared memory: the lockstep engine below
+                    --attempt;
+                    continue;
+                }
                 const int G = auto_slots(M, (int)std::min<long long>(jobs, 1 << 20));
                 if ((long long)N * kc * M * 8 > (1LL << 40)) raise(SEMD_NO_MEMORY, "slicewise IMF store too large");
                 configure(M, G, N * kc, 0);

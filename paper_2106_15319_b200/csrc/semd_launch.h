@@ -127,7 +127,7 @@ struct CeeArgs {
     CeeCtl* ctl;
 };
 int launch_res_ceemdan(const ResArgs& P, const CeeArgs& Q, int grid, cudaStream_t st);  // cudaError_t
-void launch_res_accum(const RJob* jobs, const RResult* res, int njobs, const double* store, int kc, long long Lp,
+void launch_res_accum(const RJob* jobs, const RResult* res, const int* rowj, const double* store, int kc, long long Lp,
                       int L, double* sums, int rows, cudaStream_t st);
 
 }  // namespace dev

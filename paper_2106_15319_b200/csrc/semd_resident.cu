@@ -1000,17 +1000,22 @@ int launch_res_ceemdan(const ResArgs& P, const CeeArgs& Q, int grid, cudaStream_
     return (int)cudaLaunchCooperativeKernel((const void*)k_res_ceemdan, dim3(grid), dim3(kResThreads), args, smem, st);
 }
 
-// sums[r][t] += store rows of every write_imf job in job order (emd.cpp:246-251 / :301-306):
-// job j's IMF kk lands in row rowbase_j + kk. One thread per (row, sample).
-__global__ void __launch_bounds__(256) k_res_accum(const RJob* jobs, const RResult* res, int njobs, const double* store,
-                                                   int kc, long long Lp, int L, double* sums, int rows) {
+// sums[r][t] += store rows of every write_imf job in job order (emd.cpp:246-251 / :301-306;
+// baseline.cpp:14 per channel): job j's IMF kk lands in row rowbase_j + kk. One thread per
+// (row, sample); the jobs that can write row r are the range rowj[2r] .. rowj[2r+1] (job rows are
+// non-decreasing in job order in every driver).
+__global__ void __launch_bounds__(256) k_res_accum(const RJob* jobs, const RResult* res, const int* rowj,
+                                                   const double* store, int kc, long long Lp, int L, double* sums,
+                                                   int rows) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (long long)rows * L) return;
     const int r = (int)(i / L), t = (int)(i % L);
+    const int j0 = rowj[2 * r], j1 = rowj[2 * r + 1];
+    if (j0 >= j1) return;
     double* dst = sums + (size_t)r * L + t;
     double acc = *dst;
     bool any = false;
-    for (int j = 0; j < njobs; ++j) {
+    for (int j = j0; j < j1; ++j) {
         if (!jobs[j].write_imf) continue;
         const int kk = r - (jobs[j].k0 + jobs[j].k);
         if (kk < 0 || kk >= res[j].produced) continue;
@@ -1020,11 +1025,11 @@ __global__ void __launch_bounds__(256) k_res_accum(const RJob* jobs, const RResu
     if (any) *dst = acc;
 }
 
-void launch_res_accum(const RJob* jobs, const RResult* res, int njobs, const double* store, int kc, long long Lp,
+void launch_res_accum(const RJob* jobs, const RResult* res, const int* rowj, const double* store, int kc, long long Lp,
                       int L, double* sums, int rows, cudaStream_t st) {
     const long long n = (long long)rows * L;
     if (n <= 0) return;
-    k_res_accum<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(jobs, res, njobs, store, kc, Lp, L, sums, rows);
+    k_res_accum<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(jobs, res, rowj, store, kc, Lp, L, sums, rows);
     count_launches(1);
 }
 
