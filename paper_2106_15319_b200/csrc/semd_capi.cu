@@ -1063,18 +1063,20 @@ struct semd_ctx {
                 ck(cudaMemcpyAsync(cs_noise() + (size_t)i * cs.Ls, noise_override + (size_t)(m0 + i) * n, n * 8,
                                    cudaMemcpyDeviceToDevice, stream),
                    "noise override");
-        } else {
-            for (int i0 = 0; i0 < cnt; i0 += 1024) {
-                const int g = std::min(1024, cnt - i0);
-                std::vector<uint64_t> seeds(g);
-                for (int i = 0; i < g; ++i) seeds[i] = derive_seed(ens.base_seed, (uint64_t)(m0 + i0 + i));
-                gen_noise(seeds, n, cs.Ls, cs_noise() + (size_t)i0 * cs.Ls);
-            }
+        } else if (cnt > 0) {  // w^(m) on the side stream (seeds derive_seed(base, m) on the device),
+            // overlapping the sequential std below
+            semd::dev::launch_rng_ensemble(ens.base_seed, m0, cnt, reinterpret_cast<uint64_t*>(cs_noise()), cs.Ls, n,
+                                           rng_stream);
+            semd::dev::launch_box_muller(reinterpret_cast<uint64_t*>(cs_noise()), (long long)cnt * cs.Ls, 1.0,
+                                         rng_stream);
+            ck(cudaGetLastError(), "rng");
+            ck(cudaEventRecord(noise_ready[1], rng_stream), "rng event");
         }
         cs.alive.assign(cnt, 1);
         semd::dev::launch_copy(d_x, cs_residue(), n, stream);
         fill_sums(cs.kcap, 0.0);
         cs.beta0 = device_std(d_x, n, ens.nstd);  // emd.cpp:293
+        if (!noise_override && cnt > 0) ck(cudaStreamWaitEvent(stream, noise_ready[1], 0), "noise wait");
         cs.active = true;
     }
 
