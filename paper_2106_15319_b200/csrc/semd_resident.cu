@@ -506,26 +506,28 @@ __device__ __forceinline__ double res_env(const double2* A, const double2* B, in
 // One sift pass (emd.cpp:142-148) in place; the candidate before it goes to oldc (SD recheck).
 __device__ __forceinline__ void res_eval(ResCtx& C, double& num, double& den) {
     double x = 0.0, y = 0.0;
-    const double2 *const A0 = sm_d2(C.o_A[0]), *const B0 = sm_d2(C.o_B[0]), *const A1 = sm_d2(C.o_A[1]), *const B1 = sm_d2(C.o_B[1]);
+    const double2 *const A0 = sm_d2(C.o_A[0]), *const B0 = sm_d2(C.o_B[0]), *const A1 = sm_d2(C.o_A[1]),
+                  *const B1 = sm_d2(C.o_B[1]);
     double* const cur = sm_d(C.o_cur);
     double* const oldc = C.oldc;
     const unsigned char* const fl = sm_u8(C.o_fl);
     const unsigned short* const pre0 = sm_u16(C.o_pre0);
     const unsigned short* const pre1 = sm_u16(C.o_pre1);
     const int NG = C.NG, L = C.L;
-    for (int g = threadIdx.x; g < NG; g += kResThreads) {
-        const int t0 = 4 * g;
+    // items of 2 samples (half a detection group): the rounds over the CTA are better filled
+    for (int hg = threadIdx.x; hg < 2 * NG; hg += kResThreads) {
+        const int g = hg >> 1, kb = (hg & 1) * 2;
+        const int t0 = 4 * g + kb;
         const unsigned f = fl[g];
         const int q0 = 1 + pre0[g], q1 = 1 + pre1[g];
-        const double2 v01 = *reinterpret_cast<const double2*>(cur + t0);
-        const double2 v23 = *reinterpret_cast<const double2*>(cur + t0 + 2);
-        const double cv[4] = {v01.x, v01.y, v23.x, v23.y};
-        double nv[4];
+        const double2 v = *reinterpret_cast<const double2*>(cur + t0);
+        const double cv[2] = {v.x, v.y};
+        double nv[2];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < 2; ++k) {
             const int t = t0 + k;
             const double tt = (double)t;
-            const unsigned below = (1u << k) - 1u;  // extrema at t0 .. t-1 precede t
+            const unsigned below = (1u << (kb + k)) - 1u;  // the group's extrema before t precede t
             const double u = res_env(A0, B0, q0 + __popc(f & below), tt);
             const double l = res_env(A1, B1, q1 + __popc((f >> 4) & below), tt);
             const double mean = 0.5 * (u + l);
@@ -538,9 +540,7 @@ __device__ __forceinline__ void res_eval(ResCtx& C, double& num, double& den) {
             }
         }
         *reinterpret_cast<double2*>(cur + t0) = make_double2(nv[0], nv[1]);
-        *reinterpret_cast<double2*>(cur + t0 + 2) = make_double2(nv[2], nv[3]);
-        *reinterpret_cast<double2*>(oldc + t0) = v01;
-        *reinterpret_cast<double2*>(oldc + t0 + 2) = v23;
+        *reinterpret_cast<double2*>(oldc + t0) = v;
     }
     num = x;
     den = y;
