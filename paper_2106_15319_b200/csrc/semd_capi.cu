@@ -618,6 +618,9 @@ struct semd_ctx {
         r_ticket.alloc(16);
         ck(cudaMemcpyAsync(r_jobs.p, h.data(), (size_t)nj * sizeof(RJob), cudaMemcpyHostToDevice, stream), "jobs");
         ck(cudaMemsetAsync(r_ticket.p, 0, 16, stream), "ticket");
+        // the trace and SD-recheck counters live in the control block: start from a reset one (the
+        // lockstep engine uploads its own per run; a fresh context's block is uninitialised)
+        ck(cudaMemcpyAsync(A.ctrl, pin_reset_ctrl(), sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
         ResArgs P{};
         P.jobs = r_jobs.as<RJob>();
         P.res = r_res.as<RResult>();
@@ -1241,6 +1244,7 @@ struct semd_ctx {
         const int grid = std::max(1, std::min(nr, sms));
         r_scratch.alloc((size_t)grid * 2 * Lp * 8);
         ensure_pin(A.G);
+        ck(cudaMemcpyAsync(A.ctrl, pin_reset_ctrl(), sizeof(Ctrl), cudaMemcpyHostToDevice, stream), "ctrl reset");
         ResArgs P{};
         P.L = (int)n;
         P.scratch = r_scratch.as<double>();

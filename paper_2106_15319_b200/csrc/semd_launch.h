@@ -94,6 +94,7 @@ struct ResArgs {
     unsigned long long* prof;  // [16] SM cycles per phase (debug bit 1): detect, tables, solve, eval, sums, final, init, -, solve: rhs, fwd, back, table
 };
 size_t resident_smem_bytes(int L, int rows);
+cudaError_t resident_setup();  // per device (launch_setup)
 int resident_max_smem();
 void launch_resident(const ResArgs& P, int grid, cudaStream_t st);
 

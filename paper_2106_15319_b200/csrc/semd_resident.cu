@@ -786,13 +786,18 @@ int resident_max_smem() {
     return v;
 }
 
+__global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeArgs Q);
+
+// the kernels' dynamic shared-memory limit (a per-device function attribute; launch_setup() runs
+// this for every context's device)
+cudaError_t resident_setup() {
+    cudaError_t e = cudaFuncSetAttribute(k_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, resident_max_smem());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_res_ceemdan, cudaFuncAttributeMaxDynamicSharedMemorySize, resident_max_smem());
+}
+
 void launch_resident(const ResArgs& P, int grid, cudaStream_t st) {
     const size_t smem = resident_smem_bytes(P.L, P.tab_rows);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, resident_max_smem());
-        attr = true;
-    }
     k_resident<<<grid, kResThreads, smem, st>>>(P);
     count_launches(1);
 }
@@ -988,11 +993,6 @@ __global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeAr
 
 int launch_res_ceemdan(const ResArgs& P, const CeeArgs& Q, int grid, cudaStream_t st) {
     const size_t smem = resident_smem_bytes(P.L, P.tab_rows);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_res_ceemdan, cudaFuncAttributeMaxDynamicSharedMemorySize, resident_max_smem());
-        attr = true;
-    }
     ResArgs p = P;
     CeeArgs q = Q;
     void* args[] = {&p, &q};

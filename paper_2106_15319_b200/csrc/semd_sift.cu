@@ -1428,7 +1428,9 @@ size_t solve_smem_bytes() {
 }
 
 cudaError_t launch_setup() {
-    cudaError_t e = eval_setup();
+    cudaError_t e = resident_setup();
+    if (e != cudaSuccess) return e;
+    e = eval_setup();
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem_bytes());
 }

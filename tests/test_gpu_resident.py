@@ -151,3 +151,16 @@ def test_resident_eemd_small_vs_oracle(se, oracle, n, nr):
     assert b["stats"]["resident_jobs"] == nr
     assert np.array_equal(bits(b["imfs"]), bits(oi)) and np.array_equal(bits(b["residue"]), bits(ores))
     assert np.array_equal(sort_trace(b["trace"]), sort_trace(otr))
+
+
+def test_smoke_in_fresh_process():
+    """__graft_entry__.smoke() as the driver runs it: a fresh process whose first decomposition is
+    on the resident engine (the control block's trace counter must start reset)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "smoke ok" in r.stdout
