@@ -24,26 +24,39 @@ def needs_build() -> bool:
     return any(os.path.getmtime(os.path.join(HERE, f)) > t for f in SRCS + HDRS + ["semd_cli.cpp"])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+CHECKED = os.path.join(PKG, "libsemd_b200_checked.so")
+
+
+def build_checked(verbose: bool = False) -> str:
+    """The bounds-checked variant (-DSEMD_CHECK: SEMD_ASSERT traps; tests/test_gpu_checked.py)."""
+    if os.path.exists(CHECKED) and os.path.getmtime(CHECKED) >= max(
+            os.path.getmtime(os.path.join(HERE, f)) for f in SRCS + HDRS):
+        return CHECKED
+    return build(force=True, verbose=verbose, checked=True)
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     objs = []
     for src in SRCS:
-        obj = os.path.join(HERE, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(HERE, src), "-o", obj]
+        obj = os.path.join(HERE, src.replace(".cu", "_chk.o" if checked else ".o"))
+        cmd = [NVCC, *FLAGS, *(["-DSEMD_CHECK"] if checked else []), "-c", os.path.join(HERE, src), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
         objs.append(obj)
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp", *objs, "-lcudart"]
+    out = CHECKED if checked else LIB
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out + ".tmp", *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(LIB + ".tmp", LIB)
-    build_cli(verbose)
-    return LIB
+    os.replace(out + ".tmp", out)
+    if not checked:
+        build_cli(verbose)
+    return out
 
 
 CLI = os.path.join(PKG, "semd-cli")
@@ -64,4 +77,7 @@ def build_cli(verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--checked" in sys.argv:
+        print(build_checked(verbose=True))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -361,6 +361,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
             for (int k = 0; k < kSpt; ++k) {
                 const double tt = (double)(t0 + k);
                 const int q = q0 + __popc((fl >> 1) & ((1u << k) - 1u));
+                SEMD_ASSERT(q >= 0 && q <= qmax[s]);  // the tile's staged rows (k_solve's table, toff)
                 const double2 a0 = R[q], b0 = R[nab + q], a1 = R[q + 1];
                 const double m1 = R[nab + q + 1].x;
                 const double h = a1.x - a0.x;

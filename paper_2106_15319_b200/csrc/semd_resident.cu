@@ -276,6 +276,7 @@ __device__ __forceinline__ unsigned long long res_detect(ResCtx& C, ResShared& s
     }
     C.n[0] = base & 0xFFFF;
     C.n[1] = base >> 16;
+    SEMD_ASSERT(C.n[0] <= C.L / 2 && C.n[1] <= C.L / 2);
     __syncthreads();
     return tracing ? res_sum_u64(h, sh) : 0ull;
 }
@@ -306,6 +307,7 @@ __device__ __forceinline__ bool res_tables(ResCtx& C) {
     __syncthreads();
     if (threadIdx.x < 2) {
         const int s = threadIdx.x, n = C.n[s];
+        SEMD_ASSERT(n >= 2 && C.o_B[1] + 16 * C.N[1] <= C.o_tab + 16 * C.tab_rows);
         double2* A = sm_d2(C.o_A[s]);
         const double e2 = 2.0 * (double)(C.L - 1);
         const double2 k0 = A[2], k1 = A[3], kn2 = A[n], kn1 = A[n + 1];
@@ -351,6 +353,7 @@ __device__ __forceinline__ int res_solve(ResCtx& C, ResShared& sh, int& replays_
     const bool mine = c < nch;
     const int s = 1 + c * CH, e = min(s + CH, N - 1);
     const int warm = (C.P->debug & 1) ? 2 : kResWarm;  // test hook: short warm-ups force the replays
+    SEMD_ASSERT(!mine || (s >= 1 && s < e && e <= N - 1));
     if (threadIdx.x == 0) sh.bad = 0;
     // ---- 1. rhs per row (parked in B.x, then moved to A.y once every y has been read)
     for (int i = c + 1; i <= R; i += kResChains) {
@@ -497,6 +500,7 @@ __device__ __forceinline__ int res_solve(ResCtx& C, ResShared& sh, int& replays_
 
 // Envelope value of side s at sample t whose segment row is q (spline_eval_fast, emd.cpp:80-85).
 __device__ __forceinline__ double res_env(const double2* A, const double2* B, int q, double tt) {
+    SEMD_ASSERT(q >= 0 && A + q + 1 < B);  // rows q, q+1 of the {x, y} plane (B follows A)
     const double2 a0 = A[q], b0 = B[q], a1 = A[q + 1];
     const double m1 = B[q + 1].x;
     const double h = a1.x - a0.x;
@@ -1019,6 +1023,7 @@ __global__ void __launch_bounds__(256) k_res_accum(const RJob* jobs, const RResu
         if (!jobs[j].write_imf) continue;
         const int kk = r - (jobs[j].k0 + jobs[j].k);
         if (kk < 0 || kk >= res[j].produced) continue;
+        SEMD_ASSERT(kk < kc);
         acc = acc + store[((size_t)j * kc + kk) * Lp + t];
         any = true;
     }

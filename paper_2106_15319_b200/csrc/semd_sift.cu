@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(Arena A) {
                 unsigned q = o[side] + ((w >> (8 + 8 * side)) & 0xFFu);
                 for (; fl; fl &= fl - 1u, ++q) {  // the lane's extrema in order (at most 2)
                     const int t = p0 + __ffs(fl) - 1;
+                    SEMD_ASSERT(q < (unsigned)A.cap && t >= 1 && t <= A.L - 2);  // knot list row, interior extremum
                     gi[side][q] = t;
                     if (tracing) (side ? h1 : h0) += knot_hash(side, q, (unsigned)t);
                 }

@@ -20,6 +20,24 @@
 //   sums    f64 [kcap][L]                 ensemble / IMF accumulators
 #pragma once
 #include <cstdint>
+#include <cstdio>
+
+// Bounds checks of the checked build (-DSEMD_CHECK, build.py --checked; the GPU pool offers no
+// compute-sanitizer): a failed check prints its condition and traps the kernel.
+#ifdef SEMD_CHECK
+#define SEMD_ASSERT(c)                                                                       \
+    do {                                                                                     \
+        if (!(c)) {                                                                          \
+            printf("SEMD_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                       \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define SEMD_ASSERT(c) \
+    do {               \
+    } while (0)
+#endif
 #include <vector_types.h>
 
 namespace semd {
