@@ -525,6 +525,7 @@ struct semd_ctx {
     // ---- the resident engine (semd_resident.cu): short signals, one persistent CTA per job ----
     int engine = SEMD_ENGINE_AUTO;
     DBuf r_jobs, r_res, r_store, r_sifts, r_scratch, r_ticket, r_noise, r_prof, r_rows;
+    DBuf ser_sig, ser_modes, ser_out;  // serial_decompose scratch (grow-only)
     bool r_prof_init = false;
     cudaEvent_t r_t0 = nullptr, r_t1 = nullptr;  // SEMD_RES_LOG timing
     std::vector<semd::dev::RResult> r_out;
@@ -2108,7 +2109,8 @@ int semd_decompose(semd_ctx* ctx, int algo, const double* x, size_t n, const sem
         need_ctx(ctx);
         size_t K = 0;
         const double* d_x = ctx->upload(ctx->in_x, x, n);
-        DBuf outb((k_cap + 1) * std::max<size_t>(n, 1) * 8);
+        DBuf& outb = ctx->ser_out;  // context scratch (grow-only)
+        outb.alloc((k_cap + 1) * std::max<size_t>(n, 1) * 8);
         double* d_imfs = outb.as<double>();
         double* d_res = d_imfs + k_cap * n;
         int rc = SEMD_OK;
@@ -2296,12 +2298,12 @@ static void serial_device(semd_ctx* ctx, int algo, const double* d_x, size_t M, 
                           size_t* modes_out, semd_trace* trace) {
     validate_serial(M, N, D);
     const size_t L = M * N + D * (N - 1);
-    DBuf sig(L * 8);
+    DBuf& sig = ctx->ser_sig;  // context scratch (grow-only): no cudaMalloc / cudaFree per call
+    sig.alloc(L * 8);
     concat_device(ctx, d_x, M, N, D, sig.as<double>(), 0);
-    ck(cudaStreamSynchronize(ctx->stream), "concatenate");
     // modes = imfs + residue, row k contiguous
     size_t kc = std::max<size_t>(k_cap, 1);
-    DBuf modes;
+    DBuf& modes = ctx->ser_modes;
     size_t K = 0;
     for (int attempt = 0;; ++attempt) {
         modes.alloc((kc + 1) * L * 8);
@@ -2338,7 +2340,8 @@ int semd_serial_decompose(semd_ctx* ctx, int algo, const double* x, size_t M, si
         need_ctx(ctx);
         validate_serial(M, N, D);
         const double* d_x = ctx->upload(ctx->in_x, x, M * N);
-        DBuf t(std::max<size_t>(k_cap, 1) * M * N * 8);
+        DBuf& t = ctx->ser_out;
+        t.alloc(std::max<size_t>(k_cap, 1) * M * N * 8);
         size_t mo = 0;
         try {
             serial_device(ctx, algo, d_x, M, N, D, cfg, ens, t.as<double>(), k_cap, &mo, trace);
