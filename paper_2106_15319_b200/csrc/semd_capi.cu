@@ -1052,7 +1052,9 @@ struct semd_ctx {
         cs.m0 = m0;
         cs.m1 = m1;
         const int cnt = m1 - m0;
-        cs.G = auto_slots(n, std::max(1, cnt));
+        // lockstep slots only when the stage jobs can run on the lockstep engine (the resident
+        // engine needs none; auto_slots queries the free memory)
+        cs.G = resident_for(n) ? 1 : auto_slots(n, std::max(1, cnt));
         cs.kcap = default_kcap(n, cfg.max_imfs);
         configure(n, cs.G, cs.kcap, tr ? trace_cap_for(tr) : 0);
         A.sd_threshold = cfg.sd_threshold;
