@@ -164,3 +164,23 @@ def test_smoke_in_fresh_process():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "smoke ok" in r.stdout
+
+
+@pytest.mark.parametrize("algo,kw", [("eemd", dict(max_sift_iters=300, max_imfs=10, nr=100)),
+                                     ("ceemdan", dict(max_sift_iters=5000, nr=500))])
+def test_resident_untraced_equals_lockstep(se, algo, kw):
+    """C2/C3 without tracing (the bench's and the CLI's mode, where the resident kernels take their
+    untraced paths): IMFs and residue bit-identical to the lockstep engine."""
+    s = pickup(se)
+    c = se.context()
+    out = {}
+    for eng in (LOCKSTEP, RESIDENT):
+        c.check(c.lib.semd_set_engine(c.ptr, eng))
+        try:
+            out[eng] = se.decompose_full(s, algo, **kw)
+        finally:
+            c.check(c.lib.semd_set_engine(c.ptr, AUTO))
+    a, b = out[LOCKSTEP], out[RESIDENT]
+    assert b["stats"]["resident_jobs"] > 0 and a["stats"]["resident_jobs"] == 0
+    assert a["imfs"].shape == b["imfs"].shape
+    assert np.array_equal(bits(a["imfs"]), bits(b["imfs"])) and np.array_equal(bits(a["residue"]), bits(b["residue"]))
