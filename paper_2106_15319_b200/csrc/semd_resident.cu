@@ -47,44 +47,15 @@ __device__ __forceinline__ unsigned char* sm_u8(int off) { return res_smem + off
 
 struct ResShared {
     double red[2][kResWarps];
-    int scan[kResWarps];
-    int scan4[4][kResWarps];
+    int scan4[4][kResWarps];  // res_detect's four-round block scan
     unsigned long long hred[kResWarps];
     int job;
     bool moved[kResThreads];  // solve replay rounds: the chain's end changed
-    int bad;
-    int unc;
+    int unc;  // a control word broadcast to the CTA
 };
 
 __device__ __forceinline__ bool same_bits(double a, double b) {
     return __double_as_longlong(a) == __double_as_longlong(b);
-}
-
-// Exclusive block scan of one int per thread; *tot = block total. Three barriers.
-__device__ __forceinline__ int res_excl_scan(int v, int* tot, ResShared& sh) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) sh.scan[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        int x = lane < kResWarps ? sh.scan[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane < kResWarps) sh.scan[lane] = x;
-    }
-    __syncthreads();
-    const int off = wid ? sh.scan[wid - 1] : 0;
-    *tot = sh.scan[kResWarps - 1];
-    __syncthreads();
-    return off + incl - v;
 }
 
 // Fixed-order block sum of two doubles (warp trees, then warps in order by one thread).
@@ -354,7 +325,6 @@ __device__ __forceinline__ int res_solve(ResCtx& C, ResShared& sh, int& replays_
     const int s = 1 + c * CH, e = min(s + CH, N - 1);
     const int warm = (C.P->debug & 1) ? 2 : kResWarm;  // test hook: short warm-ups force the replays
     SEMD_ASSERT(!mine || (s >= 1 && s < e && e <= N - 1));
-    if (threadIdx.x == 0) sh.bad = 0;
     // ---- 1. rhs per row (parked in B.x, then moved to A.y once every y has been read)
     for (int i = c + 1; i <= R; i += kResChains) {
         const double2 p = A[i - 1], q = A[i], n = A[i + 1];
