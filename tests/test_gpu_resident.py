@@ -184,3 +184,46 @@ def test_resident_untraced_equals_lockstep(se, algo, kw):
     assert b["stats"]["resident_jobs"] > 0 and a["stats"]["resident_jobs"] == 0
     assert a["imfs"].shape == b["imfs"].shape
     assert np.array_equal(bits(a["imfs"]), bits(b["imfs"])) and np.array_equal(bits(a["residue"]), bits(b["residue"]))
+
+
+def _fuzz_signal(rng, n, kind):
+    t = np.arange(n, dtype=np.float64)
+    if kind == "noise":
+        return rng.standard_normal(n)
+    if kind == "chirp":
+        return np.sin(t * t * 1e-4 * rng.uniform(0.5, 2)) + 0.1 * rng.standard_normal(n)
+    if kind == "steps":  # long plateaus and equal neighbours
+        return np.round(np.cumsum(rng.standard_normal(n)) * rng.uniform(0.5, 2)) / 2
+    if kind == "spikes":
+        x = 0.01 * rng.standard_normal(n)
+        x[rng.integers(0, n, max(1, n // 50))] += rng.uniform(-1e3, 1e3, max(1, n // 50))
+        return x
+    # mixed scales
+    return np.sin(t * 0.02) * 1e6 + rng.standard_normal(n) * 1e-3
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_resident_fuzz_vs_oracle(se, oracle, case):
+    """Seeded random lengths (4 .. the resident maximum), algorithms and signal shapes (noise,
+    chirps, plateaus/steps, spikes, mixed scales): the resident engine's IMFs, residue and trace
+    equal the oracle's bit for bit."""
+    rng = np.random.default_rng(1000 + case)
+    kind = ["noise", "chirp", "steps", "spikes", "mixed"][case % 5]
+    algo = ["emd", "eemd", "ceemdan"][case % 3]
+    n = int(rng.integers(4, 7000 if algo == "emd" else 2500))
+    x = _fuzz_signal(rng, n, kind)
+    iters = int(rng.choice([3, 50, 300]))
+    imfs = int(rng.choice([0, 0, 2, 5]))
+    nr = int(rng.integers(1, 6))
+    code = {"emd": 0, "eemd": 1, "ceemdan": 2}[algo]
+    try:
+        oi, ores, _, otr = oracle.decompose(x, code, iters=iters, imfs=imfs, nr=nr, trace_cap=400000)
+    except Exception as e:  # the reference rejects the input: so must the engine, with the same message
+        with pytest.raises(se.InvalidInput, match=str(e).split(": ", 1)[-1][:40] if ": " in str(e) else None):
+            run(se, RESIDENT, x, algo, max_sift_iters=iters, max_imfs=imfs, nr=nr)
+        return
+    d = run(se, RESIDENT, x, algo, max_sift_iters=iters, max_imfs=imfs, nr=nr)
+    assert d["imfs"].shape == oi.shape, (n, kind, algo)
+    assert np.array_equal(bits(d["imfs"]), bits(oi)), (n, kind, algo)
+    assert np.array_equal(bits(d["residue"]), bits(ores)), (n, kind, algo)
+    assert np.array_equal(sort_trace(d["trace"]), sort_trace(otr)), (n, kind, algo)
