@@ -136,6 +136,15 @@ class Context:
     def set_max_slots(self, g: int):
         self.run("semd_set_max_slots", int(g))
 
+    ENGINES = {"auto": 0, "lockstep": 1, "resident": 2}
+
+    def set_engine(self, engine: str):
+        """'auto' (default: the resident engine for signals of at most 8188 samples, the lockstep
+        engine above), 'lockstep' or 'resident' (include/semd_b200.h semd_set_engine)."""
+        if engine not in self.ENGINES:
+            raise InvalidInput(f"unknown engine '{engine}' (expected auto, lockstep or resident)")
+        self.run("semd_set_engine", self.ENGINES[engine])
+
     def set_stream(self, stream_ptr: int | None):
         self.run("semd_set_stream", C.c_void_p(stream_ptr or 0))
 

@@ -227,3 +227,18 @@ def test_resident_fuzz_vs_oracle(se, oracle, case):
     assert np.array_equal(bits(d["imfs"]), bits(oi)), (n, kind, algo)
     assert np.array_equal(bits(d["residue"]), bits(ores)), (n, kind, algo)
     assert np.array_equal(sort_trace(d["trace"]), sort_trace(otr)), (n, kind, algo)
+
+
+def test_python_set_engine(se):
+    """Context.set_engine: the Python mirror of semd_set_engine."""
+    c = se.context()
+    s = pickup(se)
+    try:
+        c.set_engine("lockstep")
+        assert se.decompose_full(s, "emd")["stats"]["resident_jobs"] == 0
+        c.set_engine("resident")
+        assert se.decompose_full(s, "emd")["stats"]["resident_jobs"] == 1
+        with pytest.raises(se.InvalidInput, match="unknown engine"):
+            c.set_engine("fast")
+    finally:
+        c.set_engine("auto")
