@@ -230,7 +230,7 @@ struct semd_ctx {
         const int rows_max = cap + 2;
         const int max_blocks = rows_max / semd::dev::kSolveBlock + 2;
         const long long Lp = (long long)tiles * semd::dev::kEvalTile;  // whole tiles: bulk copies stay inside
-        bufs.alloc((size_t)G * 3 * Lp * 8);
+        bufs.alloc((size_t)G * semd::dev::kBufs * Lp * 8);
         kidx.alloc(((size_t)4 * G * cap + 16) * 4);
         const size_t t4 = ((size_t)tiles + 3) & ~(size_t)3, t4p = ((size_t)tiles + 4) & ~(size_t)3;
         const int chunks = (tiles + semd::dev::kScanChunk - 1) / semd::dev::kScanChunk;
@@ -326,7 +326,7 @@ struct semd_ctx {
         // the engine's own slot-scaled buffers count as available (they are reused or regrown)
         const size_t held = bufs.bytes + kidx.bytes + toff.bytes + ktab.bytes + scnt.bytes + tnum.bytes + tden.bytes +
                             thash.bytes + tflags.bytes + sb.bytes + noise.bytes;
-        const long long per_slot = 94LL * L + 4096;  // slot buffers, knot lists, tables, detection words, noise
+        const long long per_slot = 102LL * L + 4096;  // slot buffers, knot lists, tables, detection words, noise
         const long long mem_g = (long long)(0.5 * (double)(free_b + held)) / per_slot;
         g = std::max(1LL, std::min(g, mem_g));
         g = std::min<long long>(g, std::max(1, jobs));
@@ -401,6 +401,7 @@ struct semd_ctx {
         const int ne = std::min((int)jobs.size(), G);
         for (int s = 0; s < ne; ++s) el[s] = s;
         c.n_eval = ne;
+        c.n_eval_pass = ne;
         c.active = ne;
         ck(cudaMemcpyAsync(A.slots, pin_jobs, sb, cudaMemcpyHostToDevice, stream), "upload slots");
         ck(cudaMemcpyAsync(A.ctrl, &c, cb, cudaMemcpyHostToDevice, stream), "upload ctrl");
@@ -436,7 +437,16 @@ struct semd_ctx {
         }();
         return v;
     }
+    // SEMD_SPEC=0 turns the speculative last sifts off, =2 makes every sift speculative (A/B runs)
+    static int spec_env_bits() {
+        static const int v = [] {
+            const char* e = std::getenv("SEMD_SPEC");
+            return !e ? 0 : (e[0] == '0' ? 8 : (e[0] == '2' ? 16 : 0));
+        }();
+        return v;
+    }
     void run(int max_steps) {
+        A.debug = debug_flags | spec_env_bits();
         const int LAG = lag_steps();
         int step = 0;
         for (;; ++step) {
@@ -478,6 +488,10 @@ struct semd_ctx {
             stats.sift_iterations += (uint64_t)(S.sifted / std::max(1, A.L));
         }
         stats.solve_hazards += (uint64_t)c.hazards;
+        spec_stats[0] += (unsigned long long)c.spec_pass;
+        spec_stats[1] += (unsigned long long)c.spec_hits;
+        spec_stats[2] += (unsigned long long)c.spec_misses;
+        spec_stats[3] += (unsigned long long)(step + 1);
         stats.sd_rechecks += (uint64_t)c.sd_rechecks;
         if (timing) stats.eval_ms += (double)c.ev_ns * 1e-6;
         for (int id = 0; id < 5; ++id) {  // the spans the last two steps left unfolded
@@ -513,12 +527,13 @@ struct semd_ctx {
     long long trace_total = 0;
     double span_ms[5] = {};                 // device spans of the step kernels (semd_kernel_spans)
     unsigned long long span_strips[4] = {};  // eval strips: DETECT/INIT mode, SIFT mode; their warp cycles
+    unsigned long long spec_stats[4] = {};   // speculative last sifts: run, stopped, continued; lockstep steps
     static constexpr int kHzCap = 4096;
     int debug_flags = 0;
     std::vector<int> h_hz;  // solve-hazard records since reset_stats (test hook)
 
     int max_steps_for(const semd_sift_cfg& cfg) const {
-        const long long it = std::max(1, cfg.max_sift_iters) + 2;
+        const long long it = 2LL * std::max(1, cfg.max_sift_iters) + 2;  // + a detection step per speculative miss
         return (int)std::min<long long>((long long)(A.kcap + 2) * it + 64, 1LL << 30);
     }
 
@@ -1958,6 +1973,20 @@ int semd_kernel_spans(semd_ctx* ctx, double* ms, uint64_t* strips) {
         for (int i = 0; i < 4; ++i) {
             strips[i] = ctx->span_strips[i];
             ctx->span_strips[i] = 0;
+        }
+    });
+}
+
+// Profiling hook: speculative last sifts since the last call -- run, stopped (the next IMF skipped
+// its DETECT pass and k_final its residue update), continued (an extra detection step) -- and the
+// lockstep steps (out[4]). Debug bit 8 (semd_set_debug) turns speculation off, bit 16 makes every
+// sift speculative.
+int semd_spec_stats(semd_ctx* ctx, uint64_t* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        for (int i = 0; i < 4; ++i) {
+            out[i] = ctx->spec_stats[i];
+            ctx->spec_stats[i] = 0;
         }
     });
 }

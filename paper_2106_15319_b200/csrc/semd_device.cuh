@@ -171,9 +171,11 @@ __device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parit
         : "memory");
 }
 
-__device__ __forceinline__ int pick_free_buffer(int xb, int cb) {
-    if (cb < 0) return xb == 0 ? 1 : 0;
-    return 3 - xb - cb;
+// lowest slot buffer id (of kBufs) other than the given ones (-1: none)
+__device__ __forceinline__ int pick_free_buffer(int xb, int cb, int db = -1) {
+    int b = 0;
+    while (b == xb || b == cb || b == db) ++b;
+    return b;
 }
 
 }  // namespace dev

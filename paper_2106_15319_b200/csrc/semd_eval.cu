@@ -34,6 +34,7 @@ namespace dev {
 struct EvalCtx {
     int mode, L, init_kind;
     const double* src;
+    const double* x;  // EM_SPEC: the IMF input X (R' = X - new)
     const double* a;
     const double* b;
     double beta;
@@ -49,7 +50,10 @@ __device__ EvalCtx make_ctx(const Arena& A, int slot, int mode) {
     J.a = sl.init_a;
     J.b = sl.init_b;
     J.beta = sl.beta;
-    J.src = A.bufs + buf_off(A, slot, (mode == EM_SIFT && sl.cb >= 0) ? sl.cb : sl.xb);
+    // the samples the pass reads: the candidate (SIFT, SPEC; DETECT of ST_REDETECT) or X
+    const bool cand = (mode == EM_SIFT || mode == EM_SPEC || sl.state == ST_REDETECT) && sl.cb >= 0;
+    J.src = A.bufs + buf_off(A, slot, cand ? sl.cb : sl.xb);
+    J.x = A.bufs + buf_off(A, slot, sl.xb);
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
         J.tv[s].tp = tab_planes(A, s, slot);
@@ -66,7 +70,8 @@ __device__ double new_value_global(const EvalCtx& J, int t) {
     const double u = envelope_tab(J.tv[0], t);
     const double l = envelope_tab(J.tv[1], t);
     const double mean = 0.5 * (u + l);
-    return J.src[t] - mean;
+    const double nv = J.src[t] - mean;
+    return J.mode == EM_SPEC ? J.x[t] - nv : nv;  // EM_SPEC detects R' = X - new (emd.cpp:167)
 }
 
 __device__ __noinline__ double init_value(const Arena& A, int slot, int t) {
@@ -104,6 +109,7 @@ __device__ __noinline__ unsigned plateau_flags(const Arena& A, int slot, int mod
 constexpr int kWarpRows = kEvalTile / 2 + 6;  // table rows one tile can touch per side
 // A stage holds one group of g consecutive tiles, laid out
 //   samples [base-2, base + g*T)  |  g x 32 detection words (SIFT)  |  rows side 0  |  rows side 1
+//   |  (SPEC: X [base-2, base + g*T))
 // (one bulk copy each). SIFT groups take as many tiles (<= kGroupMax) as fit; one tile
 // always fits (kWarpRows rows per side).
 constexpr int kStageBytes = 6912;
@@ -112,10 +118,10 @@ struct alignas(16) WarpStage {
     double flat[kStageBytes / 8];
     unsigned long long bar;  // mbarrier: the group's bulk copies have landed
 };
-__host__ __device__ constexpr int group_bytes(int g, int rows) {
-    return (g * kEvalTile + 2) * 8 + g * 32 * 4 + rows * 32;
+__host__ __device__ constexpr int group_bytes(int g, int rows, bool spec = false) {
+    return (g * kEvalTile + 2) * 8 * (spec ? 2 : 1) + g * 32 * 4 + rows * 32;
 }
-static_assert(group_bytes(1, 2 * kWarpRows) <= kStageBytes, "one SIFT tile fits a stage");
+static_assert(group_bytes(1, 2 * kWarpRows, true) <= kStageBytes, "one SPEC tile fits a stage");
 
 constexpr int kStripTiles = 16;  // longest strip (A.strip tiles): consecutive tiles one warp walks
 
@@ -133,6 +139,7 @@ struct Strip {
 // they were spilled, and every group's copies then waited on local-memory reloads from L2.
 struct alignas(16) CopySrc {
     const double* src;     // the samples this pass reads (SIFT, DETECT)
+    const double* xsrc;    // SPEC: X
     const unsigned* ow;    // SIFT: tflags words of tile j0 (current knot parity)
     const double2* tab0;   // side-0 segment table, {x, y} plane ({m, 1/h} plane at + cap + 8)
     const double2* tab1;   // side-1 segment table
@@ -148,13 +155,19 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
     S.nt = min(ST, A.tiles - S.j0);
     const Slot& sl = A.slots[S.slot];
     const int state = sl.state;
-    S.mode = state == ST_INIT ? EM_INIT : (state == ST_DETECT ? EM_DETECT : EM_SIFT);
+    S.mode = state == ST_INIT ? EM_INIT
+           : (state == ST_DETECT || state == ST_REDETECT) ? EM_DETECT
+           : state == ST_SIFT ? (sl.spec ? EM_SPEC : EM_SIFT)
+                              : EM_NONE;
     const int cb = sl.cb, xb = sl.xb;
     S.par = sl.par;
+    const bool sifting = S.mode == EM_SIFT || S.mode == EM_SPEC;
     S.dst = S.mode == EM_INIT ? A.bufs + buf_off(A, S.slot, xb)
-                              : (S.mode == EM_SIFT ? A.bufs + buf_off(A, S.slot, sl.db) : nullptr);
+                              : (sifting ? A.bufs + buf_off(A, S.slot, sl.db) : nullptr);
     if (lane == 0) {
-        cs.src = A.bufs + buf_off(A, S.slot, (S.mode == EM_SIFT && cb >= 0) ? cb : xb);
+        const bool cand = (sifting || state == ST_REDETECT) && cb >= 0;
+        cs.src = A.bufs + buf_off(A, S.slot, cand ? cb : xb);
+        cs.xsrc = A.bufs + buf_off(A, S.slot, xb);
         cs.tab0 = tab_planes(A, 0, S.slot).a;
         cs.tab1 = tab_planes(A, 1, S.slot).a;
         cs.ow = A.tflags + tfl_off(A, S.par, S.slot) + (size_t)S.j0 * 32;
@@ -162,7 +175,7 @@ __device__ __forceinline__ Strip strip_setup(const Arena& A, unsigned item, unsi
     S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
     S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
     S.to[0] = S.to[1] = 0;
-    if (S.mode == EM_SIFT) {
+    if (sifting) {
         const int j = S.j0 + min(lane, S.nt);
 #pragma unroll
         for (int s = 0; s < 2; ++s) S.to[s] = (int)toff_view(A, sl.par, s, S.slot)[j];
@@ -201,6 +214,7 @@ __device__ __forceinline__ Strip strip_from(const Arena& A, unsigned item, unsig
     S.mode = st.mode;
     S.par = st.par;
     S.dst = S.mode == EM_DETECT ? nullptr : A.bufs + buf_off(A, S.slot, st.dstb);
+
     S.nw = A.tflags + tfl_off(A, 1 - S.par, S.slot) + (size_t)S.j0 * 32;
     S.cnt0 = A.scnt + scnt_off(A, 0, S.slot) + S.j0;
     S.to[0] = st.to[0][lane];
@@ -218,7 +232,7 @@ __device__ __forceinline__ int group_tiles(const Strip& S, int i) {
     for (int c = 2; c <= kGroupMax; ++c) {
         const int e = min(i + c, S.nt);  // lanes >= nt hold toff of the strip's end
         const int rows = __shfl_sync(0xffffffffu, S.to[0], e) - lo0 + __shfl_sync(0xffffffffu, S.to[1], e) - lo1 + 6;
-        if (i + c <= S.nt && group_bytes(c, rows) <= kStageBytes) g = c;
+        if (i + c <= S.nt && group_bytes(c, rows, S.mode == EM_SPEC) <= kStageBytes) g = c;
     }
     return g;
 }
@@ -234,12 +248,14 @@ __device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpSt
     const int base = (S.j0 + i) * kEvalTile;
     const int e0 = base > 0 ? base - 2 : 0;  // 16-byte aligned; Lp = whole tiles
     const unsigned sb = (unsigned)(base + g * kEvalTile - e0) * 8u;
+    const bool spec = S.mode == EM_SPEC;
     double* f = st.flat;
     unsigned* ow = reinterpret_cast<unsigned*>(f + g * kEvalTile + 2);
     double2* r0 = reinterpret_cast<double2*>(ow + g * 32);  // {x,y} side 0 | side 1, then {m,1/h} side 0 | side 1
     const CopySrc c = cs;
-    bar_arrive_tx(&st.bar, sb + (unsigned)g * 128u + (unsigned)(n0 + n1) * 32u);
+    bar_arrive_tx(&st.bar, sb * (spec ? 2u : 1u) + (unsigned)g * 128u + (unsigned)(n0 + n1) * 32u);
     bulk_g2s(f + (e0 - (base - 2)), c.src + e0, sb, &st.bar);
+    if (spec) bulk_g2s(reinterpret_cast<double*>(r0 + 2 * (n0 + n1)) + (e0 - (base - 2)), c.xsrc + e0, sb, &st.bar);
     bulk_g2s(ow, c.ow + i * 32, (unsigned)g * 128u, &st.bar);
     bulk_g2s(r0, c.tab0 + lo0, (unsigned)n0 * 16u, &st.bar);
     bulk_g2s(r0 + n0, c.tab1 + lo1, (unsigned)n1 * 16u, &st.bar);
@@ -278,12 +294,15 @@ __device__ __forceinline__ int smem_search(const double2* R, int hi, double t) {
 // kSpt = 4 consecutive samples per lane; c2/c1 carry the new values at base-2/base-1.
 // Interior: the whole tile and its detection windows lie inside [1, L-2] (every tile but the
 // first and the last of a slot) -- no per-sample bound checks.
+// SPEC (a speculative last sift): as SIFT, and also R' = X - new (emd.cpp:167) from the staged X
+// (xsamp, aligned like samp) into S.rdst; the extrema detected are R''s, not new's.
 template <bool Interior, int M>
 __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i, const double* samp,
                                           const unsigned* ows, const double2* R0, const double2* R1, int nab, double& c2,
-                                          double& c1, double& snum, double& sden) {
+                                          double& c1, double& snum, double& sden, const double* xsamp = nullptr) {
     const int lane = threadIdx.x & 31;
     constexpr int mode = M;  // the pass's mode (each loop instantiates its own)
+    const bool spec = mode == EM_SIFT && xsamp != nullptr;  // a speculative last sift (warp-uniform)
     const int L = A.L;
     const int j = S.j0 + i;
     const int base = j * kEvalTile;
@@ -316,6 +335,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
                     e[s] = spline_eval_fast(a0.x, a1.x, a0.y, a1.y, b0.x, m1, h, b0.y, h * h, tt);
                 }
                 cc[u] = samp[u] - 0.5 * (e[0] + e[1]);
+                if (spec) cc[u] = xsamp[u] - cc[u];
             }
         }
         c2 = cc[0];
@@ -394,6 +414,25 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
                 if (t0 + k < L) S.dst[t0 + k] = nv[k];
         }
     }
+    if (spec) {  // R' = X - new (emd.cpp:167); the detection below runs on R'
+        // (R''s buffer is looked up per tile rather than held in a register across the strip)
+        double* const rdst = A.bufs + buf_off(A, S.slot, __ldg(&A.slots[S.slot].rb));
+        const double* xp = xsamp + 2 + lane * kSpt;
+#pragma unroll
+        for (int k = 0; k < kSpt; k += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(xp + k);
+            nv[k] = Interior || t0 + k < L ? v.x - nv[k] : 0.0;
+            nv[k + 1] = Interior || t0 + k + 1 < L ? v.y - nv[k + 1] : 0.0;
+        }
+        if (Interior || t0 + kSpt <= L) {
+#pragma unroll
+            for (int k = 0; k < kSpt; k += 2)
+                __stcs(reinterpret_cast<double2*>(rdst + t0 + k), make_double2(nv[k], nv[k + 1]));
+        } else {
+            for (int k = 0; k < kSpt; ++k)
+                if (t0 + k < L) rdst[t0 + k] = nv[k];
+        }
+    }
     // detection window t0-1 .. t0+2 needs values t0-2 .. t0+3
     double w[kSpt + 2];
     w[0] = __shfl_up_sync(0xffffffffu, nv[kSpt - 2], 1);
@@ -438,7 +477,7 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
             Win6 win;
 #pragma unroll
             for (int z = 0; z < kSpt + 2; ++z) win.w[z] = w[z];
-            if (plateau_flags(A, S.slot, mode, t0 - 1 + k, win, t0, w[k + 1], mn)) fmax |= 1u << k;
+            if (plateau_flags(A, S.slot, spec ? EM_SPEC : mode, t0 - 1 + k, win, t0, w[k + 1], mn)) fmax |= 1u << k;
             if (mn) fmin |= 1u << k;
         }
     }
@@ -479,7 +518,7 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
     const int lane = threadIdx.x & 31;
     WarpStage* stage = reinterpret_cast<WarpStage*>(eval_smem) + 2 * (threadIdx.x >> 5);
     const unsigned strips = ((unsigned)A.tiles + ST - 1) / ST;
-    const unsigned nstrips = (unsigned)A.ctrl->n_eval * strips;
+    const unsigned nstrips = (unsigned)A.ctrl->n_eval_pass * strips;  // ST_PRIMED slots have no pass
     if (lane == 0) {
         bar_init(&stage[0].bar);
         bar_init(&stage[1].bar);
@@ -514,10 +553,10 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
             const unsigned nx = __shfl_sync(0xffffffffu, next, 0);
             if (nx >= nstrips) return;
             const Strip S2 = strip_setup<ST>(A, nx, strips, csrc[ci ^ 1]);
-            if (S2.mode == EM_INIT) return;
+            if (S2.mode == EM_INIT || S2.mode == EM_NONE) return;
             __syncwarp();
             int g2 = 0;
-            if (S2.mode == EM_SIFT) {
+            if (S2.mode == EM_SIFT || S2.mode == EM_SPEC) {
                 g2 = group_tiles(S2, 0);
                 issue_group(S2, 0, g2, stage[fb], A.cap + 8, csrc[ci ^ 1]);
             } else {
@@ -549,7 +588,8 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
                 __syncwarp();  // stage b is refilled next
                 b ^= 1;
             }
-        } else if (S.mode == EM_SIFT) {
+        } else if (S.mode == EM_SIFT || S.mode == EM_SPEC) {
+            const bool spec = S.mode == EM_SPEC;
             int g = pre ? g_pre : group_tiles(S, 0);
             if (!pre) issue_group(S, 0, g, stage[b], A.cap + 8, csrc[ci]);
             for (int i = 0; i < S.nt;) {
@@ -571,21 +611,22 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
                     const double2* T0 = R0 + (__shfl_sync(0xffffffffu, S.to[0], t) - lo0);
                     const double2* T1 = R1 + (__shfl_sync(0xffffffffu, S.to[1], t) - lo1);
                     const double* sp = flat + u * kEvalTile;
+                    const double* xp = spec ? reinterpret_cast<const double*>(R0 + 2 * nab) + u * kEvalTile : nullptr;
                     if (base >= kEvalTile && base + 2 * kEvalTile <= A.L)
-                        eval_tile<true, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, nab, c2, c1, snum, sden);
+                        eval_tile<true, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, nab, c2, c1, snum, sden, xp);
                     else
-                        eval_tile<false, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, nab, c2, c1, snum, sden);
+                        eval_tile<false, EM_SIFT>(A, S, t, sp, ows + u * 32, T0, T1, nab, c2, c1, snum, sden, xp);
                 }
                 __syncwarp();  // stage b is refilled next
                 b ^= 1;
                 i += g;
                 g = gn;
             }
-        } else {  // INIT: values computed from the job's inputs, nothing staged
+        } else if (S.mode == EM_INIT) {  // values computed from the job's inputs, nothing staged
             for (int i = 0; i < S.nt; ++i)
                 eval_tile<false, EM_INIT>(A, S, i, nullptr, nullptr, nullptr, nullptr, 0, c2, c1, snum, sden);
         }
-        if (S.mode == EM_SIFT) {
+        if (S.mode == EM_SIFT || S.mode == EM_SPEC) {
             snum = warp_sum(snum);
             sden = warp_sum(sden);
             if (lane == 0) {
@@ -594,8 +635,9 @@ __global__ void __launch_bounds__(kEvalThreads, 2) k_eval(Arena A) {
             }
         }
         if (lane == 0) {
-            atomicAdd(&A.ctrl->strips[S.mode == EM_SIFT ? 1 : 0], 1ull);
-            atomicAdd(&A.ctrl->strip_cyc[S.mode == EM_SIFT ? 1 : 0], (unsigned long long)(clock64() - cyc0));
+            const int sx = S.mode == EM_SIFT || S.mode == EM_SPEC;
+            atomicAdd(&A.ctrl->strips[sx], 1ull);
+            atomicAdd(&A.ctrl->strip_cyc[sx], (unsigned long long)(clock64() - cyc0));
         }
         item = __shfl_sync(0xffffffffu, next, 0);
         pre = pre_next;

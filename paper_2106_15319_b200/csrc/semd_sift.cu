@@ -55,23 +55,25 @@ __device__ void build_lists(const Arena& A, bool allow_final) {
     int busy = 0, wait = 0;
     for (int s = s0; s < s1; ++s) {
         const int st = A.slots[s].state;
-        busy += (st == ST_INIT || st == ST_DETECT || st == ST_SIFT);
+        busy += eval_state(st);
         wait += (st == ST_WAITK);
     }
     int tb, tw;
     block_excl_scan(busy, &tb);
     block_excl_scan(wait, &tw);
     const bool finalize = allow_final && tb == 0 && tw > 0;
-    int ne = 0, nf = 0, ns = 0, nb = 0, act = 0;
+    int ne = 0, np = 0, nf = 0, ns = 0, nb = 0, act = 0;
     for (int s = s0; s < s1; ++s) {
         Slot& S = A.slots[s];
         if (finalize && S.state == ST_WAITK) S.state = ST_FINAL;
         const int st = S.state;
-        ne += (st == ST_INIT || st == ST_DETECT || st == ST_SIFT);
+        ne += eval_state(st) && st != ST_PRIMED;
+        np += (st == ST_PRIMED);
         nf += (st == ST_FINAL);
         act += (st != ST_FREE && st != ST_DONE);
         if (st == ST_SIFT) {
             S.db = pick_free_buffer(S.xb, S.cb);
+            S.rb = S.spec ? pick_free_buffer(S.xb, S.cb, S.db) : -1;
             ns += 2;
             for (int side = 0; side < 2; ++side) {
                 const int rows = (int)S.n[side] + 2;
@@ -79,8 +81,9 @@ __device__ void build_lists(const Arena& A, bool allow_final) {
             }
         }
     }
-    int tne, tnf, tns, tnb, tact;
+    int tne, tnp, tnf, tns, tnb, tact;
     int oe = block_excl_scan(ne, &tne);
+    int op = block_excl_scan(np, &tnp);
     int of = block_excl_scan(nf, &tnf);
     int os = block_excl_scan(ns, &tns);
     int ob = block_excl_scan(nb, &tnb);
@@ -88,7 +91,8 @@ __device__ void build_lists(const Arena& A, bool allow_final) {
     for (int s = s0; s < s1; ++s) {
         const Slot& S = A.slots[s];
         const int st = S.state;
-        if (st == ST_INIT || st == ST_DETECT || st == ST_SIFT) A.eval_list[oe++] = s;
+        if (eval_state(st) && st != ST_PRIMED) A.eval_list[oe++] = s;
+        if (st == ST_PRIMED) A.eval_list[tne + op++] = s;  // decided (and compacted) without an eval pass
         if (st == ST_FINAL) A.final_list[of++] = s;
         if (st == ST_SIFT) {
             for (int side = 0; side < 2; ++side) {
@@ -102,7 +106,8 @@ __device__ void build_lists(const Arena& A, bool allow_final) {
     }
     if (threadIdx.x == 0) {
         A.solve_off[tns] = tnb;
-        C->n_eval = tne;
+        C->n_eval = tne + tnp;
+        C->n_eval_pass = tne;
         C->n_final = tnf;
         C->n_solve = tns;
         C->solve_blocks = tnb;
@@ -165,6 +170,28 @@ __device__ __noinline__ void sd_fix_uncertain(const Arena& A, int ne) {
     }
 }
 
+// Is sift number `sift` (1-based) of the slot's current IMF likely its last? Then it runs as a
+// speculative last sift (ST_PRIMED). The stop statistics of this run's earlier IMFs with the same
+// index decide (speculate when at least half of those that reached this sift stopped there);
+// without them, from the second sift on. Any choice gives the same results: speculation only
+// changes which detection runs when.
+__device__ int spec_policy(const Arena& A, const Slot& S, int sift) {
+    if (A.debug & 8) return 0;
+    if (S.detect_only || S.imf_out || S.res_out) return 0;  // single-IMF jobs: no next IMF
+    if (S.kmax > 0 && S.k + 1 >= S.kmax) return 0;
+    if (A.debug & 16) return 1;
+    if (sift >= A.max_sift_iters) return 1;  // the iteration cap stops it
+    const int* h = A.ctrl->spec_hist[min(S.k, kSpecK - 1)];
+    const int j = min(sift, kSpecS - 1);
+    int reach = 0;
+    for (int q = j; q < kSpecS; ++q) reach += *(volatile const int*)(h + q);
+    if (reach < 4) return sift >= 2;
+    return 2 * *(volatile const int*)(h + j) >= reach;
+}
+__device__ __forceinline__ void spec_count_stop(const Arena& A, const Slot& S) {
+    atomicAdd(&A.ctrl->spec_hist[min(S.k, kSpecK - 1)][min(S.iter, kSpecS - 1)], 1);
+}
+
 // extract_imf's control flow (emd.cpp:131-151) for one slot after its eval
 // pass; returns 1 when this step's extrema must be compacted.
 __device__ int decide_slot(const Arena& A, int s) {
@@ -179,8 +206,11 @@ __device__ int decide_slot(const Arena& A, int s) {
     S.cpar = np;
     S.tn[0] = nmax;
     S.tn[1] = nmin;
-    if (state == ST_INIT || state == ST_DETECT) {
-        // iteration 0 of IMF k: extract_imf's first find_extrema
+    if (state == ST_INIT || state == ST_DETECT || state == ST_PRIMED) {
+        // iteration 0 of IMF k: extract_imf's first find_extrema (ST_PRIMED: detected by the
+        // previous IMF's speculative last sift, on its residue R' = this IMF's input)
+        S.spec = 0;
+        S.spec_hit = 0;
         if (A.max_sift_iters <= 0 && !S.detect_only) {  // loop body never runs: IMF = input
             S.cb = -1;
             S.iter = 0;
@@ -206,6 +236,25 @@ __device__ int decide_slot(const Arena& A, int s) {
             return tracing;
         }
         S.state = ST_SIFT;
+        S.spec = spec_policy(A, S, 1);
+        return 1;
+    }
+    if (state == ST_REDETECT) {
+        // the candidate's find_extrema of sift iteration `iter` (emd.cpp:132), after a speculative
+        // sift that did not stop
+        S.trace_iter = S.iter;
+        if (nmax < 2 || nmin < 2) {  // envelope throws: the candidate is the IMF (emd.cpp:137-140)
+            S.state = ST_WAITK;
+            S.spec_hit = 0;
+            if (A.imf_sifts && S.k0 + S.k < A.kcap) A.imf_sifts[S.k0 + S.k] = S.iter;
+            spec_count_stop(A, S);
+            return tracing;
+        }
+        S.par = np;
+        S.n[0] = nmax;
+        S.n[1] = nmin;
+        S.state = ST_SIFT;
+        S.spec = spec_policy(A, S, S.iter + 1);
         return 1;
     }
     if (state == ST_SIFT) {
@@ -214,6 +263,20 @@ __device__ int decide_slot(const Arena& A, int s) {
         S.cb = S.db;
         const double num = S.num, den = S.den;  // reference-order sums when uncertified (sd_fix_uncertain)
         bool stop = (den == 0.0 || num / den < A.sd_threshold) || S.iter >= A.max_sift_iters;
+        if (S.spec) {  // this step detected R' = X - candidate, not the candidate
+            atomicAdd(&A.ctrl->spec_pass, 1);
+            if (stop) {
+                atomicAdd(&A.ctrl->spec_hits, 1);
+                S.state = ST_WAITK;
+                S.spec_hit = 1;
+                if (A.imf_sifts && S.k0 + S.k < A.kcap) A.imf_sifts[S.k0 + S.k] = S.iter;
+                spec_count_stop(A, S);
+            } else {
+                atomicAdd(&A.ctrl->spec_misses, 1);
+                S.state = ST_REDETECT;
+            }
+            return 0;
+        }
         if (!stop) {
             S.trace_iter = S.iter;
             if (nmax < 2 || nmin < 2) {
@@ -224,11 +287,14 @@ __device__ int decide_slot(const Arena& A, int s) {
                 S.n[0] = nmax;
                 S.n[1] = nmin;
                 compact = 1;
+                S.spec = spec_policy(A, S, S.iter + 1);
             }
         }
         if (stop) {
             S.state = ST_WAITK;
+            S.spec_hit = 0;
             if (A.imf_sifts && S.k0 + S.k < A.kcap) A.imf_sifts[S.k0 + S.k] = S.iter;
+            spec_count_stop(A, S);
         }
     }
     return compact;
@@ -1174,7 +1240,7 @@ __device__ void decide_after_final(const Arena& A) {
     const int nf = C->n_final;
     for (int li = threadIdx.x; li < nf; li += blockDim.x) {
         Slot& S = A.slots[A.final_list[li]];
-        const int rb = pick_free_buffer(S.xb, S.cb);
+        const int rb = S.spec_hit ? S.rb : pick_free_buffer(S.xb, S.cb);  // k_final's residue / R'
         S.last_imf_b = S.cb >= 0 ? S.cb : S.xb;
         S.xb = rb;
         S.cb = -1;
@@ -1182,7 +1248,7 @@ __device__ void decide_after_final(const Arena& A) {
         S.iter = 0;
         if (S.kmax > 0 && S.k >= S.kmax) S.state = ST_DONE;
         else if (S.write_imf && !imf_row_ok(A, S.k0, S.k - 1)) S.state = ST_DONE;  // overflowed (counted): host grows kcap
-        else S.state = ST_DETECT;
+        else S.state = S.spec_hit ? ST_PRIMED : ST_DETECT;
     }
     __syncthreads();
     build_lists(A, false);
@@ -1243,6 +1309,7 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
                 const int li = (int)(q / (unsigned)tiles), tq = (int)(q % (unsigned)tiles);
                 const int sl = A.final_list[li];
                 const Slot& S = A.slots[sl];
+                if (S.spec_hit) continue;  // R' was written by the speculative last sift
                 const double* x = A.bufs + buf_off(A, sl, S.xb);
                 const double* imf = S.cb >= 0 ? A.bufs + buf_off(A, sl, S.cb) : x;
                 double* res = A.bufs + buf_off(A, sl, pick_free_buffer(S.xb, S.cb));
@@ -1328,7 +1395,8 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
                 FinalSlot f;
                 f.x = A.bufs + buf_off(A, A.final_list[c0 + li], S.xb);
                 f.imf = S.cb >= 0 ? A.bufs + buf_off(A, A.final_list[c0 + li], S.cb) : f.x;
-                f.res = A.bufs + buf_off(A, A.final_list[c0 + li], pick_free_buffer(S.xb, S.cb));
+                f.res = S.spec_hit ? nullptr  // R' was written by the speculative last sift
+                                   : A.bufs + buf_off(A, A.final_list[c0 + li], pick_free_buffer(S.xb, S.cb));
                 f.imf_out = S.imf_out;
                 f.res_out = S.res_out;
                 const int r = S.k0 + S.k;
@@ -1345,11 +1413,13 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
                     if (g + u >= cn) break;
                     const FinalSlot& f = tab[g + u];
                     if (full) {
-                        const double2 a0 = __ldcs(reinterpret_cast<const double2*>(f.x + tb));
-                        const double2 a1 = __ldcs(reinterpret_cast<const double2*>(f.x + tb) + 1);
+                        if (f.res) {
+                            const double2 a0 = __ldcs(reinterpret_cast<const double2*>(f.x + tb));
+                            const double2 a1 = __ldcs(reinterpret_cast<const double2*>(f.x + tb) + 1);
+                            xv[u][0] = a0.x; xv[u][1] = a0.y; xv[u][2] = a1.x; xv[u][3] = a1.y;
+                        }
                         const double2 b0 = __ldcs(reinterpret_cast<const double2*>(f.imf + tb));
                         const double2 b1 = __ldcs(reinterpret_cast<const double2*>(f.imf + tb) + 1);
-                        xv[u][0] = a0.x; xv[u][1] = a0.y; xv[u][2] = a1.x; xv[u][3] = a1.y;
                         iv[u][0] = b0.x; iv[u][1] = b0.y; iv[u][2] = b1.x; iv[u][3] = b1.y;
                     } else {
 #pragma unroll
@@ -1366,7 +1436,8 @@ __global__ void __launch_bounds__(256) k_final(Arena A) {
                     double rv[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) rv[e] = xv[u][e] - iv[u][e];  // emd.cpp:167
-                    if (full) {
+                    if (!f.res) {
+                    } else if (full) {
                         reinterpret_cast<double2*>(f.res + tb)[0] = make_double2(rv[0], rv[1]);
                         reinterpret_cast<double2*>(f.res + tb)[1] = make_double2(rv[2], rv[3]);
                     } else {

@@ -7,7 +7,8 @@
 // needed between sift iterations.
 //
 // HBM layout per engine (L = serialized length, G = slots, T = eval tile):
-//   bufs    f64 [G][3][L]        rotating X (IMF input), C (candidate), R (next residue)
+//   bufs    f64 [G][4][L]        rotating X (IMF input), C (candidate), D (new candidate), R (residue of a
+//                                speculative last sift, see ST_PRIMED)
 //   tflags  u32 [2 par][G][tiles][32]     k_eval's detection word per lane: window flags + tile ranks
 //   scnt    u32 [2 side][G][tiles]        extrema per tile
 //   kidx    i32 [2 par][2 side][G][cap]   compacted extrema indices (cap = L/2+2)
@@ -74,9 +75,24 @@ enum State : int {
     ST_WAITK = 4,   // IMF converged; waiting for every slot to reach the same IMF (lockstep)
     ST_FINAL = 5,   // residue update + accumulation this step
     ST_DONE = 6,
+    // Speculative last sift (Slot::spec): a sift that is likely the IMF's last also writes the
+    // residue R' = X - new (emd.cpp:167) and detects R''s extrema instead of new's. When the SD
+    // test then stops, R' and its extrema are the next IMF's input and its find_extrema, so the
+    // next IMF starts in ST_PRIMED (decide + compact only; no DETECT pass) and k_final only
+    // accumulates. When it does not stop, the candidate's extrema are detected in ST_REDETECT.
+    ST_PRIMED = 7,    // the next IMF's input extrema were detected by the previous IMF's last sift
+    ST_REDETECT = 8,  // detect the candidate's extrema (a speculative sift that did not stop)
 };
 
-enum EvalMode : int { EM_NONE = 0, EM_INIT = 1, EM_DETECT = 2, EM_SIFT = 3 };
+enum EvalMode : int { EM_NONE = 0, EM_INIT = 1, EM_DETECT = 2, EM_SIFT = 3, EM_SPEC = 4 };
+
+// slot states that take part in a step's eval / scan / decide phase
+__host__ __device__ inline bool eval_state(int st) {
+    return st == ST_INIT || st == ST_DETECT || st == ST_SIFT || st == ST_PRIMED || st == ST_REDETECT;
+}
+constexpr int kBufs = 4;        // slot buffers (X, C, D, R')
+constexpr int kSpecK = 16;      // speculation statistics: IMF index (last row: all later IMFs)
+constexpr int kSpecS = 8;       // ... and sift count (last column: all longer IMFs)
 
 struct Slot {
     // ---- job description (host-written before ST_INIT) ----
@@ -108,6 +124,9 @@ struct Slot {
     int cpar;            // parity the stage knots are compacted into this step
     unsigned tn[2];      // extrema counts of this step's detect
     int hazards;         // speculative-solve boundary mismatches observed
+    int spec;            // this SIFT pass is a speculative last sift (writes R' into rb, detects R')
+    int rb;              // buffer id of R'
+    int spec_hit;        // the finished IMF's residue R' is in rb and its extrema are detected
     long long sifted;    // sifted samples (L per completed sift)
     double num, den;
 };
@@ -135,7 +154,9 @@ struct Ctrl {
     int hz_count;  // hazard log records produced
     int finished;  // the run's last step has published active == 0: later steps return at once
     int sd_rechecks;  // SD stop tests redone with the reference's sequential sums (uncertified decisions)
-    int pad[3];
+    int spec_pass, spec_hits, spec_misses;  // speculative last sifts: run, stopped, continued
+    int n_eval_pass;  // eval_list[0, n_eval_pass): slots with an eval pass (ST_PRIMED slots follow)
+    int spec_hist[kSpecK][kSpecS];  // IMFs of this run that stopped after s sifts, per IMF index
     unsigned long long ev_t0;  // k_eval span of this step (globaltimer): min CTA start, max CTA end
     unsigned long long ev_t1;
     unsigned long long ev_ns;  // accumulated k_eval spans of this run (timing mode)
@@ -219,7 +240,8 @@ struct Arena {
     int* hzlog;       // [hzlog_cap][8] solve-hazard records {m, k, iter, side, n, block, blocks, 0}
     int hzlog_cap;
     int debug;        // test hooks: bit 0 treat every solve block boundary as a hazard (exercise the repair);
-                      // bit 2 redo every SD stop test with the sequential sums
+                      // bit 2 redo every SD stop test with the sequential sums; bit 3 no speculative
+                      // last sifts; bit 4 every sift speculative
                       // bit 1: accumulate k_solve per-phase clock cycles into prof[]
     unsigned long long* prof;  // [16]
     int* status_host; // mapped pinned: [0] active slots after this step, [1] step counter
@@ -230,7 +252,7 @@ __host__ __device__ inline bool imf_row_ok(const Arena& a, int k0, int k) {
     return k0 + k < a.kcap && (a.kper == 0 || k < a.kper);
 }
 __host__ __device__ inline size_t buf_off(const Arena& a, int slot, int b) {
-    return ((size_t)slot * 3 + (size_t)b) * (size_t)a.Lp;
+    return ((size_t)slot * kBufs + (size_t)b) * (size_t)a.Lp;
 }
 __host__ __device__ inline size_t knot_off(const Arena& a, int par, int side, int slot) {
     return (((size_t)par * 2 + side) * a.G + slot) * (size_t)a.cap;

@@ -26,6 +26,7 @@ sums = torch.zeros((64, n), dtype=torch.float64, device="cuda")
 k = C.c_size_t()
 ms = (C.c_double * 5)()
 strips = (C.c_uint64 * 4)()
+spec = (C.c_uint64 * 4)()
 
 
 def run(nr):
@@ -36,6 +37,7 @@ def run(nr):
 
 run(4)
 c.check(c.lib.semd_kernel_spans(c.ptr, ms, strips))
+getattr(c.lib, 'semd_spec_stats', lambda *a: 0)(c.ptr, spec)
 for _ in range(2):
     torch.cuda.synchronize()
     t = time.time()
@@ -44,6 +46,7 @@ for _ in range(2):
     el = time.time() - t
     st = c.stats()
     c.check(c.lib.semd_kernel_spans(c.ptr, ms, strips))
+    getattr(c.lib, 'semd_spec_stats', lambda *a: 0)(c.ptr, spec)
     names = ["solve", "eval", "scan", "compact", "final"]
     tot = sum(ms)
     print(key, "nr", nr, "wall %.1f ms" % (el * 1e3), "steps", st["steps"], "waves", st["waves"],
@@ -52,3 +55,4 @@ for _ in range(2):
           " sum %.1f" % tot, " strips detect %d sift %d" % (strips[0], strips[1]),
           " warp-cycles/strip detect %.0f sift %.0f" % (strips[2] / max(1, strips[0]), strips[3] / max(1, strips[1])),
           flush=True)
+    print("   speculative last sifts: run %d, stopped %d, continued %d; lockstep steps %d" % tuple(spec), flush=True)
