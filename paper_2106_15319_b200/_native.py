@@ -134,6 +134,7 @@ EXTRA = {"semd_set_noise_override": (C.c_int, [C.c_void_p, _dp, C.c_size_t, C.c_
          "semd_solve_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
          "semd_resident_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
          "semd_kernel_spans": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
+         "semd_std_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
          "semd_hazard_log": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
          "semd_mt19937_64_device_test": (C.c_int, [C.c_void_p, C.c_uint64, C.c_size_t, C.POINTER(C.c_uint64)])}
 

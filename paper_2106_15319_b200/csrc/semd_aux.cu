@@ -6,6 +6,7 @@
 // Compiled with -fmad=false (reference rounding, see semd_device.cuh).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "semd_device.cuh"
@@ -183,6 +184,233 @@ __global__ void __launch_bounds__(64) k_signal_std(const double* x, long long n,
         __syncthreads();
     }
     if (threadIdx.x == 0) *out = scale * sqrt(acc / (double)n);
+}
+
+// ---- the same sequential sums, computed in parallel and still bit-identical ("binade-locked"
+// integer accumulation), for long signals.
+//
+// s_{i+1} = RN(s_i + v_i) is not associative, but while the running sum stays inside one binade
+// [2^e, 2^(e+1)) (same sign) every s_i is an integer multiple S_i of u = 2^(e-52), and
+//     RN(s_i + v_i) = (S_i + rint(v_i / u)) * u
+// because the rounding grid is u throughout: the additions become exact INTEGER additions of
+// k_i = rint(v_i / u), which are associative. A tie (v_i / u = k + 1/2) rounds to even, which depends
+// on the parity of S_i only, so each piece of the sum is a function of the entry parity p:
+//     p -> (K_p = sum of k_i, min and max over the running prefixes)
+// and pieces compose in order: (f ; g)(p) = f(p) followed by g((p + K_p(f)) & 1).
+// The signal is cut into segments of kSeqSeg terms (one warp each). A segment's binade is guessed
+// from tree-summed approximate prefix sums; a single warp then walks the segments in order with
+// the EXACT running sum: when the guess matches the sum's sign and exponent, no term was too
+// large, and entry + min/max stay inside [2^52 + 1, 2^53 - 1] (so every exact intermediate lies
+// strictly inside the binade), the segment is one integer addition; otherwise the segment is
+// added term by term in fp64, as the reference does. Any input gives the reference's bits; the
+// guesses only decide how many segments take the slow path (C5: 2.5% of 33,280 in the mean pass,
+// 15 in the variance pass).
+constexpr int kSeqSeg = 512;
+constexpr long long kSeqMinLen = 1 << 16;  // shorter signals: the single-thread kernel (fewer launches)
+constexpr int kSeqLane = kSeqSeg / 32;  // consecutive terms per lane
+constexpr long long kSeqBig = 1ll << 61;
+struct alignas(16) SeqRec {
+    long long K[2], mn[2], mx[2];  // per entry parity
+    int guess;                     // sign << 11 | biased exponent of the guessed running sum
+    int bad;                       // a term too large for the binade's integers (or NaN): slow path
+};
+struct SeqHead {       // workspace header
+    double mean;       // pass 0's result: sum / n
+    unsigned slow[2];  // segments added term by term, per pass
+    unsigned pad[2];
+};
+
+__device__ __forceinline__ double seq_term(const double* x, long long i, int pass, double mean) {
+    const double v = x[i];
+    return pass == 0 ? v : (v - mean) * (v - mean);  // emd.cpp:212 / :215
+}
+
+// approximate segment sums (any order)
+__global__ void __launch_bounds__(256) k_seq_segsum(const double* x, long long n, int pass, const SeqHead* hd,
+                                                    double* segsum, long long nseg) {
+    const int lane = threadIdx.x & 31;
+    const double mean = pass ? hd->mean : 0.0;
+    for (long long sg = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); sg < nseg;
+         sg += (long long)gridDim.x * (blockDim.x >> 5)) {
+        const long long o = sg * kSeqSeg;
+        double a = 0.0;
+#pragma unroll 4
+        for (int j = 0; j < kSeqLane; ++j) {
+            const long long i = o + j * 32 + lane;
+            if (i < n) a += seq_term(x, i, pass, mean);
+        }
+        a = warp_sum(a);
+        if (lane == 0) segsum[sg] = a;
+    }
+}
+
+// guess[c] = sign and exponent of the approximate sum of segments 0..c-1 (one CTA)
+__global__ void __launch_bounds__(1024) k_seq_guess(const double* segsum, long long nseg, int* guess) {
+    __shared__ double wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long per = (nseg + blockDim.x - 1) / blockDim.x;
+    const long long c0 = min(nseg, tid * per), c1 = min(nseg, c0 + per);
+    double a = 0.0;
+    for (long long c = c0; c < c1; ++c) a += segsum[c];
+    double inc = a;  // inclusive scan over the CTA
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        double w = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    double run = (inc - a) + (warp ? wsum[warp - 1] : 0.0);
+    for (long long c = c0; c < c1; ++c) {
+        guess[c] = (int)((unsigned long long)__double_as_longlong(run) >> 52);
+        run += segsum[c];
+    }
+}
+
+struct SeqFn {
+    long long K[2], mn[2], mx[2];
+};
+__device__ __forceinline__ SeqFn seq_compose(const SeqFn& f, const SeqFn& g) {  // f first, then g
+    SeqFn r;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int q = (int)((p + f.K[p]) & 1);
+        const long long gk = q ? g.K[1] : g.K[0], gmn = q ? g.mn[1] : g.mn[0], gmx = q ? g.mx[1] : g.mx[0];
+        r.K[p] = f.K[p] + gk;
+        r.mn[p] = min(f.mn[p], f.K[p] + gmn);
+        r.mx[p] = max(f.mx[p], f.K[p] + gmx);
+    }
+    return r;
+}
+
+// one warp per segment: the segment as a function of the entry parity, for the guessed binade
+__global__ void __launch_bounds__(256) k_seq_records(const double* x, long long n, int pass, const SeqHead* hd,
+                                                     const int* guess, SeqRec* rec, long long nseg) {
+    const int lane = threadIdx.x & 31;
+    const double mean = pass ? hd->mean : 0.0;
+    for (long long sg = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); sg < nseg;
+         sg += (long long)gridDim.x * (blockDim.x >> 5)) {
+        const int g = guess[sg];
+        const int eb = g & 0x7ff;
+        // 1/u = 2^(52-e) (sign folded in: a negative running sum is mirrored); exponents where
+        // that power is not a normal double take the slow path
+        int bad = eb < 60 || eb > 2040;
+        const double scale =
+            __longlong_as_double(((long long)(g >> 11) << 63) | ((long long)(bad ? 1023 : 1023 + 52 - (eb - 1023)) << 52));
+        SeqFn f;
+        f.K[0] = f.K[1] = 0;
+        f.mn[0] = f.mn[1] = kSeqBig;
+        f.mx[0] = f.mx[1] = -kSeqBig;
+        const long long o = sg * kSeqSeg + lane * kSeqLane;
+#pragma unroll 4
+        for (int j = 0; j < kSeqLane; ++j) {
+            if (o + j >= n) break;
+            const double t = seq_term(x, o + j, pass, mean) * scale;  // v / u, exact
+            if (!(fabs(t) < 0x1p53)) {
+                bad = 1;
+                break;
+            }
+            const double fl = floor(t);
+            const double fr = t - fl;  // exact
+            const long long kf = (long long)fl;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                long long k = kf;
+                if (fr > 0.5) k += 1;
+                else if (fr == 0.5) k += (p + f.K[p] + kf) & 1;  // tie: to the even S
+                f.K[p] += k;
+                f.mn[p] = min(f.mn[p], f.K[p]);
+                f.mx[p] = max(f.mx[p], f.K[p]);
+            }
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {  // in-order fold: lane l takes lanes l .. l+2d-1
+            SeqFn h;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                h.K[p] = __shfl_down_sync(0xffffffffu, f.K[p], d);
+                h.mn[p] = __shfl_down_sync(0xffffffffu, f.mn[p], d);
+                h.mx[p] = __shfl_down_sync(0xffffffffu, f.mx[p], d);
+            }
+            if (lane + d < 32) f = seq_compose(f, h);
+        }
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            SeqRec r;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                r.K[p] = f.K[p];
+                r.mn[p] = f.mn[p];
+                r.mx[p] = f.mx[p];
+            }
+            r.guess = g;
+            r.bad = bad;
+            rec[sg] = r;
+        }
+    }
+}
+
+// one warp walks the segments in order with the exact running sum (every lane computes the same)
+__global__ void __launch_bounds__(32) k_seq_stitch(const double* x, long long n, int pass, SeqHead* hd,
+                                                   const SeqRec* rec, long long nseg, double* out, double scale) {
+    __shared__ double buf[kSeqSeg];
+    __shared__ SeqRec rs[2][32];
+    const int lane = threadIdx.x;
+    const double mean = pass ? hd->mean : 0.0;
+    double s = 0.0;
+    unsigned slow = 0;
+    if (lane < nseg) rs[0][lane] = rec[lane];
+    __syncwarp();
+    for (long long b = 0; b * 32 < nseg; ++b) {
+        const SeqRec* cur = rs[b & 1];
+        SeqRec nxt;  // the next 32 records travel while these are walked
+        const long long c2 = (b + 1) * 32 + lane;
+        if (c2 < nseg) nxt = rec[c2];
+        const int cnt = (int)min(32ll, nseg - b * 32);
+        for (int j = 0; j < cnt; ++j) {
+            const SeqRec r = cur[j];
+            const long long bits = __double_as_longlong(s);
+            const long long S = (bits & ((1ll << 52) - 1)) | (1ll << 52);
+            const int p = (int)(S & 1);
+            const long long K = p ? r.K[1] : r.K[0], mn = p ? r.mn[1] : r.mn[0], mx = p ? r.mx[1] : r.mx[0];
+            const bool fast = !r.bad && (int)((unsigned long long)bits >> 52) == r.guess && S + mn >= (1ll << 52) + 1 &&
+                              S + mx <= (1ll << 53) - 1;
+            if (fast) {
+                s = __longlong_as_double((bits & ~((1ll << 52) - 1)) | ((S + K) & ((1ll << 52) - 1)));
+            } else {  // the reference's additions, term by term
+                ++slow;
+                const long long o = (b * 32 + j) * kSeqSeg;
+                const int len = (int)min((long long)kSeqSeg, n - o);
+                for (int i = lane; i < len; i += 32) buf[i] = seq_term(x, o + i, pass, mean);
+                __syncwarp();
+                int i = 0;
+                for (; i + 8 <= len; i += 8) {
+                    const double v0 = buf[i], v1 = buf[i + 1], v2 = buf[i + 2], v3 = buf[i + 3];
+                    const double v4 = buf[i + 4], v5 = buf[i + 5], v6 = buf[i + 6], v7 = buf[i + 7];
+                    s += v0; s += v1; s += v2; s += v3; s += v4; s += v5; s += v6; s += v7;
+                }
+                for (; i < len; ++i) s += buf[i];
+                __syncwarp();
+            }
+        }
+        if (c2 < nseg) rs[(b + 1) & 1][lane] = nxt;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        hd->slow[pass] = slow;
+        if (pass == 0) hd->mean = s / (double)n;       // emd.cpp:213
+        else *out = scale * sqrt(s / (double)n);       // emd.cpp:216
+    }
 }
 
 // signal_std of B signals of length n (row b contiguous), one thread per signal:
@@ -454,9 +682,31 @@ void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t s
     k_box_muller<<<grid > 0 ? grid : 1, 256, 0, st>>>(draws, n, stdv);
     count_launches(1);
 }
-void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st) {
-    k_signal_std<<<1, 64, 0, st>>>(x, n, out, scale);
-    count_launches(1);
+size_t signal_std_workspace(long long n) {
+    if (n < kSeqMinLen) return 0;
+    const size_t nseg = (size_t)((n + kSeqSeg - 1) / kSeqSeg);
+    return sizeof(SeqHead) + 32 + nseg * (sizeof(SeqRec) + sizeof(double) + sizeof(int));
+}
+// ws: signal_std_workspace(n) bytes (16-byte aligned), or null for the single-thread kernel
+void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st, void* ws) {
+    if (!ws || n < kSeqMinLen) {
+        k_signal_std<<<1, 64, 0, st>>>(x, n, out, scale);
+        count_launches(1);
+        return;
+    }
+    const long long nseg = (n + kSeqSeg - 1) / kSeqSeg;
+    SeqHead* hd = reinterpret_cast<SeqHead*>(ws);
+    SeqRec* rec = reinterpret_cast<SeqRec*>(reinterpret_cast<unsigned char*>(ws) + 32);
+    double* segsum = reinterpret_cast<double*>(rec + nseg);
+    int* guess = reinterpret_cast<int*>(segsum + nseg);
+    const int grid = (int)std::min<long long>((nseg + 7) / 8, 148 * 8);
+    for (int pass = 0; pass < 2; ++pass) {
+        k_seq_segsum<<<grid, 256, 0, st>>>(x, n, pass, hd, segsum, nseg);
+        k_seq_guess<<<1, 1024, 0, st>>>(segsum, nseg, guess);
+        k_seq_records<<<grid, 256, 0, st>>>(x, n, pass, hd, guess, rec, nseg);
+        k_seq_stitch<<<1, 32, 0, st>>>(x, n, pass, hd, rec, nseg, out, scale);
+    }
+    count_launches(8);
 }
 static int grid_for(long long n);
 void launch_signal_std_batch(const double* x, long long n, int B, double* out, double scale, cudaStream_t st) {

@@ -189,7 +189,7 @@ struct semd_ctx {
     std::vector<Slot> h_slots;
     std::vector<TraceRec> h_trace;
     // scratch
-    DBuf in_x, in_y, noise, scratch, scratch2, scalar, rng_jobs;
+    DBuf in_x, in_y, noise, scratch, scratch2, scalar, rng_jobs, std_ws;
     cudaEvent_t ev[16]{};
     cudaStream_t rng_stream = nullptr;  // noise for the next wave is generated here, overlapping the sift
     cudaEvent_t noise_ready[2]{};
@@ -890,9 +890,19 @@ struct semd_ctx {
         ck(cudaStreamSynchronize(stream), "rng sync");  // jobs vector lifetime
     }
 
+    // Workspace of the parallel (still reference-ordered) signal_std; null for short signals and
+    // under debug bit 32, which keeps the single-thread kernel (tests compare the two).
+    long long std_last_n = 0;
+    void* std_workspace(long long n) {
+        const size_t b = (debug_flags & 32) ? 0 : semd::dev::signal_std_workspace(n);
+        std_last_n = b ? n : 0;
+        if (!b) return nullptr;
+        std_ws.alloc(b);
+        return std_ws.p;
+    }
     double device_std(const double* d_x, long long n, double scale) {
         scalar.alloc((2 + 2 * 256 + 8) * 8);
-        semd::dev::launch_signal_std(d_x, n, scalar.as<double>(), scale, stream);
+        semd::dev::launch_signal_std(d_x, n, scalar.as<double>(), scale, stream, std_workspace(n));
         double v = 0.0;
         ck(cudaMemcpyAsync(&v, scalar.p, 8, cudaMemcpyDeviceToHost, stream), "std");
         ck(cudaStreamSynchronize(stream), "std");
@@ -1190,7 +1200,7 @@ struct semd_ctx {
         scalar.alloc((2 + 2 * 256 + 8) * 8);
         ck(cudaEventRecord(res_ready, stream), "residue event");
         ck(cudaStreamWaitEvent(rng_stream, res_ready, 0), "residue wait");
-        semd::dev::launch_signal_std(cs_residue(), n, scalar.as<double>(), cs.ens.nstd, rng_stream);
+        semd::dev::launch_signal_std(cs_residue(), n, scalar.as<double>(), cs.ens.nstd, rng_stream, std_workspace(n));
         double* beta_host = reinterpret_cast<double*>(status_host + 8);  // pinned
         ck(cudaMemcpyAsync(beta_host, scalar.p, 8, cudaMemcpyDeviceToHost, rng_stream), "std");
         {  // E_i(w^(m)) for the living noise residues (emd.cpp:316-325)
@@ -1988,6 +1998,22 @@ int semd_spec_stats(semd_ctx* ctx, uint64_t* out) {
             out[i] = ctx->spec_stats[i];
             ctx->spec_stats[i] = 0;
         }
+    });
+}
+
+// Test hook: segments of the last parallel signal_std that were added term by term (the slow,
+// reference-literal path), per pass: out[0] mean pass, out[1] variance pass, out[2] segments per pass
+// (0: the last call used the single-thread kernel). Debug bit 32 forces the single-thread kernel.
+int semd_std_stats(semd_ctx* ctx, uint64_t* out) {
+    return guard([&] {
+        need_ctx(ctx);
+        out[0] = out[1] = out[2] = 0;
+        if (!ctx->std_ws.p || !ctx->std_last_n) return;
+        unsigned h[6];
+        ck(cudaMemcpy(h, ctx->std_ws.p, sizeof(h), cudaMemcpyDeviceToHost), "std stats");
+        out[0] = h[2];
+        out[1] = h[3];
+        out[2] = (uint64_t)((ctx->std_last_n + 511) / 512);
     });
 }
 

@@ -29,7 +29,8 @@ void launch_rng(const RngJob* jobs, int njobs, cudaStream_t st);
 void launch_rng_ensemble(uint64_t base, long long m0, int count, uint64_t* out, long long stride, long long n,
                          cudaStream_t st);
 void launch_box_muller(uint64_t* draws, long long n, double stdv, cudaStream_t st);
-void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st);
+size_t signal_std_workspace(long long n);  // 0: the signal is short, no workspace used
+void launch_signal_std(const double* x, long long n, double* out, double scale, cudaStream_t st, void* ws = nullptr);
 void launch_ensemble_finish(double* sums, int K, long long L, const double* x, double* residue, double inv,
                             cudaStream_t st);
 void launch_concatenate(const double* x, long long M, long long N, long long D, const double* a, double* out,
