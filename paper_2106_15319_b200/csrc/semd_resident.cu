@@ -45,6 +45,7 @@ __device__ __forceinline__ double2* sm_d2(int off) { return reinterpret_cast<dou
 __device__ __forceinline__ unsigned short* sm_u16(int off) { return reinterpret_cast<unsigned short*>(res_smem + off); }
 __device__ __forceinline__ unsigned char* sm_u8(int off) { return res_smem + off; }
 
+constexpr int kResRcpTab = 64;
 struct ResShared {
     double red[2][kResWarps];
     int scan4[4][kResWarps];  // res_detect's four-round block scan
@@ -52,7 +53,16 @@ struct ResShared {
     int job;
     bool moved[kResThreads];  // solve replay rounds: the chain's end changed
     int unc;  // a control word broadcast to the CTA
+    double rtab[kResRcpTab + 1];  // RN(1/h) of small integer knot spacings (the IEEE quotients themselves)
 };
+// 1/h of a knot spacing (an integer >= 1, except across the reference's non-monotone right mirror
+// knots): from the table when small, else the IEEE division
+__device__ __forceinline__ double res_rcp_h(const ResShared& sh, double h) {
+    return h >= 1.0 && h <= (double)kResRcpTab ? sh.rtab[(int)h] : 1.0 / h;
+}
+__device__ __forceinline__ void res_rcp_init(ResShared& sh) {  // visible after the next __syncthreads
+    for (int i = threadIdx.x + 1; i <= kResRcpTab; i += blockDim.x) sh.rtab[i] = 1.0 / (double)i;
+}
 
 __device__ __forceinline__ bool same_bits(double a, double b) {
     return __double_as_longlong(a) == __double_as_longlong(b);
@@ -325,14 +335,16 @@ __device__ __forceinline__ int res_solve(ResCtx& C, ResShared& sh, int& replays_
     const int s = 1 + c * CH, e = min(s + CH, N - 1);
     const int warm = (C.P->debug & 1) ? 2 : kResWarm;  // test hook: short warm-ups force the replays
     SEMD_ASSERT(!mine || (s >= 1 && s < e && e <= N - 1));
-    // ---- 1. rhs per row (parked in B.x, then moved to A.y once every y has been read)
-    for (int i = c + 1; i <= R; i += kResChains) {
-        const double2 p = A[i - 1], q = A[i], n = A[i + 1];
-        const double h0 = q.x - p.x, h1 = n.x - q.x;
-        B[i].x = 6.0 * ((n.y - q.y) / h1 - (q.y - p.y) / h0);
+    // ---- 1. rhs per row: the slope (y[i+1]-y[i])/h_i of every segment once (exactly rounded:
+    // div_rn with RN(1/h)), parked in B.x; then rhs_i = 6 (slope_i - slope_{i-1}) into A.y, once
+    // every y has been read
+    for (int i = c; i <= R; i += kResChains) {
+        const double2 q = A[i], n = A[i + 1];
+        const double h = n.x - q.x;
+        B[i].x = div_rn(n.y - q.y, h, res_rcp_h(sh, h));
     }
     __syncthreads();
-    for (int i = c + 1; i <= R; i += kResChains) A[i].y = B[i].x;
+    for (int i = c + 1; i <= R; i += kResChains) A[i].y = 6.0 * (B[i].x - B[i - 1].x);
     __syncthreads();
     SOLVE_SUB(8);
     // ---- 2. forward sweep
@@ -454,7 +466,7 @@ __device__ __forceinline__ int res_solve(ResCtx& C, ResShared& sh, int& replays_
     for (int v = c; v < N; v += kResChains) {
         const double x = A[v].x;
         const double h = v + 1 < N ? A[v + 1].x - x : 0.0;
-        B[v] = make_double2(v == 0 || v == N - 1 ? 0.0 : A[v].y, v + 1 < N ? 1.0 / h : 0.0);
+        B[v] = make_double2(v == 0 || v == N - 1 ? 0.0 : A[v].y, v + 1 < N ? res_rcp_h(sh, h) : 0.0);
     }
     __syncthreads();
     for (int v = c; v < N; v += kResChains) {
@@ -734,6 +746,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(ResArgs P) {
     __shared__ ResShared sh;
     ResCtx C;
     res_setup(C, P);
+    res_rcp_init(sh);
     while (true) {
         if (threadIdx.x == 0) sh.job = (int)atomicAdd(P.ticket, 1u);
         __syncthreads();
@@ -833,6 +846,8 @@ __global__ void __launch_bounds__(kResThreads, 1) k_res_ceemdan(ResArgs P, CeeAr
     __shared__ ResShared sh;
     ResCtx C;
     res_setup(C, P);
+    res_rcp_init(sh);
+    __syncthreads();
     CeeCtl* ctl = Q.ctl;
     const int L = C.L;
     const bool tracing = P.trace != nullptr;

@@ -4,7 +4,7 @@
 # resident engine's k_res_ceemdan (C3) and k_resident (C2).
 cd $GRAFT_REPO_ROOT
 NCU=/usr/local/cuda/bin/ncu
-O=gpurun_out/r02b
+O=gpurun_out/${OUT:-r02c}
 mkdir -p $O
 timeout 1200 python bench.py > $O/bench_c5_n1.json 2> $O/bench_c5.err; echo "bench c5 rc=$?"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_c5_reference.json 2> $O/bench_c5_ref.err; echo "ref c5 rc=$?"
@@ -18,7 +18,7 @@ python tests/probes/ncu_summary.py $O/launches_c5.csv > $O/launches_c5_summary.t
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv \
     python bench.py --config c3 --steps 1 --warmup 0 --no-cpu > $O/ncu_launches_c3.log 2>&1
 python tests/probes/ncu_summary.py $O/launches_c3.csv > $O/launches_c3_summary.txt 2>&1
-for spec in "c5 k_eval 12 eval_c5" "c5 k_solve 5 solve_c5" "c5 k_final 3 final_c5" "c3 k_res_ceemdan 0 resident_c3" "c2 k_resident 0 resident_c2"; do
+for spec in "c5 k_eval 12 eval_c5" "c5 k_solve 2 solve_c5" "c5 k_final 4 final_c5" "c5 k_eval 13 evalspec_c5" "c3 k_res_ceemdan 0 resident_c3" "c2 k_resident 0 resident_c2"; do
   set -- $spec
   timeout 900 $NCU --set full --import-source on --clock-control none -k regex:$2 -s $3 -c 1 \
       -o $O/$4 -f python bench.py --config $1 --steps 1 --warmup 0 --no-cpu > $O/ncu_$4.log 2>&1
