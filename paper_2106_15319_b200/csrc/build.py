@@ -35,26 +35,38 @@ def build_checked(verbose: bool = False) -> str:
     return build(force=True, verbose=verbose, checked=True)
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+TOL = os.path.join(PKG, "libsemd_b200_tol.so")
+
+
+def build_tol(verbose: bool = False) -> str:
+    """EXPERIMENT ONLY (tests/probes/tol_experiment.py): the engine with a
+    tolerance-mode spline (-DSEMD_TOL_SPLINE: reciprocal multiplications and FMAs instead of the
+    correctly rounded divisions). Not loaded by the package; select it with SEMD_LIB."""
+    return build(force=True, verbose=verbose, variant="tol")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False, variant: str = "") -> str:
     if not force and not needs_build():
         return LIB
     objs = []
+    tol = variant == "tol"
     for src in SRCS:
-        obj = os.path.join(HERE, src.replace(".cu", "_chk.o" if checked else ".o"))
-        cmd = [NVCC, *FLAGS, *(["-DSEMD_CHECK"] if checked else []), "-c", os.path.join(HERE, src), "-o", obj]
+        obj = os.path.join(HERE, src.replace(".cu", "_chk.o" if checked else ("_tol.o" if tol else ".o")))
+        cmd = [NVCC, *FLAGS, *(["-DSEMD_CHECK"] if checked else []), *(["-DSEMD_TOL_SPLINE"] if tol else []), "-c",
+               os.path.join(HERE, src), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
         objs.append(obj)
-    out = CHECKED if checked else LIB
+    out = CHECKED if checked else (TOL if tol else LIB)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out + ".tmp", *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(out + ".tmp", out)
-    if not checked:
+    if not checked and not tol:
         build_cli(verbose)
     return out
 
@@ -79,5 +91,7 @@ def build_cli(verbose: bool = False) -> str:
 if __name__ == "__main__":
     if "--checked" in sys.argv:
         print(build_checked(verbose=True))
+    elif "--tol" in sys.argv:
+        print(build_tol(verbose=True))
     else:
         print(build(force="--force" in sys.argv, verbose=True))

@@ -99,10 +99,22 @@ __device__ __forceinline__ double spline_eval_ref(double x0, double x1, double y
 // The same value with the divisions done by div_rn (rh = RN(1/h), hh = h*h).
 __device__ __forceinline__ double spline_eval_fast(double x0, double x1, double y0, double y1, double m0, double m1,
                                                    double h, double rh, double hh, double tt) {
+#ifdef SEMD_TOL_SPLINE
+    // EXPERIMENT (not the product arithmetic): the same spline with reciprocal multiplications and
+    // fused multiply-adds, a few ulp from the reference value (16 instead of 27 fp64 operations).
+    const double a = (x1 - tt) * rh;
+    const double b = (tt - x0) * rh;
+    const double ca = fma(a * a, a, -a);
+    const double cb = fma(b * b, b, -b);
+    const double p = fma(ca, m0, cb * m1);
+    const double k6 = (h * h) * (1.0 / 6.0);
+    return fma(p, k6, fma(a, y0, b * y1));
+#else
     const double a = div_rn(x1 - tt, h, rh);
     const double b = div_rn(tt - x0, h, rh);
     const double p = ((a * a * a - a) * m0 + (b * b * b - b) * m1) * hh;
     return a * y0 + b * y1 + div_rn(p, 6.0, 1.0 / 6.0);
+#endif
 }
 
 // The segment table of one envelope (written by k_solve), in two planes of 16-byte rows:
