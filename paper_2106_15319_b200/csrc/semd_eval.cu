@@ -434,17 +434,17 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
         }
     }
     // detection window t0-1 .. t0+2 needs values t0-2 .. t0+3
+    // One rotation by a lane serves both the window's left values (lane l takes lane l-1's last two
+    // values) and the carry across tiles: lane 31 sends its last two values of the PREVIOUS tile
+    // (c2, c1: each lane keeps its own), which lane 0 -- the only reader of lane 31 -- needs.
     double w[kSpt + 2];
-    w[0] = __shfl_up_sync(0xffffffffu, nv[kSpt - 2], 1);
-    w[1] = __shfl_up_sync(0xffffffffu, nv[kSpt - 1], 1);
-    if (lane == 0) {
-        w[0] = c2;
-        w[1] = c1;
-    }
+    const int from = (lane + 31) & 31;
+    w[0] = __shfl_sync(0xffffffffu, lane == 31 ? c2 : nv[kSpt - 2], from);
+    w[1] = __shfl_sync(0xffffffffu, lane == 31 ? c1 : nv[kSpt - 1], from);
 #pragma unroll
     for (int k = 0; k < kSpt; ++k) w[k + 2] = nv[k];
-    c2 = __shfl_sync(0xffffffffu, nv[kSpt - 2], 31);  // carried into the next tile of the strip
-    c1 = __shfl_sync(0xffffffffu, nv[kSpt - 1], 31);
+    c2 = nv[kSpt - 2];  // (lane 31's: the values at base+T-2, base+T-1 for the next tile of the strip)
+    c1 = nv[kSpt - 1];
 
     // extrema flags branch-free (find_extrema, emd.cpp:16-33); samples equal to a neighbour
     // take the reference's plateau rule in a warp-uniform slow path
