@@ -328,7 +328,11 @@ __device__ __forceinline__ void eval_tile(const Arena& A, const Strip& S, int i,
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
                     const double2* R = s ? R1 : R0;
-                    const int qq = smem_search(R, qmax[s], tt);
+                    // rows 0 and 1 are the two knots before the tile's detection window [base-1, ..):
+                    // x_1 <= base-2 and x_2 >= base-1, so the last row with x < t is row 1, or row 0
+                    // when t = base-2 sits on knot 1 (what the search over the staged rows returns)
+                    const int qq = R[1].x < tt ? 1 : 0;
+                    SEMD_ASSERT(qq == smem_search(R, qmax[s], tt));
                     const double2 a0 = R[qq], b0 = R[nab + qq], a1 = R[qq + 1];
                     const double m1 = R[nab + qq + 1].x;
                     const double h = a1.x - a0.x;
