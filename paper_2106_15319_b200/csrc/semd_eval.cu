@@ -226,15 +226,15 @@ __device__ __forceinline__ Strip strip_from(const Arena& A, unsigned item, unsig
 // Tile j's extrema are those of window [base-1, base+T-1); its samples [base-2, base+T) need
 // table rows [toff[j], toff[j+1]+2], so the group needs rows [toff[j_i], toff[j_i+g]+2].
 __device__ __forceinline__ int group_tiles(const Strip& S, int i) {
+    // lane l holds toff of tile j0 + min(l, nt): it rates the group of c = l - i tiles i .. l-1
+    // (bytes grow with c, so the largest fitting c is the highest lane that fits; c = 1 always does)
+    const int lane = threadIdx.x & 31;
     const int lo0 = __shfl_sync(0xffffffffu, S.to[0], i), lo1 = __shfl_sync(0xffffffffu, S.to[1], i);
-    int g = 1;
-#pragma unroll
-    for (int c = 2; c <= kGroupMax; ++c) {
-        const int e = min(i + c, S.nt);  // lanes >= nt hold toff of the strip's end
-        const int rows = __shfl_sync(0xffffffffu, S.to[0], e) - lo0 + __shfl_sync(0xffffffffu, S.to[1], e) - lo1 + 6;
-        if (i + c <= S.nt && group_bytes(c, rows, S.mode == EM_SPEC) <= kStageBytes) g = c;
-    }
-    return g;
+    const int c = lane - i;
+    const int rows = S.to[0] - lo0 + S.to[1] - lo1 + 6;
+    const bool fit = c >= 1 && c <= kGroupMax && lane <= S.nt &&
+                     (c == 1 || group_bytes(c, rows, S.mode == EM_SPEC) <= kStageBytes);
+    return 31 - __clz((int)__ballot_sync(0xffffffffu, fit)) - i;
 }
 
 // Issue group (i, g)'s copies: samples, detection words, both sides' rows (lane 0 arms the barrier).
