@@ -237,13 +237,20 @@ __device__ __forceinline__ int group_tiles(const Strip& S, int i) {
     return 31 - __clz((int)__ballot_sync(0xffffffffu, fit)) - i;
 }
 
+// One lane of the converged warp (elect.sync: the compiler then knows the region is single-lane).
+__device__ __forceinline__ bool elect_one() {
+    unsigned pred;
+    asm volatile("{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
+    return pred != 0;
+}
+
 // Issue group (i, g)'s copies: samples, detection words, both sides' rows (lane 0 arms the barrier).
 __device__ __forceinline__ void issue_group(const Strip& S, int i, int g, WarpStage& st, int bofs,
                                             const CopySrc& cs) {
     const int lo0 = __shfl_sync(0xffffffffu, S.to[0], i), lo1 = __shfl_sync(0xffffffffu, S.to[1], i);
     const int n0 = __shfl_sync(0xffffffffu, S.to[0], i + g) + 3 - lo0;
     const int n1 = __shfl_sync(0xffffffffu, S.to[1], i + g) + 3 - lo1;
-    if ((threadIdx.x & 31) != 0) return;
+    if (!elect_one()) return;  // one lane issues (every operand is warp-uniform)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
     const int base = (S.j0 + i) * kEvalTile;
     const int e0 = base > 0 ? base - 2 : 0;  // 16-byte aligned; Lp = whole tiles
@@ -270,7 +277,7 @@ constexpr int kDetChunk = 6;
 static_assert((kDetChunk * kEvalTile + 2) * 8 <= kStageBytes, "a DETECT chunk fits one stage");
 __device__ __forceinline__ double* stage_flat(WarpStage& st) { return st.flat; }
 __device__ __forceinline__ void issue_chunk(const Strip& S, int c, WarpStage& st, const CopySrc& cs) {
-    if ((threadIdx.x & 31) != 0) return;
+    if (!elect_one()) return;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
     const int base = (S.j0 + c * kDetChunk) * kEvalTile;
     const int end = (S.j0 + min(S.nt, (c + 1) * kDetChunk)) * kEvalTile;  // <= Lp (whole tiles)
