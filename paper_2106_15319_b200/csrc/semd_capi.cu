@@ -189,7 +189,7 @@ struct semd_ctx {
     std::vector<Slot> h_slots;
     std::vector<TraceRec> h_trace;
     // scratch
-    DBuf in_x, in_y, noise, scratch, scratch2, scalar, rng_jobs, std_ws;
+    DBuf in_x, in_y, noise, scratch, scratch2, scalar, rng_jobs, std_ws, spec_hist;
     cudaEvent_t ev[16]{};
     cudaStream_t rng_stream = nullptr;  // noise for the next wave is generated here, overlapping the sift
     cudaEvent_t noise_ready[2]{};
@@ -297,6 +297,11 @@ struct semd_ctx {
         A.debug = debug_flags;
         prof.alloc(16 * 8);
         A.prof = prof.as<unsigned long long>();
+        if (!spec_hist.p) {  // once per context: the statistics outlive reconfigurations
+            spec_hist.alloc((size_t)semd::dev::kSpecK * semd::dev::kSpecS * 4);
+            ck(cudaMemsetAsync(spec_hist.p, 0, spec_hist.bytes, stream), "memset spec_hist");
+        }
+        A.spec_hist = spec_hist.as<int>();
         ck(cudaMemsetAsync(toff.p, 0, toff.bytes, stream), "memset toff");
         ck(cudaMemsetAsync(tbase.p, 0, tbase.bytes, stream), "memset tbase");
         ck(cudaMemsetAsync(sb.p, 0, sb.bytes, stream), "memset sb");
@@ -955,6 +960,7 @@ struct semd_ctx {
             configure(n, G, kcap, tr ? trace_cap_for(tr) : 0);
             A.sd_threshold = cfg.sd_threshold;
             A.max_sift_iters = cfg.max_sift_iters;
+            semd::dev::launch_spec_decay(A.spec_hist, stream);  // the speculation policy's memory fades per call
             noise.alloc((size_t)2 * G * Ls * 8);  // double-buffered: wave i+1's noise is made during wave i
             fill_sums(kcap, 0.0);
             h_trace.clear();

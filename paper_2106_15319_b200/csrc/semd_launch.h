@@ -17,6 +17,7 @@ struct RngJob {
 
 size_t eval_smem_bytes();
 cudaError_t eval_setup();
+void launch_spec_decay(int* spec_hist, cudaStream_t st);  // halve the speculation statistics
 void launch_eval(const Arena& A, int sms, cudaStream_t st);
 size_t solve_smem_bytes();
 cudaError_t launch_setup();

@@ -171,9 +171,10 @@ __device__ __noinline__ void sd_fix_uncertain(const Arena& A, int ne) {
 }
 
 // Is sift number `sift` (1-based) of the slot's current IMF likely its last? Then it runs as a
-// speculative last sift (ST_PRIMED). The stop statistics of this run's earlier IMFs with the same
-// index decide (speculate when at least half of those that reached this sift stopped there);
-// without them, from the second sift on. Any choice gives the same results: speculation only
+// speculative last sift (ST_PRIMED). The stop statistics of earlier IMFs with the same index decide
+// (speculate when at least half of those that reached this sift stopped there) -- of earlier waves
+// and earlier calls on this context (A.spec_hist; the slots of one wave decide together, so a
+// wave cannot learn from itself); without them, from the second sift on. Any choice gives the same results: speculation only
 // changes which detection runs when.
 __device__ int spec_policy(const Arena& A, const Slot& S, int sift) {
     if (A.debug & 8) return 0;
@@ -181,7 +182,7 @@ __device__ int spec_policy(const Arena& A, const Slot& S, int sift) {
     if (S.kmax > 0 && S.k + 1 >= S.kmax) return 0;
     if (A.debug & 16) return 1;
     if (sift >= A.max_sift_iters) return 1;  // the iteration cap stops it
-    const int* h = A.ctrl->spec_hist[min(S.k, kSpecK - 1)];
+    const int* h = A.spec_hist + min(S.k, kSpecK - 1) * kSpecS;
     const int j = min(sift, kSpecS - 1);
     int reach = 0;
     for (int q = j; q < kSpecS; ++q) reach += *(volatile const int*)(h + q);
@@ -189,7 +190,7 @@ __device__ int spec_policy(const Arena& A, const Slot& S, int sift) {
     return 2 * *(volatile const int*)(h + j) >= reach;
 }
 __device__ __forceinline__ void spec_count_stop(const Arena& A, const Slot& S) {
-    atomicAdd(&A.ctrl->spec_hist[min(S.k, kSpecK - 1)][min(S.iter, kSpecS - 1)], 1);
+    atomicAdd(A.spec_hist + min(S.k, kSpecK - 1) * kSpecS + min(S.iter, kSpecS - 1), 1);
 }
 
 // extract_imf's control flow (emd.cpp:131-151) for one slot after its eval
@@ -1497,6 +1498,17 @@ size_t solve_smem_bytes() {
     const size_t chunked = (size_t)5 * kSolvePadWin * sizeof(double) + kSolveIdxBuf * sizeof(int) + 8;
     const size_t seq = (size_t)4 * (kSolveSeqMax + 4) * sizeof(double);
     return chunked > seq ? chunked : seq;
+}
+
+// The speculation statistics fade: halved at the start of every decomposition, so a context
+// follows a change of input within a call or two.
+__global__ void k_spec_decay(int* h) {
+    const int i = threadIdx.x;
+    if (i < kSpecK * kSpecS) h[i] >>= 1;
+}
+void launch_spec_decay(int* h, cudaStream_t st) {
+    k_spec_decay<<<1, kSpecK * kSpecS, 0, st>>>(h);
+    count_launches(1);
 }
 
 cudaError_t launch_setup() {

@@ -156,7 +156,6 @@ struct Ctrl {
     int sd_rechecks;  // SD stop tests redone with the reference's sequential sums (uncertified decisions)
     int spec_pass, spec_hits, spec_misses;  // speculative last sifts: run, stopped, continued
     int n_eval_pass;  // eval_list[0, n_eval_pass): slots with an eval pass (ST_PRIMED slots follow)
-    int spec_hist[kSpecK][kSpecS];  // IMFs of this run that stopped after s sifts, per IMF index
     unsigned long long ev_t0;  // k_eval span of this step (globaltimer): min CTA start, max CTA end
     unsigned long long ev_t1;
     unsigned long long ev_ns;  // accumulated k_eval spans of this run (timing mode)
@@ -244,6 +243,8 @@ struct Arena {
                       // last sifts; bit 4 every sift speculative
                       // bit 1: accumulate k_solve per-phase clock cycles into prof[]
     unsigned long long* prof;  // [16]
+    int* spec_hist;   // [kSpecK][kSpecS] IMFs that stopped after s sifts, per IMF index: the speculation policy's
+                      // memory, kept across waves and calls of a context (halved at each decomposition's start)
     int* status_host; // mapped pinned: [0] active slots after this step, [1] step counter
 };
 
