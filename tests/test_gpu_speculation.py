@@ -93,3 +93,26 @@ def test_ceemdan_and_plateaus_speculation(se):
     r = run_modes(se, y, "emd")
     same(r["off"], r["default"])
     same(r["off"], r["every"])
+
+
+def test_speculation_statistics_persist_across_calls(se):
+    """The policy's stop statistics live in the context (across waves and calls, halved per
+    decomposition): a repeated decomposition mispredicts no more often than the first one, and its
+    results do not depend on what the context has seen before."""
+    x = rng_signal(9090, 60000)
+    y = rng_signal(9191, 45000) * 3.0 + np.sin(np.arange(45000) * 0.002)
+    c = se.context()
+    c.set_engine("lockstep")
+    try:
+        spec_stats(c)
+        a = se.decompose_full(x, "eemd", nr=6, trace_cap=400000)
+        first = spec_stats(c)
+        se.decompose_full(y, "eemd", nr=6)  # another input in between
+        spec_stats(c)
+        b = se.decompose_full(x, "eemd", nr=6, trace_cap=400000)
+        again = spec_stats(c)
+    finally:
+        c.set_engine("auto")
+    same(a, b)
+    assert first[0] > 0 and again[0] > 0
+    assert again[2] * first[0] <= first[2] * again[0] + again[0]  # miss rate did not grow (one miss of slack)
